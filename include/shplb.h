@@ -1,0 +1,210 @@
+/*
+ * shplb.h — C ABI of the B200-native S-HPLB sparse-attention hot path.
+ *
+ * This is the drop-in boundary. Each entry point replaces one function of the
+ * reference operator API (C++ namespace `headbal`, /root/reference/proj); the
+ * reference interface it stands in for is cited on every declaration. Plain
+ * pointers and sizes only: no C++ or torch types. Device pointers are caller-
+ * owned; the opaque shplb_ctx owns all device workspace (one per device/rank).
+ * Device calls are asynchronous on the caller's CUDA stream (passed as void*,
+ * a cudaStream_t; NULL = legacy default stream). There is no CPU fallback:
+ * every attention entry point runs the sm_100a kernels or fails.
+ *
+ * Errors: the reference throws (std::invalid_argument for shapes, budgets and
+ * infeasible totals; std::runtime_error for I/O; std::logic_error for the
+ * unreachable). Here every function returns a shplb_status and the message
+ * text — identical to the reference's where the reference has one — is
+ * available from shplb_last_error() (thread-local) until the next call.
+ */
+#ifndef SHPLB_H_
+#define SHPLB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SHPLB_OK = 0,
+    SHPLB_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+    SHPLB_RUNTIME_ERROR = 2,    /* reference: std::runtime_error    */
+    SHPLB_LOGIC_ERROR = 3,      /* reference: std::logic_error      */
+    SHPLB_CUDA_ERROR = 4,       /* CUDA runtime / driver failure    */
+    SHPLB_NOT_SUPPORTED = 5     /* shape or policy the kernels do not implement */
+} shplb_status;
+
+/* Message of the last failed call on this thread ("" after success). */
+const char* shplb_last_error(void);
+/* Library version string, e.g. "shplb-b200 0.1.0 sm_100a". */
+const char* shplb_version(void);
+
+/* ======================================================================
+ * Per-head budget table   (reference: proj/include/headbal/allocator.hpp)
+ * Budgets are in TOKENS, like the reference's BudgetAllocation::budgets.
+ * ====================================================================== */
+
+/* uniform_allocate(num_heads, total, floor, context_length)
+ * (allocator.hpp:46-47, allocator.cpp:72-95): b_h = floor(B/N), remainder one
+ * token each to the lowest-indexed heads. B must lie in [N*floor, N*n_k]. */
+int shplb_uniform_allocate(int64_t num_heads, int64_t total, int64_t floor,
+                           int64_t context_length, int64_t* budgets_out);
+
+typedef struct {
+    int64_t transfers;            /* committed transfers (BudgetAllocation::transfers.size()) */
+    int32_t hit_iteration_cap;    /* BudgetAllocation::hit_iteration_cap */
+    int64_t off_grid_evaluations; /* BudgetAllocation::off_grid_evaluations */
+    double min_recovery_start;    /* min_recovery_trace.front() */
+    double min_recovery_end;      /* min_recovery_trace.back()  */
+} shplb_maxmin_diag;
+
+/* maxmin_allocate(curves, total, AllocatorConfig{quantum, floor, max_iterations})
+ * (allocator.hpp:53-54, allocator.cpp:97-186). The recovery curves (one per
+ * head, profiler.hpp:29-41) are flattened: head h owns points
+ * [curve_offsets[h], curve_offsets[h+1]) of curve_budgets / curve_recovery.
+ * max_iterations = 0 means the reference default 10*N*n_k/quantum. diag may
+ * be NULL. Bit-exact with the reference. */
+int shplb_maxmin_allocate(int32_t num_heads, int64_t context_length,
+                          const int64_t* curve_offsets, const int64_t* curve_budgets,
+                          const double* curve_recovery, int64_t total, int64_t quantum,
+                          int64_t floor, int64_t max_iterations, int64_t* budgets_out,
+                          shplb_maxmin_diag* diag);
+
+/* recovery_at (profiler.cpp:55-62): recovery at the largest sampled budget
+ * <= budget, 0 below the first sample. */
+int shplb_recovery_at(int64_t n_points, const int64_t* curve_budgets,
+                      const double* curve_recovery, int64_t budget, double* recovery_out);
+
+/* build_profiles + recovery_ratio for PerQueryTopK (profiler.cpp:157-196,
+ * attention.cpp:151-184), restated in host C++ (fp64, OpenMP over heads x
+ * rows). Offline budget-table input, not the hot path. q_rows: bf16
+ * [num_q_heads][n_rows][d] calibration query rows, k: bf16
+ * [num_kv_heads][n_k][d] (host memory). The rows attend to all n_k keys
+ * (the reference profiles without the causal mask, commands.cpp:420-423).
+ * grid: strictly increasing budgets ending at n_k. recovery_out:
+ * [num_q_heads][n_grid]. GQA: q head h uses kv head h / (Hq/Hkv). */
+int shplb_profile_curves_host(const uint16_t* q_rows, const uint16_t* k, int32_t num_q_heads,
+                              int32_t num_kv_heads, int64_t n_rows, int64_t n_k, int32_t d,
+                              const int64_t* grid, int64_t n_grid, double* recovery_out);
+
+/* ======================================================================
+ * Head -> GPU plan   (reference: proj/include/headbal/partitioner.hpp)
+ * ====================================================================== */
+
+/* naive_assign(budgets, devices, Contiguous|RoundRobin) (partitioner.hpp:36-37,
+ * partitioner.cpp:130-162). Requires devices <= num_heads. */
+int shplb_plan_naive(const int64_t* budgets, int32_t num_heads, int32_t devices,
+                     int32_t round_robin, int32_t* device_of_head);
+
+/* greedy_assign(budgets, devices) — LPT (partitioner.hpp:42, partitioner.cpp:164-183).
+ * Bit-exact with the reference (ties: lower head index first, lower device). */
+int shplb_plan_greedy(const int64_t* budgets, int32_t num_heads, int32_t devices,
+                      int32_t* device_of_head);
+
+/* imbalance(budgets, assignment) (partitioner.hpp:50, partitioner.cpp:236-266):
+ * loads[devices], total, I = max*D/total, argmax device. */
+int shplb_imbalance(const int64_t* budgets, int32_t num_heads, const int32_t* device_of_head,
+                    int32_t devices, int64_t* loads_out, int64_t* total_out,
+                    double* imbalance_out, int32_t* argmax_out);
+
+/* ======================================================================
+ * Barrier metric   (reference: proj/include/headbal/simulator.hpp)
+ * ====================================================================== */
+
+/* simulate(report, CostModel{alpha, beta}) (simulator.hpp:28, simulator.cpp:28-47):
+ * t_d = alpha + beta*L_d, T = max t_d, bubble = 1 - mean/T. */
+int shplb_simulate(const int64_t* loads, int32_t devices, double alpha, double beta,
+                   double* latency_out, double* barrier_out, double* bubble_out);
+
+/* The same barrier / bubble definitions on MEASURED per-rank latencies
+ * (simulator.cpp:40-44) — what replaces the affine model on hardware. */
+int shplb_barrier(const double* device_latency, int32_t devices, double* barrier_out,
+                  double* bubble_out);
+
+/* ======================================================================
+ * Block-sparse attention on sm_100a  (reference: proj/include/headbal/attention.hpp)
+ * ====================================================================== */
+
+typedef struct shplb_ctx shplb_ctx;
+
+/* One context per CUDA device (rank). Owns the device workspace. */
+int shplb_ctx_create(int device, shplb_ctx** ctx_out);
+int shplb_ctx_destroy(shplb_ctx* ctx);
+/* Number of kernel launches the context issued since creation (all kinds). */
+int64_t shplb_ctx_launch_count(const shplb_ctx* ctx);
+
+enum { SHPLB_BLOCK_TOPK = 0 }; /* selection kind: per (head, query block) top-k key blocks */
+
+/* One attention layer. q: bf16 [num_q_heads][seq_len][head_dim],
+ * k/v: bf16 [num_kv_heads][seq_len][head_dim], out: bf16 like q; all dense,
+ * 16-byte aligned device pointers. Prefill: n_q = n_k = seq_len. GQA: q head
+ * h reads kv head kv_head_of_q[h] (default h / (num_q_heads/num_kv_heads)). */
+typedef struct {
+    int32_t num_q_heads;
+    int32_t num_kv_heads;
+    int64_t seq_len;
+    int32_t head_dim;  /* 128 */
+    int32_t block_q;   /* query block (pooling and FA tile rows): 128 */
+    int32_t block_k;   /* key block (pooling and FA tile cols): 128 */
+    int32_t causal;    /* top-left causal mask (attention.cpp:28-30) */
+    int32_t kind;      /* SHPLB_BLOCK_TOPK */
+    int32_t validate;  /* 1: scan q/k/v for NaN/Inf first (workload.cpp:56-58); synchronises */
+    /* Optional host int32 [num_q_heads]: kv head read by each q head. NULL =
+     * standard GQA grouping h / (num_q_heads/num_kv_heads). A rank under
+     * head parallelism holds an arbitrary subset of q heads and only the kv
+     * heads they need, so its local map is not the contiguous grouping. */
+    const int32_t* kv_head_of_q;
+} shplb_layer_shape;
+
+/* Kernel 1 — block-importance estimator. Mean-pools q/k blocks (fp32,
+ * fixed summation order) and scores pooled q.k * (1/sqrt(d)).
+ * scores_out: fp32 device [num_q_heads][ceil(n/bq)][ceil(n/bk)], causally
+ * invisible blocks = -inf. (Exposed for parity; the layer call fuses it.) */
+int shplb_block_scores(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
+                       const void* k, float* scores_out, void* stream);
+
+/* Kernel 2 — per-head top-k block selector over precomputed scores. Keeps
+ * min(k_h, visible blocks) per (head, query block) under (score desc, block
+ * index asc), emitted ascending (attention.cpp:53-64). k_blocks: host int64
+ * [num_q_heads]. idx_out: int32 device [num_q_heads][nqb][kmax] (tail -1),
+ * cnt_out: int32 device [num_q_heads][nqb]. */
+int shplb_select_blocks(shplb_ctx* ctx, const shplb_layer_shape* shape, const float* scores,
+                        const int64_t* k_blocks, int64_t kmax, int32_t* idx_out,
+                        int32_t* cnt_out, void* stream);
+
+/* Kernel 3 — block-sparse FlashAttention prefill over given selections
+ * (tcgen05 MMA, TMEM accumulators, TMA-staged K/V tiles, online softmax).
+ * Output row i of head h is softmax-weighted V over the tokens of the
+ * selected key blocks that are causally visible to i (attention.cpp:35-49);
+ * a row with no such token is zero. */
+int shplb_block_sparse_attention(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
+                                 const void* k, const void* v, const int32_t* idx,
+                                 const int32_t* cnt, int64_t kmax, void* out, void* stream);
+
+/* The whole hot path for one layer: sparse_attention for every head with its
+ * own budget (the per-head loop of run_skyline, commands.cpp:464-470, which
+ * calls sparse_attention(head, {policy, budgets[h]}), attention.cpp:116-149).
+ * budgets_tokens: host int64 [num_q_heads], each in [1, seq_len]
+ * (check_budget, attention.cpp:75-80); head h keeps ceil(b_h/block_k) key
+ * blocks per query block. Runs kernel 1+2 fused, then kernel 3, on stream. */
+int shplb_sparse_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
+                                 const void* k, const void* v,
+                                 const int64_t* budgets_tokens, void* out, void* stream);
+
+/* Device pointers of the selection made by the last shplb_sparse_attention_layer
+ * call on this context (valid until the next call): idx [Hq][nqb][kmax],
+ * cnt [Hq][nqb]. */
+int shplb_last_selection(const shplb_ctx* ctx, const int32_t** idx, const int32_t** cnt,
+                         int64_t* kmax);
+
+/* Algorithmic work of one layer call, for roofline accounting:
+ * selected (head, q-block, k-block) tiles, and the FLOPs 4*d*bq*bk*tiles. */
+int shplb_layer_work(const shplb_layer_shape* shape, const int64_t* budgets_tokens,
+                     int64_t* selected_tiles_out, double* flops_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SHPLB_H_ */

@@ -1,0 +1,423 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes access to the parity oracle.
+
+Two libraries, both built by ``oracle/Makefile``:
+
+* ``oracle/build/liboracle.so`` — our plain-C restatement of the reference's
+  sparse-attention algorithm at block granularity (``shplb_oracle.c``; every
+  function cites the reference file:line it follows).
+* ``oracle/_ref/libheadbal_ref.so`` — the UNMODIFIED reference library
+  (``/root/reference/proj/src``) behind an extern "C" shim
+  (``oracle/ref_shim.cpp``). Used to pin the restatement and, in bench.py, as
+  the reference CPU arm.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu-baseline /
+``--impl reference`` legs may import this module. The product package
+(``paper_2603_10353_b200``) never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "build", "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libheadbal_ref.so")
+
+_i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+_u16p = np.ctypeslib.ndpointer(np.uint16, flags="C_CONTIGUOUS")
+
+_orc = None
+_ref = None
+
+
+def build() -> None:
+    """Build the oracle (and the reference when /root/reference is present)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _load_oracle():
+    global _orc
+    if _orc is None:
+        if not os.path.exists(ORACLE_SO):
+            build()
+        L = C.CDLL(ORACLE_SO)
+        L.orc_pool_blocks.argtypes = [_u16p, C.c_int64, C.c_int32, C.c_int32, _f32p]
+        L.orc_score_scale.argtypes = [C.c_int32]
+        L.orc_score_scale.restype = C.c_float
+        L.orc_visible_blocks.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int]
+        L.orc_visible_blocks.restype = C.c_int64
+        L.orc_block_scores.argtypes = [_f32p, _f32p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                       C.c_int, _f32p]
+        L.orc_score_rows.argtypes = [_f32p, _f32p, C.c_int64, C.c_int64, C.c_int32, _f32p]
+        L.orc_select_topk.argtypes =[_f32p, C.c_int64, C.c_int32, C.c_int32, C.c_int, C.c_int64,
+                                      C.c_int64, _i32p, _i32p]
+        L.orc_topk_row.argtypes = [_f64p, C.c_int64, C.c_int64, _i64p]
+        L.orc_block_sparse_attention.argtypes = [_u16p, _u16p, _u16p, C.c_int64, C.c_int32,
+                                                 C.c_int32, C.c_int32, C.c_int, _i32p, _i32p,
+                                                 C.c_int64, _f64p]
+        L.orc_layer.argtypes = [_u16p, _u16p, _u16p, C.c_int32, C.c_int32, C.c_int64, C.c_int32,
+                                C.c_int32, C.c_int32, C.c_int, _i64p, C.c_int64, _f32p, _i32p,
+                                _i32p, C.c_void_p]
+        L.orc_recovery_at.argtypes = [_i64p, _f64p, C.c_int64, C.c_int64]
+        L.orc_recovery_at.restype = C.c_double
+        L.orc_uniform_allocate.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, _i64p]
+        L.orc_maxmin_allocate.argtypes = [C.c_int32, C.c_int64, _i64p, _i64p, _f64p, C.c_int64,
+                                          C.c_int64, C.c_int64, C.c_int64, _i64p,
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+        L.orc_naive_assign.argtypes = [C.c_int32, C.c_int32, C.c_int, _i32p]
+        L.orc_greedy_assign.argtypes = [_i64p, C.c_int32, C.c_int32, _i32p]
+        L.orc_imbalance.argtypes = [_i64p, C.c_int32, _i32p, C.c_int32, _i64p,
+                                    C.POINTER(C.c_int32)]
+        L.orc_imbalance.restype = C.c_double
+        L.orc_barrier.argtypes = [_f64p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        _orc = L
+    return _orc
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def _load_ref():
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_SO):
+            raise FileNotFoundError(
+                f"{REF_SO} missing: build it here with `make -C oracle` (needs /root/reference)")
+        L = C.CDLL(REF_SO)
+        L.ref_last_error.restype = C.c_char_p
+        attn = [_f64p, _f64p, _f64p, C.c_int64, C.c_int64, C.c_int64, C.c_int64]
+        L.ref_dense_attention.argtypes = attn + [C.c_int, C.c_void_p, _f64p]
+        L.ref_sparse_attention.argtypes = attn + [C.c_int, C.c_int64, C.c_int, _f64p]
+        L.ref_serial_sparse_attention.argtypes = attn + [C.c_int, C.c_int64, C.c_int, _f64p]
+        L.ref_recovery_ratio.argtypes = [_f64p, C.c_int64, C.c_int64, C.c_int64, C.c_int,
+                                         C.POINTER(C.c_double)]
+        L.ref_build_profiles.argtypes = [_f64p, _f64p, _f64p, C.c_int32, C.c_int64, C.c_int64,
+                                         C.c_int64, _i64p, C.c_int64, C.c_int, C.c_int, _f64p]
+        L.ref_uniform_allocate.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, _i64p]
+        L.ref_maxmin_allocate.argtypes = [C.c_int32, C.c_int64, _i64p, _i64p, _f64p, C.c_int64,
+                                          C.c_int64, C.c_int64, C.c_int64, _i64p,
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                          C.POINTER(C.c_int64)]
+        L.ref_budget_for_recovery.argtypes = [C.c_int64, C.c_int64, _i64p, _f64p, C.c_double,
+                                              C.POINTER(C.c_int64)]
+        L.ref_naive_assign.argtypes = [_i64p, C.c_int32, C.c_int32, C.c_int, _i32p]
+        L.ref_greedy_assign.argtypes = [_i64p, C.c_int32, C.c_int32, _i32p]
+        L.ref_optimal_assign.argtypes = [_i64p, C.c_int32, C.c_int32, _i32p]
+        L.ref_imbalance.argtypes = [_i64p, C.c_int32, _i32p, C.c_int32, _i64p,
+                                    C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_int32)]
+        L.ref_simulate.argtypes = [_i64p, C.c_int32, C.c_double, C.c_double, _f64p,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.ref_max_threads.restype = C.c_int
+        _ref = L
+    return _ref
+
+
+class ReferenceError(Exception):
+    """A C++ exception raised inside the reference library."""
+
+
+def _ref_check(rc: int) -> None:
+    if rc != 0:
+        raise ReferenceError(_load_ref().ref_last_error().decode())
+
+
+# --------------------------------------------------------------------------
+# bf16 helpers (numpy has no bf16: we carry raw uint16 bit patterns)
+# --------------------------------------------------------------------------
+
+def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even fp32 -> bf16 bit pattern (what torch's .bfloat16() does)."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    rounding = ((u >> 16) & 1) + np.uint32(0x7FFF)
+    return ((u + rounding) >> 16).astype(np.uint16)
+
+
+def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return (np.ascontiguousarray(b, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+# --------------------------------------------------------------------------
+# Block-level restatement
+# --------------------------------------------------------------------------
+
+def nblocks(n: int, b: int) -> int:
+    return (n + b - 1) // b
+
+
+def pool_blocks(x_bits: np.ndarray, block: int) -> np.ndarray:
+    x_bits = np.ascontiguousarray(x_bits, dtype=np.uint16)
+    n, d = x_bits.shape
+    out = np.empty((nblocks(n, block), d), np.float32)
+    _load_oracle().orc_pool_blocks(x_bits, n, d, block, out)
+    return out
+
+
+def score_scale(d: int) -> float:
+    return float(_load_oracle().orc_score_scale(d))
+
+
+def visible_blocks(qb: int, n: int, bq: int, bk: int, causal: bool) -> int:
+    return int(_load_oracle().orc_visible_blocks(qb, n, bq, bk, int(causal)))
+
+
+def block_scores(qp: np.ndarray, kp: np.ndarray, n: int, bq: int, bk: int,
+                 causal: bool) -> np.ndarray:
+    d = qp.shape[1]
+    out = np.empty((nblocks(n, bq), nblocks(n, bk)), np.float32)
+    _load_oracle().orc_block_scores(np.ascontiguousarray(qp, np.float32),
+                                    np.ascontiguousarray(kp, np.float32), n, d, bq, bk,
+                                    int(causal), out)
+    return out
+
+
+def select_topk(scores: np.ndarray, n: int, bq: int, bk: int, causal: bool, k_blocks: int,
+                kmax: int):
+    nqb = nblocks(n, bq)
+    idx = np.empty((nqb, kmax), np.int32)
+    cnt = np.empty(nqb, np.int32)
+    _load_oracle().orc_select_topk(np.ascontiguousarray(scores, np.float32), n, bq, bk,
+                                   int(causal), k_blocks, kmax, idx, cnt)
+    return idx, cnt
+
+
+def topk_row(values: np.ndarray, k: int) -> np.ndarray:
+    values = np.ascontiguousarray(values, np.float64)
+    out = np.empty(k, np.int64)
+    _load_oracle().orc_topk_row(values, values.size, k, out)
+    return out
+
+
+def layer(q_bits, k_bits, v_bits, k_blocks, *, bq=128, bk=128, causal=True, kmax=None,
+          with_output=True):
+    """Whole layer: pooled scores, selections and fp64 outputs for every q head.
+
+    q_bits [Hq, n, d], k_bits/v_bits [Hkv, n, d] (bf16 bit patterns);
+    k_blocks [Hq] per-head budgets in blocks.
+    """
+    q_bits = np.ascontiguousarray(q_bits, np.uint16)
+    k_bits = np.ascontiguousarray(k_bits, np.uint16)
+    v_bits = np.ascontiguousarray(v_bits, np.uint16)
+    hq, n, d = q_bits.shape
+    hkv = k_bits.shape[0]
+    nqb, nkb = nblocks(n, bq), nblocks(n, bk)
+    k_blocks = np.ascontiguousarray(k_blocks, np.int64)
+    if kmax is None:
+        kmax = int(min(nkb, k_blocks.max()))
+    scores = np.empty((hq, nqb, nkb), np.float32)
+    idx = np.empty((hq, nqb, kmax), np.int32)
+    cnt = np.empty((hq, nqb), np.int32)
+    out = np.empty((hq, n, d), np.float64) if with_output else None
+    _load_oracle().orc_layer(q_bits, k_bits, v_bits, hq, hkv, n, d, bq, bk, int(causal),
+                             k_blocks, kmax, scores, idx, cnt,
+                             out.ctypes.data if with_output else None)
+    return scores, idx, cnt, out
+
+
+def sparse_rows(q_bits_h, k_bits_g, v_bits_g, rows, sel_blocks, *, bq=128, bk=128, causal=True):
+    """fp64 outputs of selected query rows of one head (numpy restatement of
+    orc_block_sparse_attention for row subsets at full sequence length).
+
+    rows: query indices (all in one query block); sel_blocks: that block's
+    selected key blocks. Follows attention.cpp:35-49 on the kept tokens.
+    """
+    n, d = k_bits_g.shape
+    toks = np.concatenate([np.arange(b * bk, min(n, (b + 1) * bk)) for b in sorted(sel_blocks)])
+    K = bf16_bits_to_f32(k_bits_g[toks]).astype(np.float64)
+    V = bf16_bits_to_f32(v_bits_g[toks]).astype(np.float64)
+    scale = 1.0 / np.sqrt(d)
+    out = np.zeros((len(rows), d), np.float64)
+    for r, i in enumerate(rows):
+        q = bf16_bits_to_f32(q_bits_h[i]).astype(np.float64)
+        keep = toks <= i if causal else np.ones_like(toks, bool)
+        if not keep.any():
+            continue
+        s = (K[keep] @ q) * scale
+        w = np.exp(s - s.max())
+        out[r] = (w / w.sum()) @ V[keep]
+    return out
+
+
+def pooled_scores_rows(q_bits_h, kp, qbs, *, bq=128, bk=128, causal=True):
+    """Block scores of the query blocks `qbs` of one head against the pooled
+    keys `kp` [nkb][d] of its kv head (C restatement, bit-exact with kernel 1)."""
+    n = q_bits_h.shape[0]
+    rows = []
+    for qb in qbs:
+        rows.append(pool_blocks(q_bits_h[qb * bq:min(n, (qb + 1) * bq)], bq)[0])
+    qp = np.ascontiguousarray(np.stack(rows), np.float32)
+    nkb, d = kp.shape
+    out = np.empty((len(qbs), nkb), np.float32)
+    _load_oracle().orc_score_rows(qp, np.ascontiguousarray(kp, np.float32), len(qbs), nkb, d, out)
+    for r, qb in enumerate(qbs):
+        out[r, visible_blocks(qb, n, bq, bk, causal):] = -np.inf
+    return out
+
+
+# --------------------------------------------------------------------------
+# Budget table / plan / metric restatement
+# --------------------------------------------------------------------------
+
+def _flatten_curves(curves):
+    offsets = np.zeros(len(curves) + 1, np.int64)
+    for h, (b, _) in enumerate(curves):
+        offsets[h + 1] = offsets[h] + len(b)
+    pb = np.concatenate([np.asarray(b, np.int64) for b, _ in curves])
+    pr = np.concatenate([np.asarray(r, np.float64) for _, r in curves])
+    return offsets, pb, pr
+
+
+def uniform_allocate(n, total, floor, n_k):
+    out = np.empty(n, np.int64)
+    if _load_oracle().orc_uniform_allocate(n, total, floor, n_k, out):
+        raise ValueError("infeasible total")
+    return out
+
+
+def maxmin_allocate(curves, n_k, total, quantum=64, floor=128, max_iterations=0):
+    """curves: list of (budgets, recoveries) per head."""
+    offsets, pb, pr = _flatten_curves(curves)
+    out = np.empty(len(curves), np.int64)
+    tr = C.c_int64()
+    cap = C.c_int32()
+    if _load_oracle().orc_maxmin_allocate(len(curves), n_k, offsets, pb, pr, total, quantum,
+                                          floor, max_iterations, out, C.byref(tr), C.byref(cap)):
+        raise ValueError("infeasible total")
+    return out, int(tr.value), bool(cap.value)
+
+
+def naive_assign(n, devices, round_robin=False):
+    out = np.empty(n, np.int32)
+    if _load_oracle().orc_naive_assign(n, devices, int(round_robin), out):
+        raise ValueError("bad device count")
+    return out
+
+
+def greedy_assign(budgets, devices):
+    budgets = np.ascontiguousarray(budgets, np.int64)
+    out = np.empty(budgets.size, np.int32)
+    _load_oracle().orc_greedy_assign(budgets, budgets.size, devices, out)
+    return out
+
+
+def imbalance(budgets, dev, devices):
+    budgets = np.ascontiguousarray(budgets, np.int64)
+    loads = np.empty(devices, np.int64)
+    am = C.c_int32()
+    imb = _load_oracle().orc_imbalance(budgets, budgets.size,
+                                       np.ascontiguousarray(dev, np.int32), devices, loads,
+                                       C.byref(am))
+    return loads, float(imb), int(am.value)
+
+
+def barrier(latencies):
+    lat = np.ascontiguousarray(latencies, np.float64)
+    b, bub = C.c_double(), C.c_double()
+    _load_oracle().orc_barrier(lat, lat.size, C.byref(b), C.byref(bub))
+    return float(b.value), float(bub.value)
+
+
+# --------------------------------------------------------------------------
+# The reference itself (oracle/_ref)
+# --------------------------------------------------------------------------
+
+class ref:
+    """Thin wrappers over the compiled, unmodified reference library."""
+
+    @staticmethod
+    def dense_attention(Q, K, V, causal=False, with_weights=False):
+        Q, K, V = (np.ascontiguousarray(a, np.float64) for a in (Q, K, V))
+        out = np.empty((Q.shape[0], V.shape[1]), np.float64)
+        w = np.empty((Q.shape[0], K.shape[0]), np.float64) if with_weights else None
+        _ref_check(_load_ref().ref_dense_attention(
+            Q, K, V, Q.shape[0], K.shape[0], Q.shape[1], V.shape[1], int(causal),
+            w.ctypes.data if with_weights else None, out))
+        return (w, out) if with_weights else out
+
+    @staticmethod
+    def sparse_attention(Q, K, V, budget, causal=False, kind=0, serial=False):
+        Q, K, V = (np.ascontiguousarray(a, np.float64) for a in (Q, K, V))
+        out = np.empty((Q.shape[0], V.shape[1]), np.float64)
+        fn = _load_ref().ref_serial_sparse_attention if serial else _load_ref().ref_sparse_attention
+        _ref_check(fn(Q, K, V, Q.shape[0], K.shape[0], Q.shape[1], V.shape[1], kind, budget,
+                      int(causal), out))
+        return out
+
+    @staticmethod
+    def build_profiles(Q, K, V, grid, causal=False, kind=0):
+        """Q/K/V [H, n, d] fp64 -> recovery [H, len(grid)]."""
+        Q, K, V = (np.ascontiguousarray(a, np.float64) for a in (Q, K, V))
+        grid = np.ascontiguousarray(grid, np.int64)
+        h, n_q, d = Q.shape
+        out = np.empty((h, grid.size), np.float64)
+        _ref_check(_load_ref().ref_build_profiles(Q, K, V, h, n_q, K.shape[1], d, grid, grid.size,
+                                                  kind, int(causal), out))
+        return out
+
+    @staticmethod
+    def uniform_allocate(n, total, floor, n_k):
+        out = np.empty(n, np.int64)
+        _ref_check(_load_ref().ref_uniform_allocate(n, total, floor, n_k, out))
+        return out
+
+    @staticmethod
+    def maxmin_allocate(curves, n_k, total, quantum=64, floor=128, max_iterations=0):
+        offsets, pb, pr = _flatten_curves(curves)
+        out = np.empty(len(curves), np.int64)
+        tr, cap, off = C.c_int64(), C.c_int32(), C.c_int64()
+        _ref_check(_load_ref().ref_maxmin_allocate(len(curves), n_k, offsets, pb, pr, total,
+                                                   quantum, floor, max_iterations, out,
+                                                   C.byref(tr), C.byref(cap), C.byref(off)))
+        return out, int(tr.value), bool(cap.value)
+
+    @staticmethod
+    def naive_assign(budgets, devices, round_robin=False):
+        budgets = np.ascontiguousarray(budgets, np.int64)
+        out = np.empty(budgets.size, np.int32)
+        _ref_check(_load_ref().ref_naive_assign(budgets, budgets.size, devices, int(round_robin),
+                                                out))
+        return out
+
+    @staticmethod
+    def greedy_assign(budgets, devices):
+        budgets = np.ascontiguousarray(budgets, np.int64)
+        out = np.empty(budgets.size, np.int32)
+        _ref_check(_load_ref().ref_greedy_assign(budgets, budgets.size, devices, out))
+        return out
+
+    @staticmethod
+    def optimal_assign(budgets, devices):
+        budgets = np.ascontiguousarray(budgets, np.int64)
+        out = np.empty(budgets.size, np.int32)
+        _ref_check(_load_ref().ref_optimal_assign(budgets, budgets.size, devices, out))
+        return out
+
+    @staticmethod
+    def imbalance(budgets, dev, devices):
+        budgets = np.ascontiguousarray(budgets, np.int64)
+        loads = np.empty(devices, np.int64)
+        tot, imb, am = C.c_int64(), C.c_double(), C.c_int32()
+        _ref_check(_load_ref().ref_imbalance(budgets, budgets.size,
+                                             np.ascontiguousarray(dev, np.int32), devices, loads,
+                                             C.byref(tot), C.byref(imb), C.byref(am)))
+        return loads, float(imb.value), int(am.value)
+
+    @staticmethod
+    def simulate(loads, alpha=0.0, beta=1.0):
+        loads = np.ascontiguousarray(loads, np.int64)
+        lat = np.empty(loads.size, np.float64)
+        b, bub = C.c_double(), C.c_double()
+        _ref_check(_load_ref().ref_simulate(loads, loads.size, alpha, beta, lat, C.byref(b),
+                                            C.byref(bub)))
+        return lat, float(b.value), float(bub.value)
+
+    @staticmethod
+    def max_threads() -> int:
+        return int(_load_ref().ref_max_threads())

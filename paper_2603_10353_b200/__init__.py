@@ -1,0 +1,17 @@
+"""B200-native S-HPLB sparse-attention hot path (arXiv 2603.10353).
+
+Host API over libshplb.so (C ABI: include/shplb.h). See DESIGN.md.
+"""
+from ._native import (CudaError, InvalidArgument, LogicError, NotSupported, ShplbError, build,
+                      lib)
+from .api import (BLOCK, HEAD_DIM, BudgetAllocation, Context, LoadReport, RecoveryCurve,
+                  SimulationResult, barrier, default_budget_grid, greedy_assign, imbalance,
+                  layer_work, maxmin_allocate, naive_assign, profile_curves, simulate,
+                  uniform_allocate)
+
+__all__ = [
+    "BLOCK", "HEAD_DIM", "BudgetAllocation", "Context", "CudaError", "InvalidArgument",
+    "LoadReport", "LogicError", "NotSupported", "RecoveryCurve", "ShplbError", "SimulationResult",
+    "barrier", "build", "default_budget_grid", "greedy_assign", "imbalance", "layer_work", "lib",
+    "maxmin_allocate", "naive_assign", "profile_curves", "simulate", "uniform_allocate",
+]

@@ -1,0 +1,148 @@
+"""ctypes binding of libshplb.so (the C ABI declared in include/shplb.h).
+
+The shared library is built in-tree by ``paper_2603_10353_b200/csrc/Makefile``
+(``build()`` below, or ``__graft_entry__.build()``). There is no fallback: if
+the library is missing, loading fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "lib", "libshplb.so")
+CSRC_DIR = os.path.join(PKG_DIR, "csrc")
+
+# Every symbol include/shplb.h declares (checked by the CPU test suite).
+EXPORTS = (
+    "shplb_last_error", "shplb_version",
+    "shplb_uniform_allocate", "shplb_maxmin_allocate", "shplb_recovery_at",
+    "shplb_profile_curves_host",
+    "shplb_plan_naive", "shplb_plan_greedy", "shplb_imbalance",
+    "shplb_simulate", "shplb_barrier",
+    "shplb_ctx_create", "shplb_ctx_destroy", "shplb_ctx_launch_count",
+    "shplb_block_scores", "shplb_select_blocks", "shplb_block_sparse_attention",
+    "shplb_sparse_attention_layer", "shplb_last_selection", "shplb_layer_work",
+)
+
+SHPLB_OK = 0
+SHPLB_INVALID_ARGUMENT = 1
+SHPLB_RUNTIME_ERROR = 2
+SHPLB_LOGIC_ERROR = 3
+SHPLB_CUDA_ERROR = 4
+SHPLB_NOT_SUPPORTED = 5
+
+
+class ShplbError(RuntimeError):
+    """Base class of errors raised through the C ABI."""
+
+
+class InvalidArgument(ShplbError, ValueError):
+    """The reference's std::invalid_argument (bad shapes, budgets, totals)."""
+
+
+class LogicError(ShplbError):
+    """The reference's std::logic_error."""
+
+
+class CudaError(ShplbError):
+    """A CUDA runtime/driver failure."""
+
+
+class NotSupported(ShplbError, NotImplementedError):
+    """A shape or policy the sm_100a kernels do not implement."""
+
+
+_ERRORS = {
+    SHPLB_INVALID_ARGUMENT: InvalidArgument,
+    SHPLB_RUNTIME_ERROR: ShplbError,
+    SHPLB_LOGIC_ERROR: LogicError,
+    SHPLB_CUDA_ERROR: CudaError,
+    SHPLB_NOT_SUPPORTED: NotSupported,
+}
+
+
+class LayerShape(C.Structure):
+    """shplb_layer_shape."""
+    _fields_ = [
+        ("num_q_heads", C.c_int32),
+        ("num_kv_heads", C.c_int32),
+        ("seq_len", C.c_int64),
+        ("head_dim", C.c_int32),
+        ("block_q", C.c_int32),
+        ("block_k", C.c_int32),
+        ("causal", C.c_int32),
+        ("kind", C.c_int32),
+        ("validate", C.c_int32),
+        ("kv_head_of_q", C.c_void_p),
+    ]
+
+
+class MaxminDiag(C.Structure):
+    """shplb_maxmin_diag."""
+    _fields_ = [
+        ("transfers", C.c_int64),
+        ("hit_iteration_cap", C.c_int32),
+        ("off_grid_evaluations", C.c_int64),
+        ("min_recovery_start", C.c_double),
+        ("min_recovery_end", C.c_double),
+    ]
+
+
+def build(verbose: bool = False) -> None:
+    """Compile libshplb.so for sm_100a in-tree (nvcc + g++)."""
+    r = subprocess.run(["make", "-C", CSRC_DIR, "-j8"], capture_output=True, text=True)
+    if verbose or r.returncode != 0:
+        print(r.stdout[-4000:], r.stderr[-4000:])
+    if r.returncode != 0:
+        raise RuntimeError("building libshplb.so failed")
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libshplb.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise FileNotFoundError(
+            f"{LIB_PATH} not found: the CUDA extension is not built "
+            "(run paper_2603_10353_b200._native.build() or __graft_entry__.build())")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    P = C.POINTER
+    L.shplb_last_error.restype = C.c_char_p
+    L.shplb_version.restype = C.c_char_p
+    L.shplb_uniform_allocate.argtypes = [i64, i64, i64, i64, vp]
+    L.shplb_maxmin_allocate.argtypes = [i32, i64, vp, vp, vp, i64, i64, i64, i64, vp,
+                                        P(MaxminDiag)]
+    L.shplb_recovery_at.argtypes = [i64, vp, vp, i64, P(f64)]
+    L.shplb_profile_curves_host.argtypes = [vp, vp, i32, i32, i64, i64, i32, vp, i64, vp]
+    L.shplb_plan_naive.argtypes = [vp, i32, i32, i32, vp]
+    L.shplb_plan_greedy.argtypes = [vp, i32, i32, vp]
+    L.shplb_imbalance.argtypes = [vp, i32, vp, i32, vp, P(i64), P(f64), P(i32)]
+    L.shplb_simulate.argtypes = [vp, i32, f64, f64, vp, P(f64), P(f64)]
+    L.shplb_barrier.argtypes = [vp, i32, P(f64), P(f64)]
+    L.shplb_ctx_create.argtypes = [C.c_int, P(vp)]
+    L.shplb_ctx_destroy.argtypes = [vp]
+    L.shplb_ctx_launch_count.argtypes = [vp]
+    L.shplb_ctx_launch_count.restype = i64
+    L.shplb_block_scores.argtypes = [vp, P(LayerShape), vp, vp, vp, vp]
+    L.shplb_select_blocks.argtypes = [vp, P(LayerShape), vp, vp, i64, vp, vp, vp]
+    L.shplb_block_sparse_attention.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp, i64, vp,
+                                               vp]
+    L.shplb_sparse_attention_layer.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp, vp]
+    L.shplb_last_selection.argtypes = [vp, P(vp), P(vp), P(i64)]
+    L.shplb_layer_work.argtypes = [P(LayerShape), vp, P(i64), P(f64)]
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    """Translate a shplb_status into the matching Python exception."""
+    if status != SHPLB_OK:
+        msg = lib().shplb_last_error().decode()
+        raise _ERRORS.get(status, ShplbError)(msg)

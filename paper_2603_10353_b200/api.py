@@ -1,0 +1,337 @@
+"""Python face of the B200 hot path, mirroring the reference operator API.
+
+Names and argument meanings follow the reference's ``headbal`` namespace
+(/root/reference/proj/include/headbal/*.hpp): the per-head budget table
+(``uniform_allocate``, ``maxmin_allocate``), the head->GPU plan
+(``naive_assign``, ``greedy_assign``, ``imbalance``), the barrier metric
+(``simulate``, ``barrier``) and the sparse-attention entry point
+(``sparse_attention_layer`` — the per-head-budget loop of ``run_skyline``
+around ``sparse_attention``). Errors raise ``InvalidArgument`` (a
+``ValueError``) where the reference throws ``std::invalid_argument``, with the
+reference's message text.
+
+Everything computes in libshplb.so (C++ host code and sm_100a kernels). torch
+is used only to hold device memory and name the CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from ._native import (LayerShape, MaxminDiag, check, lib)
+
+BLOCK = 128
+HEAD_DIM = 128
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+# ---------------------------------------------------------------------------
+# Budget table (allocator.hpp)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class RecoveryCurve:
+    """profiler.hpp:29-41 — sampled budget -> recovery, ending at (n_k, 1)."""
+    budgets: np.ndarray
+    recovery: np.ndarray
+    context_length: int
+
+    def recovery_at(self, budget: int) -> float:
+        out = C.c_double()
+        b, r = _i64(self.budgets), _f64(self.recovery)
+        check(lib().shplb_recovery_at(b.size, _ptr(b), _ptr(r), int(budget), C.byref(out)))
+        return float(out.value)
+
+
+@dataclass
+class BudgetAllocation:
+    """allocator.hpp:23-38 (budgets in tokens) plus the diagnostics."""
+    budgets: np.ndarray
+    total: int
+    floor: int
+    transfers: int = 0
+    hit_iteration_cap: bool = False
+    off_grid_evaluations: int = 0
+    min_recovery_start: float = 0.0
+    min_recovery_end: float = 0.0
+
+
+def uniform_allocate(num_heads: int, total: int, floor: int, context_length: int) -> BudgetAllocation:
+    out = np.empty(num_heads, np.int64)
+    check(lib().shplb_uniform_allocate(num_heads, total, floor, context_length, _ptr(out)))
+    return BudgetAllocation(out, total, floor)
+
+
+def maxmin_allocate(curves: Sequence[RecoveryCurve], total: int, quantum: int = 64,
+                    floor: int = 128, max_iterations: int = 0) -> BudgetAllocation:
+    """Max-min budget shifting (allocator.hpp:53-54); bit-exact with the reference."""
+    if len(curves) == 0:
+        from ._native import InvalidArgument
+        raise InvalidArgument("need at least one recovery curve")
+    n_k = int(curves[0].context_length)
+    for c in curves:
+        if int(c.context_length) != n_k:
+            from ._native import InvalidArgument
+            raise InvalidArgument("all curves must share the context length")
+    offsets = np.zeros(len(curves) + 1, np.int64)
+    for h, c in enumerate(curves):
+        offsets[h + 1] = offsets[h] + len(c.budgets)
+    pb = _i64(np.concatenate([np.asarray(c.budgets) for c in curves]))
+    pr = _f64(np.concatenate([np.asarray(c.recovery) for c in curves]))
+    out = np.empty(len(curves), np.int64)
+    diag = MaxminDiag()
+    check(lib().shplb_maxmin_allocate(len(curves), n_k, _ptr(offsets), _ptr(pb), _ptr(pr), total,
+                                      quantum, floor, max_iterations, _ptr(out), C.byref(diag)))
+    return BudgetAllocation(out, total, floor, int(diag.transfers), bool(diag.hit_iteration_cap),
+                            int(diag.off_grid_evaluations), float(diag.min_recovery_start),
+                            float(diag.min_recovery_end))
+
+
+def default_budget_grid(context_length: int, stride: int) -> np.ndarray:
+    """profiler.cpp:385-392: {0, stride, 2*stride, ..., n_k}."""
+    g = list(range(0, context_length, stride)) + [context_length]
+    return np.asarray(g, np.int64)
+
+
+def profile_curves(q_rows_bf16: np.ndarray, k_bf16: np.ndarray, grid: np.ndarray) -> list[RecoveryCurve]:
+    """PerQueryTopK recovery curves (build_profiles, profiler.cpp:157-196) from
+    calibration query rows. q_rows_bf16: uint16 [Hq][rows][d]; k_bf16: uint16
+    [Hkv][n_k][d] (bf16 bit patterns, host). Host C++, OpenMP."""
+    q = np.ascontiguousarray(q_rows_bf16, np.uint16)
+    k = np.ascontiguousarray(k_bf16, np.uint16)
+    grid = _i64(grid)
+    hq, rows, d = q.shape
+    hkv, n_k, _ = k.shape
+    out = np.empty((hq, grid.size), np.float64)
+    check(lib().shplb_profile_curves_host(_ptr(q), _ptr(k), hq, hkv, rows, n_k, d, _ptr(grid),
+                                          grid.size, _ptr(out)))
+    return [RecoveryCurve(grid.copy(), out[h].copy(), n_k) for h in range(hq)]
+
+
+# ---------------------------------------------------------------------------
+# Head -> GPU plan (partitioner.hpp) and metric (simulator.hpp)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class LoadReport:
+    """partitioner.hpp:25-30."""
+    loads: np.ndarray
+    total: int
+    imbalance: float
+    argmax_device: int
+
+
+def naive_assign(budgets, devices: int, round_robin: bool = False) -> np.ndarray:
+    b = _i64(budgets)
+    out = np.empty(b.size, np.int32)
+    check(lib().shplb_plan_naive(_ptr(b), b.size, devices, int(round_robin), _ptr(out)))
+    return out
+
+
+def greedy_assign(budgets, devices: int) -> np.ndarray:
+    b = _i64(budgets)
+    out = np.empty(b.size, np.int32)
+    check(lib().shplb_plan_greedy(_ptr(b), b.size, devices, _ptr(out)))
+    return out
+
+
+def imbalance(budgets, device_of_head, devices: int) -> LoadReport:
+    b, a = _i64(budgets), _i32(device_of_head)
+    if a.size != b.size:
+        from ._native import InvalidArgument
+        raise InvalidArgument(f"assignment covers {a.size} heads but {b.size} budgets were given")
+    loads = np.empty(devices, np.int64)
+    tot, imb, am = C.c_int64(), C.c_double(), C.c_int32()
+    check(lib().shplb_imbalance(_ptr(b), b.size, _ptr(a), devices, _ptr(loads), C.byref(tot),
+                                C.byref(imb), C.byref(am)))
+    return LoadReport(loads, int(tot.value), float(imb.value), int(am.value))
+
+
+@dataclass
+class SimulationResult:
+    """simulator.hpp:20-25."""
+    device_latency: np.ndarray
+    barrier_latency: float
+    bubble_fraction: float
+
+
+def simulate(loads, alpha: float = 0.0, beta: float = 1.0) -> SimulationResult:
+    ld = _i64(loads)
+    lat = np.empty(ld.size, np.float64)
+    b, bub = C.c_double(), C.c_double()
+    check(lib().shplb_simulate(_ptr(ld), ld.size, alpha, beta, _ptr(lat), C.byref(b), C.byref(bub)))
+    return SimulationResult(lat, float(b.value), float(bub.value))
+
+
+def barrier(device_latency) -> SimulationResult:
+    """Barrier latency and bubble over MEASURED per-device latencies."""
+    lat = _f64(device_latency)
+    b, bub = C.c_double(), C.c_double()
+    check(lib().shplb_barrier(_ptr(lat), lat.size, C.byref(b), C.byref(bub)))
+    return SimulationResult(lat, float(b.value), float(bub.value))
+
+
+# ---------------------------------------------------------------------------
+# Sparse attention on the GPU (attention.hpp)
+# ---------------------------------------------------------------------------
+
+def _shape(num_q_heads, num_kv_heads, seq_len, causal, validate=False, kv_map=None,
+           head_dim=HEAD_DIM) -> LayerShape:
+    sh = LayerShape(num_q_heads, num_kv_heads, seq_len, head_dim, BLOCK, BLOCK, int(causal), 0,
+                    int(validate), None)
+    if kv_map is not None:
+        m = _i32(kv_map)
+        sh._kv_map_keepalive = m  # the C struct only borrows the pointer
+        sh.kv_head_of_q = m.ctypes.data
+    return sh
+
+
+def _stream_ptr(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dev_ptr(t, name, dtype=None):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        from ._native import InvalidArgument
+        raise InvalidArgument(f"{name} must be a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        from ._native import InvalidArgument
+        raise InvalidArgument(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        from ._native import InvalidArgument
+        raise InvalidArgument(f"{name} must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+class Context:
+    """shplb_ctx: per-device workspace. One per rank/device."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        check(lib().shplb_ctx_create(device, C.byref(self._h)))
+        self.device = device
+
+    def close(self) -> None:
+        if self._h:
+            check(lib().shplb_ctx_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launches(self) -> int:
+        return int(lib().shplb_ctx_launch_count(self._h))
+
+    # -- kernel 1 ---------------------------------------------------------
+    def block_scores(self, q, k, causal=True, stream=None, validate=False, out=None, kv_map=None):
+        import torch
+        hq, n, d = q.shape
+        hkv = k.shape[0]
+        nb = (n + BLOCK - 1) // BLOCK
+        if out is None:
+            out = torch.empty((hq, nb, nb), dtype=torch.float32, device=q.device)
+        sh = _shape(hq, hkv, n, causal, validate, kv_map, d)
+        check(lib().shplb_block_scores(self._h, C.byref(sh), _dev_ptr(q, "q", torch.bfloat16),
+                                       _dev_ptr(k, "k", torch.bfloat16),
+                                       _dev_ptr(out, "scores", torch.float32), _stream_ptr(stream)))
+        return out
+
+    # -- kernel 2 ---------------------------------------------------------
+    def select_blocks(self, scores, k_blocks, n, causal=True, kmax=None, stream=None):
+        import torch
+        hq, nqb, _ = scores.shape
+        kb = _i64(k_blocks)
+        kmax = int(kb.max()) if kmax is None else int(kmax)
+        idx = torch.empty((hq, nqb, kmax), dtype=torch.int32, device=scores.device)
+        cnt = torch.empty((hq, nqb), dtype=torch.int32, device=scores.device)
+        sh = _shape(hq, 1, n, causal)
+        sh.num_kv_heads = 1
+        check(lib().shplb_select_blocks(self._h, C.byref(sh), _dev_ptr(scores, "scores", torch.float32),
+                                        _ptr(kb), kmax, _dev_ptr(idx, "idx"), _dev_ptr(cnt, "cnt"),
+                                        _stream_ptr(stream)))
+        return idx, cnt
+
+    # -- kernel 3 ---------------------------------------------------------
+    def block_sparse_attention(self, q, k, v, idx, cnt, causal=True, stream=None, out=None,
+                               kv_map=None):
+        import torch
+        hq, n, d = q.shape
+        if out is None:
+            out = torch.empty_like(q)
+        sh = _shape(hq, k.shape[0], n, causal, kv_map=kv_map, head_dim=d)
+        check(lib().shplb_block_sparse_attention(
+            self._h, C.byref(sh), _dev_ptr(q, "q", torch.bfloat16), _dev_ptr(k, "k", torch.bfloat16),
+            _dev_ptr(v, "v", torch.bfloat16), _dev_ptr(idx, "idx", torch.int32),
+            _dev_ptr(cnt, "cnt", torch.int32), int(idx.shape[-1]), _dev_ptr(out, "out", torch.bfloat16),
+            _stream_ptr(stream)))
+        return out
+
+    # -- the layer: kernels 1+2 fused, then 3 -----------------------------
+    def sparse_attention_layer(self, q, k, v, budgets_tokens, causal=True, stream=None, out=None,
+                               validate=False, kv_map=None):
+        """sparse_attention for every head with its own token budget."""
+        import torch
+        hq, n, d = q.shape
+        if out is None:
+            out = torch.empty_like(q)
+        b = _i64(budgets_tokens)
+        if b.size != hq:
+            from ._native import InvalidArgument
+            raise InvalidArgument(f"need one budget per query head ({hq}), got {b.size}")
+        sh = _shape(hq, k.shape[0], n, causal, validate, kv_map, d)
+        check(lib().shplb_sparse_attention_layer(
+            self._h, C.byref(sh), _dev_ptr(q, "q", torch.bfloat16), _dev_ptr(k, "k", torch.bfloat16),
+            _dev_ptr(v, "v", torch.bfloat16), _ptr(b), _dev_ptr(out, "out", torch.bfloat16),
+            _stream_ptr(stream)))
+        return out
+
+    def last_selection(self, num_q_heads: int, seq_len: int):
+        """(idx, cnt) of the last layer call as torch views over the context workspace."""
+        import torch
+        ip, cp, km = C.c_void_p(), C.c_void_p(), C.c_int64()
+        check(lib().shplb_last_selection(self._h, C.byref(ip), C.byref(cp), C.byref(km)))
+        nqb = (seq_len + BLOCK - 1) // BLOCK
+        kmax = int(km.value)
+        idx = torch.empty((num_q_heads, nqb, kmax), dtype=torch.int32, device=f"cuda:{self.device}")
+        cnt = torch.empty((num_q_heads, nqb), dtype=torch.int32, device=f"cuda:{self.device}")
+        nbytes_i = idx.numel() * 4
+        nbytes_c = cnt.numel() * 4
+        cudart = torch.cuda.cudart()
+        torch.cuda.synchronize()
+        cudart.cudaMemcpy(idx.data_ptr(), ip.value, nbytes_i, 3)  # cudaMemcpyDeviceToDevice
+        cudart.cudaMemcpy(cnt.data_ptr(), cp.value, nbytes_c, 3)
+        return idx, cnt
+
+
+def layer_work(num_q_heads, num_kv_heads, seq_len, budgets_tokens, causal=True):
+    """(selected tiles, algorithmic FLOPs 4*d*bq*bk*tiles) of one layer call."""
+    sh = _shape(num_q_heads, num_kv_heads, seq_len, causal)
+    b = _i64(budgets_tokens)
+    t, f = C.c_int64(), C.c_double()
+    check(lib().shplb_layer_work(C.byref(sh), _ptr(b), C.byref(t), C.byref(f)))
+    return int(t.value), float(f.value)

@@ -1,0 +1,141 @@
+// Head -> GPU plan and the barrier metric.
+//
+// naive / greedy / imbalance follow the reference partitioner bit for bit
+// (proj/src/partitioner.cpp:130-183, :236-266, incl. its error messages);
+// simulate / barrier follow proj/src/simulator.cpp:13-47. greedy_assign is the
+// LPT rule: heads by (budget desc, index asc), each placed on the device with
+// the smallest (load, device index) — the pair order the reference's
+// std::priority_queue<pair<long,int>, ..., greater<>> pops.
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <queue>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../common.hpp"
+
+using namespace shplb;
+
+namespace {
+
+void check_budgets(const int64_t* budgets, int32_t n) {
+    if (n < 1) throw InvalidArgument("need at least one head");
+    require(budgets != nullptr, "budgets is null");
+    for (int32_t h = 0; h < n; ++h)
+        if (budgets[h] < 0) throw InvalidArgument("budgets must be nonnegative");
+}
+
+}  // namespace
+
+extern "C" int shplb_plan_naive(const int64_t* budgets, int32_t num_heads, int32_t devices,
+                                int32_t round_robin, int32_t* device_of_head) {
+    return guarded([&] {
+        check_budgets(budgets, num_heads);
+        if (devices < 1) throw InvalidArgument("need at least one device");
+        if (devices > num_heads) {
+            throw InvalidArgument("device count " + std::to_string(devices) +
+                                  " exceeds head count " + std::to_string(num_heads));
+        }
+        if (round_robin) {
+            for (int32_t h = 0; h < num_heads; ++h) device_of_head[h] = h % devices;
+            return;
+        }
+        // Contiguous blocks; the first N mod D devices take the ceil-size block.
+        const int32_t base = num_heads / devices, extra = num_heads % devices;
+        int32_t next = 0;
+        for (int32_t d = 0; d < devices; ++d)
+            for (int32_t i = 0; i < base + (d < extra ? 1 : 0); ++i) device_of_head[next++] = d;
+    });
+}
+
+extern "C" int shplb_plan_greedy(const int64_t* budgets, int32_t num_heads, int32_t devices,
+                                 int32_t* device_of_head) {
+    return guarded([&] {
+        check_budgets(budgets, num_heads);
+        if (devices < 1) throw InvalidArgument("need at least one device");
+        std::vector<int32_t> order(static_cast<std::size_t>(num_heads));
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int32_t a, int32_t b) { return budgets[a] > budgets[b]; });
+        using Slot = std::pair<int64_t, int32_t>;  // (load, device), min first
+        std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> q;
+        for (int32_t d = 0; d < devices; ++d) q.emplace(0, d);
+        for (int32_t h : order) {
+            const auto [load, dev] = q.top();
+            q.pop();
+            device_of_head[h] = dev;
+            q.emplace(load + budgets[h], dev);
+        }
+    });
+}
+
+extern "C" int shplb_imbalance(const int64_t* budgets, int32_t num_heads,
+                               const int32_t* device_of_head, int32_t devices, int64_t* loads_out,
+                               int64_t* total_out, double* imbalance_out, int32_t* argmax_out) {
+    return guarded([&] {
+        // Assignment::validate (partitioner.cpp:38-48).
+        if (devices < 1) throw InvalidArgument("need at least one device");
+        if (num_heads < 1) throw InvalidArgument("assignment covers no heads");
+        for (int32_t h = 0; h < num_heads; ++h) {
+            if (device_of_head[h] < 0 || device_of_head[h] >= devices) {
+                throw InvalidArgument("head " + std::to_string(h) + " assigned to invalid device " +
+                                      std::to_string(device_of_head[h]));
+            }
+        }
+        check_budgets(budgets, num_heads);
+        int64_t total = 0;
+        std::fill(loads_out, loads_out + devices, 0);
+        for (int32_t h = 0; h < num_heads; ++h) {
+            loads_out[device_of_head[h]] += budgets[h];
+            total += budgets[h];
+        }
+        int64_t mx = loads_out[0];
+        int32_t am = 0;
+        for (int32_t d = 1; d < devices; ++d)
+            if (loads_out[d] > mx) {
+                mx = loads_out[d];
+                am = d;
+            }
+        if (total_out) *total_out = total;
+        if (argmax_out) *argmax_out = am;
+        if (imbalance_out) {
+            *imbalance_out = total == 0 ? 1.0
+                                        : static_cast<double>(mx) * static_cast<double>(devices) /
+                                              static_cast<double>(total);
+        }
+    });
+}
+
+extern "C" int shplb_simulate(const int64_t* loads, int32_t devices, double alpha, double beta,
+                              double* latency_out, double* barrier_out, double* bubble_out) {
+    return guarded([&] {
+        // CostModel::validate (simulator.cpp:13-20).
+        if (!(beta > 0.0) || !std::isfinite(beta)) throw InvalidArgument("cost model beta must be > 0");
+        if (alpha < 0.0 || !std::isfinite(alpha)) throw InvalidArgument("cost model alpha must be >= 0");
+        if (devices < 1) throw InvalidArgument("load report has no devices");
+        std::vector<double> lat(static_cast<std::size_t>(devices));
+        double sum = 0.0;
+        for (int32_t d = 0; d < devices; ++d) {
+            lat[d] = alpha + beta * static_cast<double>(loads[d]);
+            sum += lat[d];
+        }
+        const double T = *std::max_element(lat.begin(), lat.end());
+        if (latency_out) std::copy(lat.begin(), lat.end(), latency_out);
+        if (barrier_out) *barrier_out = T;
+        if (bubble_out) *bubble_out = T == 0.0 ? 0.0 : 1.0 - (sum / static_cast<double>(devices)) / T;
+    });
+}
+
+extern "C" int shplb_barrier(const double* device_latency, int32_t devices, double* barrier_out,
+                             double* bubble_out) {
+    return guarded([&] {
+        if (devices < 1) throw InvalidArgument("load report has no devices");
+        double sum = 0.0;
+        for (int32_t d = 0; d < devices; ++d) sum += device_latency[d];
+        const double T = *std::max_element(device_latency, device_latency + devices);
+        if (barrier_out) *barrier_out = T;
+        if (bubble_out) *bubble_out = T == 0.0 ? 0.0 : 1.0 - (sum / static_cast<double>(devices)) / T;
+    });
+}

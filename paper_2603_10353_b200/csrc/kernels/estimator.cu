@@ -1,0 +1,281 @@
+// Kernels 1 and 2 of the hot path: the block-importance estimator (mean-pool
+// Q/K blocks, score pooled Q.K^T) and the per-head top-k block selector.
+//
+// Reference semantics (proj/src/attention.cpp): scores are q.k * (1/sqrt(d))
+// with the scale applied after the dot product (:20,26), causally masked
+// entries are -inf (:28-30), the kept set is the k largest under (value desc,
+// index asc), emitted in ascending index order (:53-64). The block
+// generalisation and the fixed fp32 summation orders are DESIGN.md §3; the C
+// oracle (oracle/shplb_oracle.c) restates them and the GPU output is
+// bit-identical to it.
+//
+// Roofline: pooling streams Q and K once from HBM (2*n*d*(Hq+Hkv) bytes) and
+// is HBM-bound. Scoring is an fp32 FFMA product of the pooled matrices (kept
+// on CUDA cores so every score is bit-reproducible on the CPU), and selection
+// is a warp-level radix (bisection) select on the order-preserving uint32
+// image of each score; both work out of shared memory / L2.
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+
+namespace shplb::kern {
+namespace {
+
+constexpr int kPoolThreads = 256;  // 16 row groups x 16 column groups of 8 columns
+
+// One CTA pools one 128-row block of one head. Thread (g, cg) sums rows
+// g, g+16, ... (ascending) of columns 8cg..8cg+7 with 16-byte loads; the 16
+// group partials per column are then added in ascending group order.
+__global__ void __launch_bounds__(kPoolThreads) pool_kernel(const __nv_bfloat16* __restrict__ x,
+                                                            int64_t n, float* __restrict__ out) {
+    __shared__ float part[kPoolSplit][kHeadDim + 4];
+    const int64_t b = blockIdx.x;
+    const int64_t head = blockIdx.y;
+    const int64_t nb = gridDim.x;
+    const int g = threadIdx.x >> 4;
+    const int cg = threadIdx.x & 15;
+    const int64_t t0 = b * kBlock;
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(kBlock), n - t0));
+    const __nv_bfloat16* base = x + (head * n + t0) * kHeadDim + cg * 8;
+
+    uint4 v[kBlock / kPoolSplit];
+#pragma unroll
+    for (int s = 0; s < kBlock / kPoolSplit; ++s) {
+        const int t = g + s * kPoolSplit;
+        v[s] = t < cnt ? __ldg(reinterpret_cast<const uint4*>(base + static_cast<int64_t>(t) * kHeadDim))
+                       : make_uint4(0, 0, 0, 0);
+    }
+    float acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+#pragma unroll
+    for (int s = 0; s < kBlock / kPoolSplit; ++s) {
+        if (g + s * kPoolSplit < cnt) {
+            const uint32_t w[4] = {v[s].x, v[s].y, v[s].z, v[s].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                acc[2 * e] = __fadd_rn(acc[2 * e], __uint_as_float(w[e] << 16));
+                acc[2 * e + 1] = __fadd_rn(acc[2 * e + 1], __uint_as_float(w[e] & 0xFFFF0000u));
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) part[g][cg * 8 + e] = acc[e];
+    __syncthreads();
+    if (threadIdx.x < kHeadDim) {
+        const int c = threadIdx.x;
+        float total = 0.0f;
+#pragma unroll
+        for (int gg = 0; gg < kPoolSplit; ++gg) total = __fadd_rn(total, part[gg][c]);
+        out[(head * nb + b) * kHeadDim + c] = __fdiv_rn(total, static_cast<float>(cnt));
+    }
+}
+
+__device__ __forceinline__ int64_t visible_blocks(int64_t qb, int64_t n, int64_t nkb, bool causal) {
+    if (!causal) return nkb;
+    const int64_t last = min((qb + 1) * kBlock, n) - 1;
+    return min(last / kBlock + 1, nkb);
+}
+
+// Order-preserving image of an fp32 score (larger float -> larger uint).
+// -0.0 is folded onto +0.0 first so equal scores get equal keys.
+__device__ __forceinline__ uint32_t order_key(float s) {
+    const uint32_t u = __float_as_uint(__fadd_rn(s, 0.0f));
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// Warp-level top-k over row[0..vis) held in shared memory: bisection on the
+// key bits finds T, the kk-th largest key; keys > T are kept, plus the first
+// (kk - #keys>T) keys == T in index order (index-ascending tie rule). Output
+// is compacted in ascending index order with ballots.
+__device__ void warp_select_row(const float* row, int vis, int kk, int64_t kmax,
+                                int32_t* __restrict__ idx_row) {
+    const int lane = threadIdx.x & 31;
+    uint32_t T = 0;
+    for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t trial = T | (1u << bit);
+        int c = 0;
+        for (int j = lane; j < vis; j += 32) c += order_key(row[j]) >= trial;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (c >= kk) T = trial;
+    }
+    int gt = 0;
+    for (int j = lane; j < vis; j += 32) gt += order_key(row[j]) > T;
+    gt = __reduce_add_sync(0xffffffffu, gt);
+    const int need = kk - gt;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    int written = 0, ties = 0;
+    for (int base = 0; base < vis; base += 32) {
+        const int j = base + lane;
+        const bool valid = j < vis;
+        const uint32_t key = valid ? order_key(row[j]) : 0u;
+        const bool eq = valid && key == T;
+        const uint32_t eq_mask = __ballot_sync(0xffffffffu, eq);
+        const int tie_rank = ties + __popc(eq_mask & lt_mask);
+        const bool sel = (valid && key > T) || (eq && tie_rank < need);
+        const uint32_t sel_mask = __ballot_sync(0xffffffffu, sel);
+        if (sel) idx_row[written + __popc(sel_mask & lt_mask)] = j;
+        written += __popc(sel_mask);
+        ties += __popc(eq_mask);
+    }
+    for (int64_t p = kk + lane; p < kmax; p += 32) idx_row[p] = -1;
+}
+
+constexpr int kSelThreads = 256;  // 8 warps
+constexpr int kRowsPerCta = 16;   // query blocks per CTA
+constexpr int kChunk = 64;        // key blocks per shared-memory chunk
+
+// One CTA: head h, query blocks [qb0, qb0+16). Scores for all visible key
+// blocks are built in shared memory with an FFMA micro-tile (2 rows x 2 key
+// blocks per thread, fmaf chain over c = 0..127 in order), then each warp
+// selects two rows.
+__global__ void __launch_bounds__(kSelThreads)
+    score_select_kernel(const float* __restrict__ qp, const float* __restrict__ kp, int hq,
+                        int hkv, int64_t n, int64_t nqb, int64_t nkb, int causal, float scale,
+                        HeadTable ht, int64_t kmax, float* __restrict__ scores_out, int select,
+                        int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
+    extern __shared__ __align__(16) float smem[];
+    float* Qs = smem;                          // [128 c][16 rows]
+    float* Ks = Qs + kHeadDim * kRowsPerCta;   // [128 c][64 key blocks]
+    float* S = Ks + kHeadDim * kChunk;         // [16 rows][nkb_pad]
+    const int64_t nkb_pad = (nkb + 3) & ~int64_t(3);
+
+    const int h = blockIdx.y;
+    const int g = ht.kv[h];
+    const int64_t qb0 = static_cast<int64_t>(blockIdx.x) * kRowsPerCta;
+    const int rows = static_cast<int>(min(static_cast<int64_t>(kRowsPerCta), nqb - qb0));
+    const int tid = threadIdx.x;
+
+    // Q tile, transposed to [c][row].
+    for (int f = tid; f < kRowsPerCta * kHeadDim; f += kSelThreads) {
+        const int r = f / kHeadDim, c = f % kHeadDim;
+        Qs[c * kRowsPerCta + r] = r < rows ? qp[((int64_t)h * nqb + qb0 + r) * kHeadDim + c] : 0.0f;
+    }
+    const int64_t vis_max = visible_blocks(qb0 + rows - 1, n, nkb, causal != 0);
+
+    const int rp = tid & 7;   // rows 2rp, 2rp+1
+    const int kq = tid >> 3;  // key blocks 2kq, 2kq+1 of the chunk
+    for (int64_t kc = 0; kc < vis_max; kc += kChunk) {
+        __syncthreads();  // previous chunk fully consumed (and Q tile visible)
+        // K chunk transposed to [c][kb]: a warp covers 32 consecutive key
+        // blocks at one column quad (conflict-free shared stores).
+        for (int f = tid; f < kChunk * (kHeadDim / 4); f += kSelThreads) {
+            const int kb = f % kChunk, c4 = f / kChunk;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (kc + kb < nkb) v = *reinterpret_cast<const float4*>(kp + ((int64_t)g * nkb + kc + kb) * kHeadDim + c4 * 4);
+            Ks[(c4 * 4 + 0) * kChunk + kb] = v.x;
+            Ks[(c4 * 4 + 1) * kChunk + kb] = v.y;
+            Ks[(c4 * 4 + 2) * kChunk + kb] = v.z;
+            Ks[(c4 * 4 + 3) * kChunk + kb] = v.w;
+        }
+        __syncthreads();
+        float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
+#pragma unroll 8
+        for (int c = 0; c < kHeadDim; ++c) {
+            const float2 q2 = *reinterpret_cast<const float2*>(Qs + c * kRowsPerCta + 2 * rp);
+            const float2 k2 = *reinterpret_cast<const float2*>(Ks + c * kChunk + 2 * kq);
+            a00 = __fmaf_rn(q2.x, k2.x, a00);
+            a01 = __fmaf_rn(q2.x, k2.y, a01);
+            a10 = __fmaf_rn(q2.y, k2.x, a10);
+            a11 = __fmaf_rn(q2.y, k2.y, a11);
+        }
+        const float a[2][2] = {{a00, a01}, {a10, a11}};
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int r = 2 * rp + i;
+            const int64_t vis = visible_blocks(qb0 + r, n, nkb, causal != 0);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int64_t kb = kc + 2 * kq + j;
+                if (kb < nkb) S[r * nkb_pad + kb] = kb < vis ? __fmul_rn(a[i][j], scale) : -INFINITY;
+            }
+        }
+    }
+    __syncthreads();
+
+    if (scores_out) {
+        for (int r = 0; r < rows; ++r) {
+            float* dst = scores_out + ((int64_t)h * nqb + qb0 + r) * nkb;
+            for (int64_t kb = tid; kb < nkb; kb += kSelThreads)
+                dst[kb] = kb < vis_max ? S[r * nkb_pad + kb] : -INFINITY;
+        }
+    }
+    if (!select) return;
+    const int warp = tid >> 5;
+    for (int r = warp; r < rows; r += kSelThreads / 32) {
+        const int64_t qb = qb0 + r;
+        const int vis = static_cast<int>(visible_blocks(qb, n, nkb, causal != 0));
+        const int kk = min(ht.k[h], vis);
+        warp_select_row(S + r * nkb_pad, vis, kk, kmax, idx + ((int64_t)h * nqb + qb) * kmax);
+        if ((tid & 31) == 0) cnt[(int64_t)h * nqb + qb] = kk;
+    }
+}
+
+// Standalone selector: one warp per (head, query block) row of a global score matrix.
+__global__ void __launch_bounds__(kSelThreads)
+    select_kernel(const float* __restrict__ scores, int hq, int64_t n, int64_t nqb, int64_t nkb,
+                  int causal, HeadTable ht, int64_t kmax, int32_t* __restrict__ idx,
+                  int32_t* __restrict__ cnt) {
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * (kSelThreads / 32) + (threadIdx.x >> 5);
+    if (row >= (int64_t)hq * nqb) return;
+    const int h = static_cast<int>(row / nqb);
+    const int64_t qb = row % nqb;
+    const int vis = static_cast<int>(visible_blocks(qb, n, nkb, causal != 0));
+    const int kk = min(ht.k[h], vis);
+    warp_select_row(scores + row * nkb, vis, kk, kmax, idx + row * kmax);
+    if ((threadIdx.x & 31) == 0) cnt[row] = kk;
+}
+
+__global__ void check_finite_kernel(const uint16_t* __restrict__ x, int64_t count,
+                                    int32_t* __restrict__ flag) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bad |= (x[i] & 0x7F80u) == 0x7F80u;  // bf16 exponent all ones: Inf or NaN
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+}  // namespace
+
+void launch_pool(const void* x, int heads, int64_t n, float* out, cudaStream_t s) {
+    const int64_t nb = (n + kBlock - 1) / kBlock;
+    pool_kernel<<<dim3(static_cast<unsigned>(nb), heads), kPoolThreads, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(x), n, out);
+}
+
+static size_t score_select_smem(int64_t nkb) {
+    const int64_t nkb_pad = (nkb + 3) & ~int64_t(3);
+    return sizeof(float) * (kHeadDim * kRowsPerCta + kHeadDim * kChunk + kRowsPerCta * nkb_pad);
+}
+
+void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n,
+                         bool causal, float scale, const HeadTable& ht, int64_t kmax,
+                         float* scores_out, bool select, int32_t* idx, int32_t* cnt,
+                         cudaStream_t s) {
+    const int64_t nqb = (n + kBlock - 1) / kBlock, nkb = nqb;
+    const size_t smem = score_select_smem(nkb);
+    cudaFuncSetAttribute(score_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    const dim3 grid(static_cast<unsigned>((nqb + kRowsPerCta - 1) / kRowsPerCta), hq);
+    score_select_kernel<<<grid, kSelThreads, smem, s>>>(qp, kp, hq, hkv, n, nqb, nkb, causal ? 1 : 0,
+                                                        scale, ht, kmax, scores_out, select ? 1 : 0,
+                                                        idx, cnt);
+}
+
+void launch_select_from_scores(const float* scores, int hq, int64_t n, bool causal,
+                               const HeadTable& ht, int64_t kmax, int32_t* idx, int32_t* cnt,
+                               cudaStream_t s) {
+    const int64_t nqb = (n + kBlock - 1) / kBlock, nkb = nqb;
+    const int64_t rows = (int64_t)hq * nqb;
+    const unsigned grid = static_cast<unsigned>((rows + (kSelThreads / 32) - 1) / (kSelThreads / 32));
+    select_kernel<<<grid, kSelThreads, 0, s>>>(scores, hq, n, nqb, nkb, causal ? 1 : 0, ht, kmax,
+                                               idx, cnt);
+}
+
+void launch_check_finite(const void* x, int64_t count, int32_t* flag, cudaStream_t s) {
+    check_finite_kernel<<<148 * 8, 256, 0, s>>>(static_cast<const uint16_t*>(x), count, flag);
+}
+
+}  // namespace shplb::kern

@@ -1,0 +1,60 @@
+// Internal launch interface between the C ABI (shplb_api.cpp) and the sm_100a
+// kernels. Host-callable, CUDA-runtime types only.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace shplb::kern {
+
+constexpr int kHeadDim = 128;   // d
+constexpr int kBlock = 128;     // bq = bk
+constexpr int kPoolSplit = 16;  // interleaved row groups of the pooled sum
+constexpr int kMaxHeads = 256;  // per-launch k-block table lives in the kernel parameters
+
+// Per-q-head table passed in kernel parameters.
+struct HeadTable {
+    int32_t k[kMaxHeads];   // key blocks to keep
+    int32_t kv[kMaxHeads];  // kv head read by this q head
+};
+
+// Kernel 1: x [heads][n][128] bf16 -> out [heads][ceil(n/128)][128] fp32 block means.
+void launch_pool(const void* x, int heads, int64_t n, float* out, cudaStream_t s);
+
+// Kernel 2 (fused score + select): pooled q [hq][nqb][128], pooled k
+// [hkv][nkb][128]; q head h scores against pooled kv head ht.kv[h]. scores_out (nullable) receives the full score matrix
+// [hq][nqb][nkb] (-inf where causally invisible). With select=true, idx/cnt
+// receive the per-(head, q block) top-k block lists.
+void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n,
+                         bool causal, float scale, const HeadTable& ht, int64_t kmax,
+                         float* scores_out, bool select, int32_t* idx, int32_t* cnt,
+                         cudaStream_t s);
+
+// Kernel 2 (standalone): selection from a precomputed score matrix.
+void launch_select_from_scores(const float* scores, int hq, int64_t n, bool causal,
+                               const HeadTable& ht, int64_t kmax, int32_t* idx, int32_t* cnt,
+                               cudaStream_t s);
+
+// Kernel 3: block-sparse FlashAttention prefill (tcgen05/TMEM/TMA).
+struct FaParams {
+    CUtensorMap tm_q;  // [hq][n][128] bf16, box {64,128,1}, 128B swizzle
+    CUtensorMap tm_k;  // [hkv][n][128]
+    CUtensorMap tm_v;  // [hkv][n][128]
+    void* out;         // [hq][n][128] bf16
+    const int32_t* idx;
+    const int32_t* cnt;
+    const int32_t* tiles;  // work list: tile t -> (h << 20) | qb, heaviest first
+    int64_t kmax;
+    int64_t n;
+    int32_t hq, hkv, nqb;
+    int32_t causal;
+    float scale_log2;  // (1/sqrt(d)) * log2(e)
+    HeadTable heads;   // kv head of each q head (k unused)
+};
+void launch_fa(const FaParams& p, int num_tiles, cudaStream_t s);
+
+// Validation: sets *flag to 1 if any element of x (count elements, bf16) is not finite.
+void launch_check_finite(const void* x, int64_t count, int32_t* flag, cudaStream_t s);
+
+}  // namespace shplb::kern

@@ -1,0 +1,460 @@
+// C ABI of the attention hot path (include/shplb.h): the per-device context,
+// shape/budget validation with the reference's messages, the work list for
+// kernel 3, TMA descriptor construction, and the kernel 1 -> 2 -> 3 sequence.
+//
+// Replaces headbal::sparse_attention / sparse_attention_all
+// (proj/include/headbal/attention.hpp:25,40-41; proj/src/attention.cpp:116-149,
+// 214-223) as driven per head with its own budget by run_skyline
+// (proj/src/commands.cpp:464-470).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+#include "kernels/kernels.hpp"
+#include "shplb.h"
+
+namespace shplb {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+void clear_last_error() { g_last_error.clear(); }
+
+#define SHPLB_CUDA(call)                                                                     \
+    do {                                                                                     \
+        cudaError_t _e = (call);                                                             \
+        if (_e != cudaSuccess)                                                               \
+            throw ::shplb::CudaError(std::string(#call) + ": " + cudaGetErrorString(_e));    \
+    } while (0)
+
+namespace {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable from the driver");
+    return fn;
+}
+
+// [heads][n][128] bf16 as a 3-D tensor map with a {64, 128, 1} box and 128-byte
+// swizzle: one box is one 128-row x 128-byte UMMA K-major chunk. Rows past n
+// are zero-filled on load and clipped on store.
+CUtensorMap make_tmap(const void* base, int64_t heads, int64_t n) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kern::kHeadDim), static_cast<cuuint64_t>(n),
+                                static_cast<cuuint64_t>(heads)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(kern::kHeadDim) * 2,
+                                   static_cast<cuuint64_t>(n) * kern::kHeadDim * 2};
+    const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kern::kBlock), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                                      const_cast<void*>(base), dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int64_t visible_blocks(int64_t qb, int64_t n, bool causal) {
+    const int64_t nkb = cdiv(n, kern::kBlock);
+    if (!causal) return nkb;
+    const int64_t last = std::min((qb + 1) * kern::kBlock, n) - 1;
+    return std::min(last / kern::kBlock + 1, nkb);
+}
+
+void check_shape(const shplb_layer_shape* s) {
+    if (!s) throw InvalidArgument("shape is null");
+    if (s->num_q_heads < 1 || s->num_kv_heads < 1)
+        throw InvalidArgument("workload must have at least one head");
+    if (!s->kv_head_of_q && s->num_q_heads % s->num_kv_heads != 0) {
+        throw InvalidArgument("num_q_heads (" + std::to_string(s->num_q_heads) +
+                              ") must be a multiple of num_kv_heads (" +
+                              std::to_string(s->num_kv_heads) + ")");
+    }
+    if (s->seq_len < 1) throw InvalidArgument("K must hold at least one key token");
+    if (s->num_q_heads > kern::kMaxHeads)
+        throw NotSupported("at most " + std::to_string(kern::kMaxHeads) + " query heads per call");
+    if (s->head_dim != kern::kHeadDim)
+        throw NotSupported("head_dim " + std::to_string(s->head_dim) + " not supported (kernels are built for 128)");
+    if (s->block_q != kern::kBlock || s->block_k != kern::kBlock)
+        throw NotSupported("block sizes must be 128 x 128");
+    if (s->kind != SHPLB_BLOCK_TOPK) throw NotSupported("selection kind not supported");
+    if (s->seq_len > (int64_t(1) << 26)) throw NotSupported("seq_len too large");
+}
+
+void check_ptr(const void* p, const char* what) {
+    if (!p) throw InvalidArgument(std::string(what) + " is null");
+    if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
+        throw InvalidArgument(std::string(what) + " must be 16-byte aligned");
+}
+
+// kv head of each q head: the caller's map, or the contiguous GQA grouping.
+void fill_kv_map(const shplb_layer_shape* s, kern::HeadTable& ht) {
+    const int group = s->num_q_heads / s->num_kv_heads;
+    for (int h = 0; h < s->num_q_heads; ++h) {
+        const int g = s->kv_head_of_q ? s->kv_head_of_q[h] : h / group;
+        if (g < 0 || g >= s->num_kv_heads) {
+            throw InvalidArgument("head " + std::to_string(h) + ": kv head " + std::to_string(g) +
+                                  " out of range [0, " + std::to_string(s->num_kv_heads) + ")");
+        }
+        ht.kv[h] = g;
+    }
+}
+
+// check_budget (attention.cpp:75-80), per head; returns blocks kept per head.
+kern::HeadTable budgets_to_blocks(const shplb_layer_shape* s, const int64_t* budgets,
+                                  std::vector<int32_t>& kb_out) {
+    if (!budgets) throw InvalidArgument("budgets is null");
+    kern::HeadTable kb{};
+    fill_kv_map(s, kb);
+    const int64_t nkb = cdiv(s->seq_len, kern::kBlock);
+    kb_out.resize(static_cast<size_t>(s->num_q_heads));
+    for (int h = 0; h < s->num_q_heads; ++h) {
+        const int64_t b = budgets[h];
+        if (b < 1 || b > s->seq_len) {
+            throw InvalidArgument("head " + std::to_string(h) + ": budget k = " + std::to_string(b) +
+                                  " out of range [1, " + std::to_string(s->seq_len) + "]");
+        }
+        kb.k[h] = static_cast<int32_t>(std::min(nkb, cdiv(b, kern::kBlock)));
+        kb_out[h] = kb.k[h];
+    }
+    return kb;
+}
+
+}  // namespace
+}  // namespace shplb
+
+struct shplb_ctx {
+    int device = 0;
+    std::atomic<int64_t> launches{0};
+    // workspace (grown on demand)
+    float* qp = nullptr;
+    size_t qp_bytes = 0;
+    float* kp = nullptr;
+    size_t kp_bytes = 0;
+    int32_t* idx = nullptr;
+    size_t idx_bytes = 0;
+    int32_t* cnt = nullptr;
+    size_t cnt_bytes = 0;
+    int32_t* flag = nullptr;
+    int64_t last_kmax = 0;
+    // Kernel-3 work lists, one per (seq_len, causal, blocks-per-head) seen.
+    // Never overwritten, so an in-flight launch never sees its list change.
+    struct WorkList {
+        int32_t* tiles = nullptr;
+        int num_tiles = 0;
+    };
+    std::map<std::vector<int64_t>, WorkList> work_lists;
+    const WorkList* current = nullptr;
+};
+
+namespace shplb {
+namespace {
+
+template <typename T>
+void grow(T*& p, size_t& cap, size_t bytes) {
+    if (bytes <= cap) return;
+    if (p) SHPLB_CUDA(cudaFree(p));
+    p = nullptr;
+    SHPLB_CUDA(cudaMalloc(&p, bytes));
+    cap = bytes;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        SHPLB_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) SHPLB_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+void check_launch(shplb_ctx* ctx, int n = 1) {
+    SHPLB_CUDA(cudaGetLastError());
+    ctx->launches += n;
+}
+
+void validate_inputs(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const void* k,
+                     const void* v, cudaStream_t st) {
+    SHPLB_CUDA(cudaMemsetAsync(ctx->flag, 0, 3 * sizeof(int32_t), st));
+    const int64_t qn = int64_t(s->num_q_heads) * s->seq_len * s->head_dim;
+    const int64_t kn = int64_t(s->num_kv_heads) * s->seq_len * s->head_dim;
+    kern::launch_check_finite(q, qn, ctx->flag + 0, st);
+    if (k) kern::launch_check_finite(k, kn, ctx->flag + 1, st);
+    if (v) kern::launch_check_finite(v, kn, ctx->flag + 2, st);
+    check_launch(ctx, 1 + (k != nullptr) + (v != nullptr));
+    int32_t f[3];
+    SHPLB_CUDA(cudaMemcpyAsync(f, ctx->flag, sizeof f, cudaMemcpyDeviceToHost, st));
+    SHPLB_CUDA(cudaStreamSynchronize(st));
+    // validate_head's messages (workload.cpp:56-58).
+    if (f[0]) throw InvalidArgument("Q contains NaN or Inf");
+    if (k && f[1]) throw InvalidArgument("K contains NaN or Inf");
+    if (v && f[2]) throw InvalidArgument("V contains NaN or Inf");
+}
+
+void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const void* k,
+                    const kern::HeadTable& kb, int64_t kmax, float* scores_out, bool select,
+                    int32_t* idx, int32_t* cnt, cudaStream_t st) {
+    const int64_t nb = cdiv(s->seq_len, kern::kBlock);
+    grow(ctx->qp, ctx->qp_bytes, sizeof(float) * s->num_q_heads * nb * kern::kHeadDim);
+    grow(ctx->kp, ctx->kp_bytes, sizeof(float) * s->num_kv_heads * nb * kern::kHeadDim);
+    kern::launch_pool(q, s->num_q_heads, s->seq_len, ctx->qp, st);
+    kern::launch_pool(k, s->num_kv_heads, s->seq_len, ctx->kp, st);
+    const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(s->head_dim)));
+    kern::launch_score_select(ctx->qp, ctx->kp, s->num_q_heads, s->num_kv_heads, s->seq_len,
+                              s->causal != 0, scale, kb, kmax, scores_out, select, idx, cnt, st);
+    check_launch(ctx, 3);
+}
+
+// Kernel-3 work list: every (head, query block) tile, heaviest first (LPT), so
+// the hardware block scheduler hands out long tiles before short ones.
+void build_tiles(shplb_ctx* ctx, const shplb_layer_shape* s, const std::vector<int32_t>& kblocks) {
+    std::vector<int64_t> key = {s->seq_len, s->causal};
+    key.insert(key.end(), kblocks.begin(), kblocks.end());
+    auto it = ctx->work_lists.find(key);
+    if (it != ctx->work_lists.end()) {
+        ctx->current = &it->second;
+        return;
+    }
+    const int64_t nqb = cdiv(s->seq_len, kern::kBlock);
+    std::vector<int32_t> tiles;
+    std::vector<int32_t> work;
+    tiles.reserve(static_cast<size_t>(s->num_q_heads * nqb));
+    for (int h = 0; h < s->num_q_heads; ++h)
+        for (int64_t qb = 0; qb < nqb; ++qb) {
+            tiles.push_back((h << 20) | static_cast<int32_t>(qb));
+            work.push_back(static_cast<int32_t>(std::min<int64_t>(kblocks[h], visible_blocks(qb, s->seq_len, s->causal != 0))));
+        }
+    std::vector<size_t> order(tiles.size());
+    std::iota(order.begin(), order.end(), size_t{0});
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return work[a] > work[b]; });
+    std::vector<int32_t> sorted(tiles.size());
+    for (size_t i = 0; i < order.size(); ++i) sorted[i] = tiles[order[i]];
+    shplb_ctx::WorkList wl;
+    SHPLB_CUDA(cudaMalloc(&wl.tiles, sizeof(int32_t) * sorted.size()));
+    SHPLB_CUDA(cudaMemcpy(wl.tiles, sorted.data(), sizeof(int32_t) * sorted.size(), cudaMemcpyHostToDevice));
+    wl.num_tiles = static_cast<int>(sorted.size());
+    ctx->current = &(ctx->work_lists[key] = wl);
+}
+
+void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const void* k,
+            const void* v, const int32_t* idx, const int32_t* cnt, int64_t kmax, void* out,
+            cudaStream_t st) {
+    kern::FaParams p;
+    std::memset(&p, 0, sizeof p);
+    p.tm_q = make_tmap(q, s->num_q_heads, s->seq_len);
+    p.tm_k = make_tmap(k, s->num_kv_heads, s->seq_len);
+    p.tm_v = make_tmap(v, s->num_kv_heads, s->seq_len);
+    p.out = out;
+    p.idx = idx;
+    p.cnt = cnt;
+    p.tiles = ctx->current->tiles;
+    p.kmax = kmax;
+    p.n = s->seq_len;
+    p.hq = s->num_q_heads;
+    p.hkv = s->num_kv_heads;
+    p.nqb = static_cast<int32_t>(cdiv(s->seq_len, kern::kBlock));
+    p.causal = s->causal;
+    fill_kv_map(s, p.heads);
+    p.scale_log2 = static_cast<float>((1.0 / std::sqrt(static_cast<double>(s->head_dim))) * 1.4426950408889634);
+    kern::launch_fa(p, ctx->current->num_tiles, st);
+    check_launch(ctx);
+}
+
+}  // namespace
+}  // namespace shplb
+
+using namespace shplb;
+
+extern "C" {
+
+const char* shplb_last_error(void) { return shplb::g_last_error.c_str(); }
+
+const char* shplb_version(void) { return "shplb-b200 0.1.0 sm_100a"; }
+
+int shplb_ctx_create(int device, shplb_ctx** ctx_out) {
+    return guarded([&] {
+        require(ctx_out != nullptr, "ctx_out is null");
+        int count = 0;
+        SHPLB_CUDA(cudaGetDeviceCount(&count));
+        if (device < 0 || device >= count)
+            throw InvalidArgument("device " + std::to_string(device) + " out of range");
+        cudaDeviceProp prop;
+        SHPLB_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10 || prop.minor != 0)
+            throw NotSupported(std::string("shplb kernels are built for sm_100a; device is ") + prop.name);
+        DeviceGuard g(device);
+        auto* ctx = new shplb_ctx();
+        ctx->device = device;
+        SHPLB_CUDA(cudaMalloc(&ctx->flag, 4 * sizeof(int32_t)));
+        *ctx_out = ctx;
+    });
+}
+
+int shplb_ctx_destroy(shplb_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        DeviceGuard g(ctx->device);
+        cudaFree(ctx->qp);
+        cudaFree(ctx->kp);
+        cudaFree(ctx->idx);
+        cudaFree(ctx->cnt);
+        for (auto& kv : ctx->work_lists) cudaFree(kv.second.tiles);
+        cudaFree(ctx->flag);
+        delete ctx;
+    });
+}
+
+int64_t shplb_ctx_launch_count(const shplb_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+int shplb_block_scores(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
+                       const void* k, float* scores_out, void* stream) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx is null");
+        check_shape(shape);
+        check_ptr(q, "q");
+        check_ptr(k, "k");
+        check_ptr(scores_out, "scores_out");
+        DeviceGuard g(ctx->device);
+        auto st = static_cast<cudaStream_t>(stream);
+        if (shape->validate) validate_inputs(ctx, shape, q, k, nullptr, st);
+        kern::HeadTable kb{};
+        fill_kv_map(shape, kb);
+        pool_and_score(ctx, shape, q, k, kb, 1, scores_out, false, nullptr, nullptr, st);
+    });
+}
+
+int shplb_select_blocks(shplb_ctx* ctx, const shplb_layer_shape* shape, const float* scores,
+                        const int64_t* k_blocks, int64_t kmax, int32_t* idx_out, int32_t* cnt_out,
+                        void* stream) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx is null");
+        check_shape(shape);
+        require(scores && idx_out && cnt_out && k_blocks, "null pointer argument");
+        const int64_t nkb = cdiv(shape->seq_len, kern::kBlock);
+        kern::HeadTable kb{};
+        fill_kv_map(shape, kb);
+        int64_t need = 1;
+        for (int h = 0; h < shape->num_q_heads; ++h) {
+            if (k_blocks[h] < 1 || k_blocks[h] > nkb) {
+                throw InvalidArgument("head " + std::to_string(h) + ": budget k = " +
+                                      std::to_string(k_blocks[h]) + " out of range [1, " +
+                                      std::to_string(nkb) + "]");
+            }
+            kb.k[h] = static_cast<int32_t>(k_blocks[h]);
+            need = std::max<int64_t>(need, k_blocks[h]);
+        }
+        if (kmax < need) throw InvalidArgument("kmax " + std::to_string(kmax) + " < largest k " + std::to_string(need));
+        DeviceGuard g(ctx->device);
+        kern::launch_select_from_scores(scores, shape->num_q_heads, shape->seq_len, shape->causal != 0,
+                                        kb, kmax, idx_out, cnt_out, static_cast<cudaStream_t>(stream));
+        check_launch(ctx);
+    });
+}
+
+int shplb_block_sparse_attention(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
+                                 const void* k, const void* v, const int32_t* idx,
+                                 const int32_t* cnt, int64_t kmax, void* out, void* stream) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx is null");
+        check_shape(shape);
+        check_ptr(q, "q");
+        check_ptr(k, "k");
+        check_ptr(v, "v");
+        check_ptr(out, "out");
+        require(idx && cnt && kmax >= 1, "null selection or kmax < 1");
+        DeviceGuard g(ctx->device);
+        auto st = static_cast<cudaStream_t>(stream);
+        if (shape->validate) validate_inputs(ctx, shape, q, k, v, st);
+        // Without budgets the work list orders tiles by causal visibility only.
+        std::vector<int32_t> kbl(static_cast<size_t>(shape->num_q_heads), static_cast<int32_t>(kmax));
+        build_tiles(ctx, shape, kbl);
+        run_fa(ctx, shape, q, k, v, idx, cnt, kmax, out, st);
+    });
+}
+
+int shplb_sparse_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
+                                 const void* k, const void* v, const int64_t* budgets_tokens,
+                                 void* out, void* stream) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx is null");
+        check_shape(shape);
+        check_ptr(q, "q");
+        check_ptr(k, "k");
+        check_ptr(v, "v");
+        check_ptr(out, "out");
+        std::vector<int32_t> kbl;
+        const kern::HeadTable kb = budgets_to_blocks(shape, budgets_tokens, kbl);
+        const int64_t kmax = *std::max_element(kbl.begin(), kbl.end());
+        DeviceGuard g(ctx->device);
+        auto st = static_cast<cudaStream_t>(stream);
+        if (shape->validate) validate_inputs(ctx, shape, q, k, v, st);
+        const int64_t nqb = cdiv(shape->seq_len, kern::kBlock);
+        grow(ctx->idx, ctx->idx_bytes, sizeof(int32_t) * shape->num_q_heads * nqb * kmax);
+        grow(ctx->cnt, ctx->cnt_bytes, sizeof(int32_t) * shape->num_q_heads * nqb);
+        build_tiles(ctx, shape, kbl);
+        pool_and_score(ctx, shape, q, k, kb, kmax, nullptr, true, ctx->idx, ctx->cnt, st);
+        run_fa(ctx, shape, q, k, v, ctx->idx, ctx->cnt, kmax, out, st);
+        ctx->last_kmax = kmax;
+    });
+}
+
+int shplb_last_selection(const shplb_ctx* ctx, const int32_t** idx, const int32_t** cnt,
+                         int64_t* kmax) {
+    return guarded([&] {
+        require(ctx != nullptr && ctx->last_kmax > 0, "no layer call on this context yet");
+        if (idx) *idx = ctx->idx;
+        if (cnt) *cnt = ctx->cnt;
+        if (kmax) *kmax = ctx->last_kmax;
+    });
+}
+
+int shplb_layer_work(const shplb_layer_shape* shape, const int64_t* budgets_tokens,
+                     int64_t* selected_tiles_out, double* flops_out) {
+    return guarded([&] {
+        check_shape(shape);
+        std::vector<int32_t> kbl;
+        budgets_to_blocks(shape, budgets_tokens, kbl);
+        const int64_t nqb = cdiv(shape->seq_len, kern::kBlock);
+        int64_t tiles = 0;
+        for (int h = 0; h < shape->num_q_heads; ++h)
+            for (int64_t qb = 0; qb < nqb; ++qb)
+                tiles += std::min<int64_t>(kbl[h], visible_blocks(qb, shape->seq_len, shape->causal != 0));
+        if (selected_tiles_out) *selected_tiles_out = tiles;
+        if (flops_out)
+            *flops_out = 4.0 * shape->head_dim * double(kern::kBlock) * double(kern::kBlock) * double(tiles);
+    });
+}
+
+}  // extern "C"
