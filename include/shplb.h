@@ -134,6 +134,14 @@ int shplb_ctx_destroy(shplb_ctx* ctx);
 /* Number of kernel launches the context issued since creation (all kinds). */
 int64_t shplb_ctx_launch_count(const shplb_ctx* ctx);
 
+/* Stage timing. While enabled, every shplb_sparse_attention_layer call records
+ * CUDA events on its stream around kernel 1 (pooling), kernel 2 (score +
+ * select) and kernel 3 (attention). shplb_ctx_read_timing synchronises on
+ * those events, writes up to max_calls rows of {k1_ms, k2_ms, k3_ms} (one per
+ * call since timing was enabled or last read) and resets the record. */
+int shplb_ctx_set_timing(shplb_ctx* ctx, int enable);
+int shplb_ctx_read_timing(shplb_ctx* ctx, double* stage_ms, int max_calls, int* n_calls_out);
+
 enum { SHPLB_BLOCK_TOPK = 0 }; /* selection kind: per (head, query block) top-k key blocks */
 
 /* One attention layer. q: bf16 [num_q_heads][seq_len][head_dim],
@@ -192,11 +200,26 @@ int shplb_sparse_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape,
                                  const void* k, const void* v,
                                  const int64_t* budgets_tokens, void* out, void* stream);
 
+/* Same layer call on HOST buffers (bf16 bit patterns, same layouts): copies q/k/v
+ * host->device into context-owned device memory, runs kernels 1-3, copies out
+ * device->host and synchronises the stream. Pinned host memory makes the
+ * copies asynchronous DMA. This is the entry a host-side caller of the
+ * reference API binds. */
+int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* shape,
+                                      const uint16_t* q_host, const uint16_t* k_host,
+                                      const uint16_t* v_host, const int64_t* budgets_tokens,
+                                      uint16_t* out_host, void* stream);
+
 /* Device pointers of the selection made by the last shplb_sparse_attention_layer
  * call on this context (valid until the next call): idx [Hq][nqb][kmax],
  * cnt [Hq][nqb]. */
 int shplb_last_selection(const shplb_ctx* ctx, const int32_t** idx, const int32_t** cnt,
                          int64_t* kmax);
+
+/* Copies that selection into caller device buffers (async on stream):
+ * idx_dst must hold idx_elems >= Hq*nqb*kmax int32, cnt_dst cnt_elems >= Hq*nqb. */
+int shplb_copy_last_selection(const shplb_ctx* ctx, int32_t* idx_dst, int64_t idx_elems,
+                              int32_t* cnt_dst, int64_t cnt_elems, void* stream);
 
 /* Algorithmic work of one layer call, for roofline accounting:
  * selected (head, q-block, k-block) tiles, and the FLOPs 4*d*bq*bk*tiles. */

@@ -50,20 +50,17 @@ def _load_oracle():
         L.orc_pool_blocks.argtypes = [_u16p, C.c_int64, C.c_int32, C.c_int32, _f32p]
         L.orc_score_scale.argtypes = [C.c_int32]
         L.orc_score_scale.restype = C.c_float
-        L.orc_visible_blocks.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int]
-        L.orc_visible_blocks.restype = C.c_int64
-        L.orc_block_scores.argtypes = [_f32p, _f32p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
-                                       C.c_int, _f32p]
-        L.orc_score_rows.argtypes = [_f32p, _f32p, C.c_int64, C.c_int64, C.c_int32, _f32p]
-        L.orc_select_topk.argtypes =[_f32p, C.c_int64, C.c_int32, C.c_int32, C.c_int, C.c_int64,
-                                      C.c_int64, _i32p, _i32p]
-        L.orc_topk_row.argtypes = [_f64p, C.c_int64, C.c_int64, _i64p]
-        L.orc_block_sparse_attention.argtypes = [_u16p, _u16p, _u16p, C.c_int64, C.c_int32,
-                                                 C.c_int32, C.c_int32, C.c_int, _i32p, _i32p,
-                                                 C.c_int64, _f64p]
-        L.orc_layer.argtypes = [_u16p, _u16p, _u16p, C.c_int32, C.c_int32, C.c_int64, C.c_int32,
-                                C.c_int32, C.c_int32, C.c_int, _i64p, C.c_int64, _f32p, _i32p,
-                                _i32p, C.c_void_p]
+        i64, i32 = C.c_int64, C.c_int32
+        L.orc_visible_blocks.argtypes = [i64, i64, i64, i32, i32, C.c_int]
+        L.orc_visible_blocks.restype = i64
+        L.orc_block_scores.argtypes = [_f32p, _f32p, i64, i64, i32, i32, i32, C.c_int, _f32p]
+        L.orc_score_rows.argtypes = [_f32p, _f32p, i64, i64, i32, _f32p]
+        L.orc_select_topk.argtypes = [_f32p, i64, i64, i32, i32, C.c_int, i64, i64, _i32p, _i32p]
+        L.orc_topk_row.argtypes = [_f64p, i64, i64, _i64p]
+        L.orc_block_sparse_attention.argtypes = [_u16p, _u16p, _u16p, i64, i64, i32, i32, i32,
+                                                 C.c_int, _i32p, _i32p, i64, _f64p]
+        L.orc_layer.argtypes = [_u16p, _u16p, _u16p, i32, i32, i64, i64, i32, i32, i32, C.c_int,
+                                _i64p, i64, _f32p, _i32p, _i32p, C.c_void_p]
         L.orc_recovery_at.argtypes = [_i64p, _f64p, C.c_int64, C.c_int64]
         L.orc_recovery_at.restype = C.c_double
         L.orc_uniform_allocate.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, _i64p]
@@ -96,6 +93,8 @@ def _load_ref():
         L.ref_dense_attention.argtypes = attn + [C.c_int, C.c_void_p, _f64p]
         L.ref_sparse_attention.argtypes = attn + [C.c_int, C.c_int64, C.c_int, _f64p]
         L.ref_serial_sparse_attention.argtypes = attn + [C.c_int, C.c_int64, C.c_int, _f64p]
+        L.ref_sparse_attention_timed.argtypes = attn + [C.c_int, C.c_int64, C.c_int, _f64p,
+                                                        C.POINTER(C.c_double)]
         L.ref_recovery_ratio.argtypes = [_f64p, C.c_int64, C.c_int64, C.c_int64, C.c_int,
                                          C.POINTER(C.c_double)]
         L.ref_build_profiles.argtypes = [_f64p, _f64p, _f64p, C.c_int32, C.c_int64, C.c_int64,
@@ -164,27 +163,31 @@ def score_scale(d: int) -> float:
     return float(_load_oracle().orc_score_scale(d))
 
 
-def visible_blocks(qb: int, n: int, bq: int, bk: int, causal: bool) -> int:
-    return int(_load_oracle().orc_visible_blocks(qb, n, bq, bk, int(causal)))
+def visible_blocks(qb: int, n: int, bq: int, bk: int, causal: bool, n_k: int = None) -> int:
+    """Key blocks visible to query block qb (n query rows, n_k keys, default n_k = n)."""
+    return int(_load_oracle().orc_visible_blocks(qb, n, n if n_k is None else n_k, bq, bk,
+                                                 int(causal)))
 
 
 def block_scores(qp: np.ndarray, kp: np.ndarray, n: int, bq: int, bk: int,
-                 causal: bool) -> np.ndarray:
+                 causal: bool, n_k: int = None) -> np.ndarray:
     d = qp.shape[1]
-    out = np.empty((nblocks(n, bq), nblocks(n, bk)), np.float32)
+    n_k = n if n_k is None else n_k
+    out = np.empty((nblocks(n, bq), nblocks(n_k, bk)), np.float32)
     _load_oracle().orc_block_scores(np.ascontiguousarray(qp, np.float32),
-                                    np.ascontiguousarray(kp, np.float32), n, d, bq, bk,
+                                    np.ascontiguousarray(kp, np.float32), n, n_k, d, bq, bk,
                                     int(causal), out)
     return out
 
 
 def select_topk(scores: np.ndarray, n: int, bq: int, bk: int, causal: bool, k_blocks: int,
-                kmax: int):
+                kmax: int, n_k: int = None):
     nqb = nblocks(n, bq)
     idx = np.empty((nqb, kmax), np.int32)
     cnt = np.empty(nqb, np.int32)
-    _load_oracle().orc_select_topk(np.ascontiguousarray(scores, np.float32), n, bq, bk,
-                                   int(causal), k_blocks, kmax, idx, cnt)
+    _load_oracle().orc_select_topk(np.ascontiguousarray(scores, np.float32), n,
+                                   n if n_k is None else n_k, bq, bk, int(causal), k_blocks,
+                                   kmax, idx, cnt)
     return idx, cnt
 
 
@@ -199,15 +202,15 @@ def layer(q_bits, k_bits, v_bits, k_blocks, *, bq=128, bk=128, causal=True, kmax
           with_output=True):
     """Whole layer: pooled scores, selections and fp64 outputs for every q head.
 
-    q_bits [Hq, n, d], k_bits/v_bits [Hkv, n, d] (bf16 bit patterns);
+    q_bits [Hq, n_q, d], k_bits/v_bits [Hkv, n_k, d] (bf16 bit patterns);
     k_blocks [Hq] per-head budgets in blocks.
     """
     q_bits = np.ascontiguousarray(q_bits, np.uint16)
     k_bits = np.ascontiguousarray(k_bits, np.uint16)
     v_bits = np.ascontiguousarray(v_bits, np.uint16)
     hq, n, d = q_bits.shape
-    hkv = k_bits.shape[0]
-    nqb, nkb = nblocks(n, bq), nblocks(n, bk)
+    hkv, n_k = k_bits.shape[0], k_bits.shape[1]
+    nqb, nkb = nblocks(n, bq), nblocks(n_k, bk)
     k_blocks = np.ascontiguousarray(k_blocks, np.int64)
     if kmax is None:
         kmax = int(min(nkb, k_blocks.max()))
@@ -215,7 +218,7 @@ def layer(q_bits, k_bits, v_bits, k_blocks, *, bq=128, bk=128, causal=True, kmax
     idx = np.empty((hq, nqb, kmax), np.int32)
     cnt = np.empty((hq, nqb), np.int32)
     out = np.empty((hq, n, d), np.float64) if with_output else None
-    _load_oracle().orc_layer(q_bits, k_bits, v_bits, hq, hkv, n, d, bq, bk, int(causal),
+    _load_oracle().orc_layer(q_bits, k_bits, v_bits, hq, hkv, n, n_k, d, bq, bk, int(causal),
                              k_blocks, kmax, scores, idx, cnt,
                              out.ctypes.data if with_output else None)
     return scores, idx, cnt, out
@@ -349,6 +352,17 @@ class ref:
         _ref_check(fn(Q, K, V, Q.shape[0], K.shape[0], Q.shape[1], V.shape[1], kind, budget,
                       int(causal), out))
         return out
+
+    @staticmethod
+    def sparse_attention_timed(Q, K, V, budget, causal=False, kind=0):
+        """(output, seconds spent inside headbal::sparse_attention)."""
+        Q, K, V = (np.ascontiguousarray(a, np.float64) for a in (Q, K, V))
+        out = np.empty((Q.shape[0], V.shape[1]), np.float64)
+        sec = C.c_double()
+        _ref_check(_load_ref().ref_sparse_attention_timed(
+            Q, K, V, Q.shape[0], K.shape[0], Q.shape[1], V.shape[1], kind, budget, int(causal),
+            out, C.byref(sec)))
+        return out, float(sec.value)
 
     @staticmethod
     def build_profiles(Q, K, V, grid, causal=False, kind=0):

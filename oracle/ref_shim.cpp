@@ -11,6 +11,7 @@
 // Matrices cross the boundary as row-major fp64 buffers, the reference's own
 // Matrix layout (proj/include/headbal/matrix.hpp:9-28).
 
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -114,7 +115,27 @@ int ref_sparse_attention(const double* q, const double* k, const double* v, int6
     });
 }
 
-// headbal::reference::sparse_attention (reference.cpp:94-141), the serial path.
+// Same call, but only the headbal::sparse_attention call itself is timed
+// (steady_clock, like bench/bench_attention.cpp:18-22); the fp64 HeadData
+// construction of this shim is excluded. Used for the CPU-baseline arm.
+int ref_sparse_attention_timed(const double* q, const double* k, const double* v, int64_t n_q,
+                               int64_t n_k, int64_t d, int64_t d_v, int kind, int64_t budget,
+                               int causal, double* out, double* seconds_out) {
+    return guarded([&] {
+        const headbal::SelectionPolicy policy{
+            kind == 0 ? headbal::SelectionKind::PerQueryTopK
+                      : headbal::SelectionKind::ColumnAggregateTopK,
+            budget};
+        const headbal::HeadData head = to_head(q, k, v, n_q, n_k, d, d_v);
+        const auto t0 = std::chrono::steady_clock::now();
+        const headbal::Matrix m = headbal::sparse_attention(head, policy, causal != 0);
+        const auto t1 = std::chrono::steady_clock::now();
+        *seconds_out = std::chrono::duration<double>(t1 - t0).count();
+        copy_out(m, out);
+    });
+}
+
+// headbal::reference::sparse_attention (reference.cpp:74-123), the serial path.
 int ref_serial_sparse_attention(const double* q, const double* k, const double* v, int64_t n_q,
                                 int64_t n_k, int64_t d, int64_t d_v, int kind, int64_t budget,
                                 int causal, double* out) {

@@ -78,24 +78,26 @@ void orc_pool_blocks(const uint16_t* x, int64_t n, int32_t d, int32_t block, flo
 
 float orc_score_scale(int32_t d) { return (float)(1.0 / sqrt((double)d)); }
 
-/* Number of key blocks visible to query block qb. */
-int64_t orc_visible_blocks(int64_t qb, int64_t n, int32_t bq, int32_t bk, int causal) {
-    const int64_t nkb = (n + bk - 1) / bk;
+/* Number of key blocks visible to query block qb (n_q query rows, n_k keys;
+ * the causal mask is top-left aligned: query i sees keys 0..i). */
+int64_t orc_visible_blocks(int64_t qb, int64_t n_q, int64_t n_k, int32_t bq, int32_t bk,
+                           int causal) {
+    const int64_t nkb = (n_k + bk - 1) / bk;
     if (!causal) return nkb;
     int64_t last = (qb + 1) * bq;
-    if (last > n) last = n;
+    if (last > n_q) last = n_q;
     last -= 1;
     int64_t v = last / bk + 1;
     return v < nkb ? v : nkb;
 }
 
 /* qp: [nqb][d], kp: [nkb][d] -> scores [nqb][nkb]; masked blocks are -inf. */
-void orc_block_scores(const float* qp, const float* kp, int64_t n, int32_t d, int32_t bq,
-                      int32_t bk, int causal, float* scores) {
-    const int64_t nqb = (n + bq - 1) / bq, nkb = (n + bk - 1) / bk;
+void orc_block_scores(const float* qp, const float* kp, int64_t n_q, int64_t n_k, int32_t d,
+                      int32_t bq, int32_t bk, int causal, float* scores) {
+    const int64_t nqb = (n_q + bq - 1) / bq, nkb = (n_k + bk - 1) / bk;
     const float scale = orc_score_scale(d);
     for (int64_t qb = 0; qb < nqb; ++qb) {
-        const int64_t vis = orc_visible_blocks(qb, n, bq, bk, causal);
+        const int64_t vis = orc_visible_blocks(qb, n_q, n_k, bq, bk, causal);
         for (int64_t kb = 0; kb < nkb; ++kb) {
             float acc = 0.0f;
             for (int32_t c = 0; c < d; ++c) acc = fmaf(qp[qb * d + c], kp[kb * d + c], acc);
@@ -139,12 +141,12 @@ static int cmp_i32(const void* a, const void* b) {
 
 /* One head: scores [nqb][nkb]; k_blocks is that head's budget in blocks.
  * idx: [nqb][kmax] ascending block ids (unused tail = -1), cnt: [nqb]. */
-void orc_select_topk(const float* scores, int64_t n, int32_t bq, int32_t bk, int causal,
-                     int64_t k_blocks, int64_t kmax, int32_t* idx, int32_t* cnt) {
-    const int64_t nqb = (n + bq - 1) / bq, nkb = (n + bk - 1) / bk;
+void orc_select_topk(const float* scores, int64_t n_q, int64_t n_k, int32_t bq, int32_t bk,
+                     int causal, int64_t k_blocks, int64_t kmax, int32_t* idx, int32_t* cnt) {
+    const int64_t nqb = (n_q + bq - 1) / bq, nkb = (n_k + bk - 1) / bk;
     scored* buf = (scored*)malloc(sizeof(scored) * (size_t)nkb);
     for (int64_t qb = 0; qb < nqb; ++qb) {
-        const int64_t vis = orc_visible_blocks(qb, n, bq, bk, causal);
+        const int64_t vis = orc_visible_blocks(qb, n_q, n_k, bq, bk, causal);
         const int64_t kk = k_blocks < vis ? k_blocks : vis;
         for (int64_t j = 0; j < vis; ++j) {
             buf[j].v = scores[qb * nkb + j];
@@ -196,25 +198,25 @@ void orc_topk_row(const double* values, int64_t n, int64_t k, int64_t* out) {
 
 /* --- attention output on the kept set -------------------------------------- */
 
-/* One q head / its kv head. q: [n][d], k/v: [n][d] bf16 bits. idx/cnt from
- * orc_select_topk. out: [n][d] fp64. Follows softmax_weighted_sum
+/* One q head / its kv head. q: [n_q][d], k/v: [n_k][d] bf16 bits. idx/cnt
+ * from orc_select_topk. out: [n_q][d] fp64. Follows softmax_weighted_sum
  * (attention.cpp:35-49) on the kept tokens: the selected blocks' tokens in
  * ascending order, minus causally masked ones. */
 void orc_block_sparse_attention(const uint16_t* q, const uint16_t* k, const uint16_t* v,
-                                int64_t n, int32_t d, int32_t bq, int32_t bk, int causal,
-                                const int32_t* idx, const int32_t* cnt, int64_t kmax,
+                                int64_t n_q, int64_t n_k, int32_t d, int32_t bq, int32_t bk,
+                                int causal, const int32_t* idx, const int32_t* cnt, int64_t kmax,
                                 double* out) {
     const double scale = 1.0 / sqrt((double)d);
     double* s = (double*)malloc(sizeof(double) * (size_t)(kmax * bk));
     int64_t* tok = (int64_t*)malloc(sizeof(int64_t) * (size_t)(kmax * bk));
     double* qrow = (double*)malloc(sizeof(double) * (size_t)d);
-    for (int64_t i = 0; i < n; ++i) {
+    for (int64_t i = 0; i < n_q; ++i) {
         const int64_t qb = i / bq;
         for (int32_t c = 0; c < d; ++c) qrow[c] = (double)bf16_to_f32(q[i * d + c]);
         int64_t m_cnt = 0;
         for (int64_t t = 0; t < cnt[qb]; ++t) {
             const int64_t b = idx[qb * kmax + t];
-            for (int64_t j = b * bk; j < (b + 1) * bk && j < n; ++j) {
+            for (int64_t j = b * bk; j < (b + 1) * bk && j < n_k; ++j) {
                 if (causal && j > i) continue;
                 double dot = 0.0;
                 for (int32_t c = 0; c < d; ++c) dot += qrow[c] * (double)bf16_to_f32(k[j * d + c]);
@@ -244,29 +246,31 @@ void orc_block_sparse_attention(const uint16_t* q, const uint16_t* k, const uint
 /* Whole layer (GQA: q head h reads kv head h / (hq/hkv)), per-head budgets in
  * blocks. Parallel over heads with OpenMP (each head is computed serially, so
  * the result is thread-count independent, as the reference's fan-out is:
- * attention.cpp:214-223). q: [hq][n][d], k/v: [hkv][n][d]; out [hq][n][d]. */
+ * attention.cpp:214-223). q: [hq][n_q][d], k/v: [hkv][n_k][d]; out
+ * [hq][n_q][d]. The GPU path is prefill (n_q == n_k); the reference (and so
+ * this restatement) also allows n_q != n_k. */
 void orc_layer(const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t hq, int32_t hkv,
-               int64_t n, int32_t d, int32_t bq, int32_t bk, int causal,
+               int64_t n_q, int64_t n_k, int32_t d, int32_t bq, int32_t bk, int causal,
                const int64_t* k_blocks, int64_t kmax, float* scores_out, int32_t* idx_out,
                int32_t* cnt_out, double* out) {
-    const int64_t nqb = (n + bq - 1) / bq, nkb = (n + bk - 1) / bk;
+    const int64_t nqb = (n_q + bq - 1) / bq, nkb = (n_k + bk - 1) / bk;
     const int32_t group = hq / hkv;
 #pragma omp parallel for schedule(dynamic)
     for (int32_t h = 0; h < hq; ++h) {
         const int32_t g = h / group;
         float* qp = (float*)malloc(sizeof(float) * (size_t)(nqb * d));
         float* kp = (float*)malloc(sizeof(float) * (size_t)(nkb * d));
-        orc_pool_blocks(q + (int64_t)h * n * d, n, d, bq, qp);
-        orc_pool_blocks(k + (int64_t)g * n * d, n, d, bk, kp);
+        orc_pool_blocks(q + (int64_t)h * n_q * d, n_q, d, bq, qp);
+        orc_pool_blocks(k + (int64_t)g * n_k * d, n_k, d, bk, kp);
         float* sc = scores_out + (int64_t)h * nqb * nkb;
-        orc_block_scores(qp, kp, n, d, bq, bk, causal, sc);
+        orc_block_scores(qp, kp, n_q, n_k, d, bq, bk, causal, sc);
         int32_t* ix = idx_out + (int64_t)h * nqb * kmax;
         int32_t* ct = cnt_out + (int64_t)h * nqb;
-        orc_select_topk(sc, n, bq, bk, causal, k_blocks[h], kmax, ix, ct);
+        orc_select_topk(sc, n_q, n_k, bq, bk, causal, k_blocks[h], kmax, ix, ct);
         if (out) {
-            orc_block_sparse_attention(q + (int64_t)h * n * d, k + (int64_t)g * n * d,
-                                       v + (int64_t)g * n * d, n, d, bq, bk, causal, ix, ct, kmax,
-                                       out + (int64_t)h * n * d);
+            orc_block_sparse_attention(q + (int64_t)h * n_q * d, k + (int64_t)g * n_k * d,
+                                       v + (int64_t)g * n_k * d, n_q, n_k, d, bq, bk, causal, ix,
+                                       ct, kmax, out + (int64_t)h * n_q * d);
         }
         free(qp);
         free(kp);

@@ -22,8 +22,11 @@ EXPORTS = (
     "shplb_plan_naive", "shplb_plan_greedy", "shplb_imbalance",
     "shplb_simulate", "shplb_barrier",
     "shplb_ctx_create", "shplb_ctx_destroy", "shplb_ctx_launch_count",
+    "shplb_ctx_set_timing", "shplb_ctx_read_timing",
     "shplb_block_scores", "shplb_select_blocks", "shplb_block_sparse_attention",
-    "shplb_sparse_attention_layer", "shplb_last_selection", "shplb_layer_work",
+    "shplb_sparse_attention_layer", "shplb_sparse_attention_layer_host",
+    "shplb_last_selection", "shplb_copy_last_selection",
+    "shplb_layer_work",
 )
 
 SHPLB_OK = 0
@@ -130,12 +133,16 @@ def lib() -> C.CDLL:
     L.shplb_ctx_destroy.argtypes = [vp]
     L.shplb_ctx_launch_count.argtypes = [vp]
     L.shplb_ctx_launch_count.restype = i64
+    L.shplb_ctx_set_timing.argtypes = [vp, C.c_int]
+    L.shplb_ctx_read_timing.argtypes = [vp, vp, C.c_int, P(C.c_int)]
     L.shplb_block_scores.argtypes = [vp, P(LayerShape), vp, vp, vp, vp]
     L.shplb_select_blocks.argtypes = [vp, P(LayerShape), vp, vp, i64, vp, vp, vp]
     L.shplb_block_sparse_attention.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp, i64, vp,
                                                vp]
     L.shplb_sparse_attention_layer.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp, vp]
+    L.shplb_sparse_attention_layer_host.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp, vp]
     L.shplb_last_selection.argtypes = [vp, P(vp), P(vp), P(i64)]
+    L.shplb_copy_last_selection.argtypes = [vp, vp, i64, vp, i64, vp]
     L.shplb_layer_work.argtypes = [P(LayerShape), vp, P(i64), P(f64)]
     _lib = L
     return L

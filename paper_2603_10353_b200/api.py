@@ -247,6 +247,18 @@ class Context:
     def launches(self) -> int:
         return int(lib().shplb_ctx_launch_count(self._h))
 
+    def set_timing(self, enable: bool) -> None:
+        """Record per-kernel CUDA events in every layer call (see read_timing)."""
+        check(lib().shplb_ctx_set_timing(self._h, int(enable)))
+
+    def read_timing(self, max_calls: int = 4096) -> np.ndarray:
+        """[calls, 3] ms of (kernel 1 pooling, kernel 2 score+select, kernel 3
+        attention) per layer call since timing was enabled / last read."""
+        buf = np.zeros((max_calls, 3), np.float64)
+        n = C.c_int()
+        check(lib().shplb_ctx_read_timing(self._h, _ptr(buf), max_calls, C.byref(n)))
+        return buf[:n.value].copy()
+
     # -- kernel 1 ---------------------------------------------------------
     def block_scores(self, q, k, causal=True, stream=None, validate=False, out=None, kv_map=None):
         import torch
@@ -310,6 +322,25 @@ class Context:
             _stream_ptr(stream)))
         return out
 
+    def sparse_attention_layer_host(self, q, k, v, budgets_tokens, causal=True, out=None,
+                                    stream=None, kv_map=None):
+        """The layer call on HOST bf16 tensors (pinned for async DMA): copy in,
+        kernels 1-3, copy out, synchronise (shplb_sparse_attention_layer_host)."""
+        import torch
+        for t, nm in ((q, "q"), (k, "k"), (v, "v")):
+            if t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous():
+                from ._native import InvalidArgument
+                raise InvalidArgument(f"{nm} must be a contiguous host bf16 tensor")
+        hq, n, d = q.shape
+        if out is None:
+            out = torch.empty_like(q)
+        b = _i64(budgets_tokens)
+        sh = _shape(hq, k.shape[0], n, causal, False, kv_map, d)
+        check(lib().shplb_sparse_attention_layer_host(
+            self._h, C.byref(sh), C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()),
+            C.c_void_p(v.data_ptr()), _ptr(b), C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
     def last_selection(self, num_q_heads: int, seq_len: int):
         """(idx, cnt) of the last layer call as torch views over the context workspace."""
         import torch
@@ -319,18 +350,15 @@ class Context:
         kmax = int(km.value)
         idx = torch.empty((num_q_heads, nqb, kmax), dtype=torch.int32, device=f"cuda:{self.device}")
         cnt = torch.empty((num_q_heads, nqb), dtype=torch.int32, device=f"cuda:{self.device}")
-        nbytes_i = idx.numel() * 4
-        nbytes_c = cnt.numel() * 4
-        cudart = torch.cuda.cudart()
-        torch.cuda.synchronize()
-        cudart.cudaMemcpy(idx.data_ptr(), ip.value, nbytes_i, 3)  # cudaMemcpyDeviceToDevice
-        cudart.cudaMemcpy(cnt.data_ptr(), cp.value, nbytes_c, 3)
+        check(lib().shplb_copy_last_selection(self._h, C.c_void_p(idx.data_ptr()), idx.numel(),
+                                              C.c_void_p(cnt.data_ptr()), cnt.numel(),
+                                              _stream_ptr(None)))
         return idx, cnt
 
 
-def layer_work(num_q_heads, num_kv_heads, seq_len, budgets_tokens, causal=True):
+def layer_work(num_q_heads, num_kv_heads, seq_len, budgets_tokens, causal=True, kv_map=None):
     """(selected tiles, algorithmic FLOPs 4*d*bq*bk*tiles) of one layer call."""
-    sh = _shape(num_q_heads, num_kv_heads, seq_len, causal)
+    sh = _shape(num_q_heads, num_kv_heads, seq_len, causal, kv_map=kv_map)
     b = _i64(budgets_tokens)
     t, f = C.c_int64(), C.c_double()
     check(lib().shplb_layer_work(C.byref(sh), _ptr(b), C.byref(t), C.byref(f)))

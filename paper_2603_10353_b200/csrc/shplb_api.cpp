@@ -165,7 +165,10 @@ struct shplb_ctx {
     int32_t* cnt = nullptr;
     size_t cnt_bytes = 0;
     int32_t* flag = nullptr;
+    void* host_io = nullptr;  // device staging for shplb_sparse_attention_layer_host
+    size_t host_io_bytes = 0;
     int64_t last_kmax = 0;
+    int64_t last_rows = 0;  // Hq * nqb of the last layer call
     // Kernel-3 work lists, one per (seq_len, causal, blocks-per-head) seen.
     // Never overwritten, so an in-flight launch never sees its list change.
     struct WorkList {
@@ -174,6 +177,11 @@ struct shplb_ctx {
     };
     std::map<std::vector<int64_t>, WorkList> work_lists;
     const WorkList* current = nullptr;
+    // Stage timing: 4 events per recorded layer call (before k1, after k1,
+    // after k2, after k3); `timed_calls` sets in use since the last read.
+    bool timing = false;
+    std::vector<cudaEvent_t> events;
+    int timed_calls = 0;
 };
 
 namespace shplb {
@@ -223,18 +231,34 @@ void validate_inputs(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, 
     if (v && f[2]) throw InvalidArgument("V contains NaN or Inf");
 }
 
+// Records stage event `slot` (0..3) of the current timed call, if timing.
+void mark(shplb_ctx* ctx, int slot, cudaStream_t st) {
+    if (!ctx->timing) return;
+    const size_t need = static_cast<size_t>(ctx->timed_calls + 1) * 4;
+    while (ctx->events.size() < need) {
+        cudaEvent_t e;
+        SHPLB_CUDA(cudaEventCreate(&e));
+        ctx->events.push_back(e);
+    }
+    SHPLB_CUDA(cudaEventRecord(ctx->events[static_cast<size_t>(ctx->timed_calls) * 4 + slot], st));
+    if (slot == 3) ++ctx->timed_calls;
+}
+
 void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const void* k,
                     const kern::HeadTable& kb, int64_t kmax, float* scores_out, bool select,
                     int32_t* idx, int32_t* cnt, cudaStream_t st) {
     const int64_t nb = cdiv(s->seq_len, kern::kBlock);
     grow(ctx->qp, ctx->qp_bytes, sizeof(float) * s->num_q_heads * nb * kern::kHeadDim);
     grow(ctx->kp, ctx->kp_bytes, sizeof(float) * s->num_kv_heads * nb * kern::kHeadDim);
+    if (select) mark(ctx, 0, st);
     kern::launch_pool(q, s->num_q_heads, s->seq_len, ctx->qp, st);
     kern::launch_pool(k, s->num_kv_heads, s->seq_len, ctx->kp, st);
+    if (select) mark(ctx, 1, st);
     const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(s->head_dim)));
     kern::launch_score_select(ctx->qp, ctx->kp, s->num_q_heads, s->num_kv_heads, s->seq_len,
                               s->causal != 0, scale, kb, kmax, scores_out, select, idx, cnt, st);
     check_launch(ctx, 3);
+    if (select) mark(ctx, 2, st);
 }
 
 // Kernel-3 work list: every (head, query block) tile, heaviest first (LPT), so
@@ -331,12 +355,41 @@ int shplb_ctx_destroy(shplb_ctx* ctx) {
         cudaFree(ctx->idx);
         cudaFree(ctx->cnt);
         for (auto& kv : ctx->work_lists) cudaFree(kv.second.tiles);
+        for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
         cudaFree(ctx->flag);
+        cudaFree(ctx->host_io);
         delete ctx;
     });
 }
 
 int64_t shplb_ctx_launch_count(const shplb_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+int shplb_ctx_set_timing(shplb_ctx* ctx, int enable) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx is null");
+        ctx->timing = enable != 0;
+        ctx->timed_calls = 0;
+    });
+}
+
+int shplb_ctx_read_timing(shplb_ctx* ctx, double* stage_ms, int max_calls, int* n_calls_out) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx is null");
+        DeviceGuard g(ctx->device);
+        const int n = std::min(ctx->timed_calls, max_calls);
+        for (int c = 0; c < n; ++c) {
+            cudaEvent_t* e = &ctx->events[static_cast<size_t>(c) * 4];
+            SHPLB_CUDA(cudaEventSynchronize(e[3]));
+            for (int s = 0; s < 3; ++s) {
+                float ms = 0.f;
+                SHPLB_CUDA(cudaEventElapsedTime(&ms, e[s], e[s + 1]));
+                stage_ms[c * 3 + s] = ms;
+            }
+        }
+        if (n_calls_out) *n_calls_out = n;
+        ctx->timed_calls = 0;
+    });
+}
 
 int shplb_block_scores(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
                        const void* k, float* scores_out, void* stream) {
@@ -426,8 +479,45 @@ int shplb_sparse_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape,
         build_tiles(ctx, shape, kbl);
         pool_and_score(ctx, shape, q, k, kb, kmax, nullptr, true, ctx->idx, ctx->cnt, st);
         run_fa(ctx, shape, q, k, v, ctx->idx, ctx->cnt, kmax, out, st);
+        mark(ctx, 3, st);
         ctx->last_kmax = kmax;
+        ctx->last_rows = shape->num_q_heads * nqb;
     });
+}
+
+int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* shape,
+                                      const uint16_t* q_host, const uint16_t* k_host,
+                                      const uint16_t* v_host, const int64_t* budgets_tokens,
+                                      uint16_t* out_host, void* stream) {
+    int rc = SHPLB_OK;
+    const int err = guarded([&] {
+        require(ctx != nullptr, "ctx is null");
+        check_shape(shape);
+        require(q_host && k_host && v_host && out_host, "null host buffer");
+        const size_t qb = sizeof(uint16_t) * shape->num_q_heads * shape->seq_len * shape->head_dim;
+        const size_t kb = sizeof(uint16_t) * shape->num_kv_heads * shape->seq_len * shape->head_dim;
+        const size_t al = 256;
+        const size_t q_off = 0, k_off = (qb + al - 1) / al * al, v_off = k_off + (kb + al - 1) / al * al,
+                     o_off = v_off + (kb + al - 1) / al * al, total = o_off + qb;
+        DeviceGuard g(ctx->device);
+        if (total > ctx->host_io_bytes) {
+            if (ctx->host_io) SHPLB_CUDA(cudaFree(ctx->host_io));
+            ctx->host_io = nullptr;
+            SHPLB_CUDA(cudaMalloc(&ctx->host_io, total));
+            ctx->host_io_bytes = total;
+        }
+        auto* base = static_cast<uint8_t*>(ctx->host_io);
+        auto st = static_cast<cudaStream_t>(stream);
+        SHPLB_CUDA(cudaMemcpyAsync(base + q_off, q_host, qb, cudaMemcpyHostToDevice, st));
+        SHPLB_CUDA(cudaMemcpyAsync(base + k_off, k_host, kb, cudaMemcpyHostToDevice, st));
+        SHPLB_CUDA(cudaMemcpyAsync(base + v_off, v_host, kb, cudaMemcpyHostToDevice, st));
+        rc = shplb_sparse_attention_layer(ctx, shape, base + q_off, base + k_off, base + v_off,
+                                          budgets_tokens, base + o_off, stream);
+        if (rc != SHPLB_OK) return;  // message already recorded
+        SHPLB_CUDA(cudaMemcpyAsync(out_host, base + o_off, qb, cudaMemcpyDeviceToHost, st));
+        SHPLB_CUDA(cudaStreamSynchronize(st));
+    });
+    return rc != SHPLB_OK ? rc : err;
 }
 
 int shplb_last_selection(const shplb_ctx* ctx, const int32_t** idx, const int32_t** cnt,
@@ -437,6 +527,20 @@ int shplb_last_selection(const shplb_ctx* ctx, const int32_t** idx, const int32_
         if (idx) *idx = ctx->idx;
         if (cnt) *cnt = ctx->cnt;
         if (kmax) *kmax = ctx->last_kmax;
+    });
+}
+
+int shplb_copy_last_selection(const shplb_ctx* ctx, int32_t* idx_dst, int64_t idx_elems,
+                              int32_t* cnt_dst, int64_t cnt_elems, void* stream) {
+    return guarded([&] {
+        require(ctx != nullptr && ctx->last_kmax > 0, "no layer call on this context yet");
+        require(idx_dst && cnt_dst, "null destination");
+        const int64_t ni = ctx->last_rows * ctx->last_kmax, nc = ctx->last_rows;
+        if (idx_elems < ni || cnt_elems < nc) throw InvalidArgument("destination buffers too small");
+        DeviceGuard g(ctx->device);
+        auto st = static_cast<cudaStream_t>(stream);
+        SHPLB_CUDA(cudaMemcpyAsync(idx_dst, ctx->idx, sizeof(int32_t) * ni, cudaMemcpyDeviceToDevice, st));
+        SHPLB_CUDA(cudaMemcpyAsync(cnt_dst, ctx->cnt, sizeof(int32_t) * nc, cudaMemcpyDeviceToDevice, st));
     });
 }
 

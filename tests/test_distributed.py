@@ -1,0 +1,72 @@
+"""Head-parallel plumbing on CPU with gloo, world_size 2 (the N>1 path of
+bench.py without the GPU kernels): plan -> per-rank shards -> uneven
+all-gather -> heads back in global order; budget broadcast; max-over-ranks
+barrier metric."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2603_10353_b200 as P
+from paper_2603_10353_b200.head_parallel import gather_heads, head_counts, rank_shard
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, budgets, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        hq, group = len(budgets), 4
+        # rank 0 owns the budget table; everyone receives it (bench.make_budgets)
+        b = torch.tensor(budgets if rank == 0 else [0] * hq, dtype=torch.int64)
+        dist.broadcast(b, 0)
+        b = b.numpy()
+        for name, plan in (("greedy", P.greedy_assign(b, world)),
+                           ("naive", P.naive_assign(b, world))):
+            sh = rank_shard(plan, rank, group, b)
+            assert all(plan[h] == rank for h in sh.heads)
+            assert [sh.kv_heads[m] for m in sh.kv_map] == [h // group for h in sh.heads]
+            # stand-in for the rank's kernel output: head h filled with h
+            local = torch.stack([torch.full((3, 2), float(h)) for h in sh.heads]) if sh.heads \
+                else torch.zeros((0, 3, 2))
+            full = gather_heads(local, plan, world)
+            expect = torch.arange(hq, dtype=torch.float32)[:, None, None].expand(hq, 3, 2)
+            assert torch.equal(full, expect), name
+            # per-rank "latency" proportional to the rank's load; max over ranks
+            load = float(b[sh.heads].sum())
+            lat = torch.tensor([load])
+            gathered = [torch.zeros(1) for _ in range(world)]
+            dist.all_gather(gathered, lat)
+            lats = [float(x) for x in gathered]
+            res = P.barrier(lats)
+            rep = P.imbalance(b, plan, world)
+            assert res.barrier_latency == float(rep.loads.max())
+            if rank == 0:
+                results[name] = (res.barrier_latency, res.bubble_fraction, head_counts(plan, world))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_head_parallel_world2_gloo():
+    budgets = [64 * 128, 128, 128, 32 * 128, 2 * 128, 128, 16 * 128, 128,
+               8 * 128, 128, 4 * 128, 128]  # 12 heads, 3 kv groups of 4
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker, args=(2, _free_port(), budgets, results), nprocs=2, join=True)
+    g_T, g_bub, g_counts = results["greedy"]
+    n_T, n_bub, n_counts = results["naive"]
+    assert n_counts == [6, 6]            # even HP splits by head count
+    assert g_T <= n_T and g_bub <= n_bub  # the balancer never does worse here
+    assert g_T == max(P.imbalance(budgets, P.greedy_assign(budgets, 2), 2).loads)

@@ -1,0 +1,225 @@
+"""Product host code (libshplb.so: budget table, head plan, metric, profiler)
+against the reference — golden fixtures always, the live reference library
+(oracle/_ref) when present — plus the C-ABI export surface. CPU only: no CUDA
+call is made."""
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2603_10353_b200 as P
+from oracle import oracle as O
+from paper_2603_10353_b200 import _native
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def _load(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+def _curves(raw, n_k):
+    return [P.RecoveryCurve(np.asarray(b), np.asarray(r), n_k) for b, r in raw]
+
+
+# ---------------------------------------------------------------- C ABI ----
+
+def test_library_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "shplb.h")).read()
+    declared = set(re.findall(r"\b(shplb_[a-z_]+)\s*\(", header))
+    assert declared == set(_native.EXPORTS), declared ^ set(_native.EXPORTS)
+    lib = P.lib()
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.shplb_version().decode().endswith("sm_100a")
+
+
+def test_no_oracle_in_product_package():
+    """The product never imports or links the oracle."""
+    pkg = os.path.join(ROOT, "paper_2603_10353_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cpp", ".cu", ".hpp", ".cuh")) or f == "Makefile":
+                text = open(os.path.join(dirpath, f), errors="ignore").read()
+                assert "from oracle" not in text and "import oracle" not in text, f
+                assert "liboracle" not in text and "headbal_ref" not in text, f
+
+
+# -------------------------------------------------------- budget table ----
+
+def test_uniform_allocate_golden_and_messages():
+    for u in _load("budget_kat.json")["uniform"]:
+        assert P.uniform_allocate(*u["args"]).budgets.tolist() == u["budgets"]
+    full = P.uniform_allocate(32, 32 * 4096, 128, 4096)
+    assert (full.budgets == 4096).all()
+    # allocator.cpp:53-62 message, incl. the range test_allocator.cpp:62-67 checks
+    with pytest.raises(P.InvalidArgument, match=r"\[512, 16384\]"):
+        P.uniform_allocate(4, 100, 128, 4096)
+    with pytest.raises(P.InvalidArgument, match="feasible"):
+        P.uniform_allocate(2, 9000, 128, 4096)
+
+
+def test_maxmin_worked_instance():
+    """test_allocator.cpp:79-94: (128, 1920), min recovery 0.46875."""
+    w = _load("budget_kat.json")["maxmin_worked"]
+    a = P.maxmin_allocate(_curves(w["curves"], w["n_k"]), w["total"], w["quantum"], w["floor"])
+    assert a.budgets.tolist() == [128, 1920]
+    assert a.transfers == w["transfers"]
+    assert abs(a.min_recovery_end - 0.46875) < 1e-12
+    assert abs(a.min_recovery_start - 0.25) < 1e-12
+
+
+def test_maxmin_golden_profiled_curves_bit_exact():
+    for c in _load("budget_kat.json")["maxmin_profiled"]:
+        a = P.maxmin_allocate(_curves(c["curves"], c["n_k"]), c["total"], c["quantum"], c["floor"])
+        assert a.budgets.tolist() == c["budgets"]
+        assert a.transfers == c["transfers"] and a.hit_iteration_cap == c["hit_cap"]
+
+
+def test_maxmin_identical_curves_cap_and_iteration_cap():
+    ramp = lambda h, n, s, st: P.RecoveryCurve(*map(np.asarray, O_ramp(n, s, st)), n)  # noqa: E731
+    same = [ramp(h, 1024, 1024, 64) for h in range(4)]
+    a = P.maxmin_allocate(same, 4 * 512)
+    assert a.budgets.tolist() == [512] * 4 and a.transfers == 0 and not a.hit_iteration_cap
+    full = P.maxmin_allocate([ramp(0, 256, 64, 16), ramp(1, 256, 256, 16)], 512, 16, 16)
+    assert full.budgets.tolist() == [256, 256] and full.transfers == 0
+    capped = P.maxmin_allocate([ramp(0, 4096, 256, 64), ramp(1, 4096, 4096, 64)], 2048,
+                               max_iterations=3)
+    assert capped.hit_iteration_cap and capped.transfers == 3 and capped.budgets.sum() == 2048
+
+
+def O_ramp(n_k, sat, stride):
+    b = list(range(0, n_k + 1, stride))
+    if b[-1] != n_k:
+        b.append(n_k)
+    return b, [min(1.0, x / sat) for x in b]
+
+
+def test_maxmin_validation_messages():
+    with pytest.raises(P.InvalidArgument, match="share the context length"):
+        P.maxmin_allocate([P.RecoveryCurve(*map(np.asarray, O_ramp(512, 256, 64)), 512),
+                           P.RecoveryCurve(*map(np.asarray, O_ramp(1024, 256, 64)), 1024)], 512)
+    pair = [P.RecoveryCurve(*map(np.asarray, O_ramp(1024, 256, 64)), 1024)] * 2
+    with pytest.raises(P.InvalidArgument):
+        P.maxmin_allocate(pair, 100)
+    with pytest.raises(P.InvalidArgument, match="quantum"):
+        P.maxmin_allocate(pair, 1024, quantum=0)
+    bad = P.RecoveryCurve(np.array([0, 512, 1024]), np.array([0.0, 0.3, 0.5]), 1024)
+    with pytest.raises(P.InvalidArgument, match="final recovery must be 1"):
+        P.maxmin_allocate([bad, bad], 1024)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built here")
+@pytest.mark.parametrize("seed", range(25))
+def test_maxmin_fuzz_vs_reference(seed):
+    """Random monotone curves, random totals/quanta/floors: bit-exact budgets."""
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(2, 40))
+    n_k = int(rng.choice([512, 1024, 4096]))
+    stride = int(rng.choice([16, 64, 128]))
+    grid = list(range(0, n_k, stride)) + [n_k]
+    curves = []
+    for _ in range(n):
+        inc = rng.exponential(1.0, len(grid)) * (rng.random(len(grid)) < 0.7)
+        r = np.cumsum(inc)
+        r = r / r[-1] if r[-1] > 0 else np.linspace(0, 1, len(grid))
+        r[0] = 0.0
+        r[-1] = 1.0
+        curves.append((grid, r.tolist()))
+    quantum = int(rng.choice([16, 64, 128]))
+    floor = int(rng.choice([0, 64, 128]))
+    total = int(rng.integers(n * floor, n * n_k + 1))
+    want, tr, cap = O.ref.maxmin_allocate(curves, n_k, total, quantum, floor)
+    got = P.maxmin_allocate(_curves(curves, n_k), total, quantum, floor)
+    assert got.budgets.tolist() == want.tolist()
+    assert got.transfers == tr and got.hit_iteration_cap == cap
+    o, otr, ocap = O.maxmin_allocate(curves, n_k, total, quantum, floor)
+    assert o.tolist() == want.tolist() and otr == tr
+
+
+# ---------------------------------------------------------- head plan -----
+
+def test_plans_golden():
+    for c in _load("plan_kat.json")["cases"]:
+        b, dev = c["budgets"], c["devices"]
+        assert P.greedy_assign(b, dev).tolist() == c["greedy"]
+        assert P.naive_assign(b, dev).tolist() == c["naive"]
+        assert P.naive_assign(b, dev, round_robin=True).tolist() == c["round_robin"]
+        rep = P.imbalance(b, c["greedy"], dev)
+        assert rep.loads.tolist() == c["greedy_loads"] and rep.imbalance == c["greedy_imbalance"]
+        rep = P.imbalance(b, c["naive"], dev)
+        assert rep.loads.tolist() == c["naive_loads"] and rep.imbalance == c["naive_imbalance"]
+        sim = P.simulate(c["greedy_loads"])
+        assert sim.barrier_latency == c["greedy_barrier"]
+        assert sim.bubble_fraction == c["greedy_bubble"]
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built here")
+@pytest.mark.parametrize("seed", range(25))
+def test_plans_fuzz_vs_reference(seed):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(1, 80))
+    dev = int(rng.integers(1, 9))
+    b = rng.integers(0, 6, n) * int(rng.choice([1, 128, 4096]))  # many ties
+    assert P.greedy_assign(b, dev).tolist() == O.ref.greedy_assign(b, dev).tolist()
+    if dev <= n:
+        assert P.naive_assign(b, dev).tolist() == O.ref.naive_assign(b, dev).tolist()
+    g = P.greedy_assign(b, dev)
+    rep = P.imbalance(b, g, dev)
+    loads, imb, am = O.ref.imbalance(b, g, dev)
+    assert rep.loads.tolist() == loads.tolist() and rep.imbalance == imb
+    assert rep.argmax_device == am
+
+
+def test_plan_errors():
+    with pytest.raises(P.InvalidArgument, match="device count 5 exceeds head count 4"):
+        P.naive_assign([1, 2, 3, 4], 5)
+    with pytest.raises(P.InvalidArgument, match="need at least one device"):
+        P.greedy_assign([1, 2], 0)
+    with pytest.raises(P.InvalidArgument, match="nonnegative"):
+        P.greedy_assign([1, -2], 2)
+    with pytest.raises(P.InvalidArgument, match="assigned to invalid device"):
+        P.imbalance([1, 2], [0, 3], 2)
+
+
+def test_metric_on_measured_latencies():
+    r = P.barrier([10.0, 12.0, 8.0, 10.0])
+    assert r.barrier_latency == 12.0 and abs(r.bubble_fraction - (1 - 10.0 / 12.0)) < 1e-15
+    assert P.barrier([0.0, 0.0]).bubble_fraction == 0.0
+    s = P.simulate([14, 13], alpha=1.0, beta=2.0)
+    assert s.device_latency.tolist() == [29.0, 27.0] and s.barrier_latency == 29.0
+    with pytest.raises(P.InvalidArgument, match="beta must be > 0"):
+        P.simulate([1, 2], beta=0.0)
+
+
+# ------------------------------------------------------------ profiler ----
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built here")
+def test_profile_curves_match_reference_build_profiles():
+    """PerQueryTopK recovery curves (build_profiles, profiler.cpp:157-196) on
+    bf16-exact inputs agree with the reference to rounding."""
+    rng = np.random.default_rng(5)
+    hq, hkv, rows, n_k, d = 4, 2, 6, 300, 128
+    q = rng.standard_normal((hq, rows, d)).astype(np.float32) * rng.uniform(0.05, 0.4, (hq, 1, 1)).astype(np.float32)
+    k = rng.standard_normal((hkv, n_k, d)).astype(np.float32)
+    qb, kb = O.f32_to_bf16_bits(q), O.f32_to_bf16_bits(k)
+    grid = P.default_budget_grid(n_k, 32)
+    curves = P.profile_curves(qb, kb, grid)
+    Q = O.bf16_bits_to_f32(qb).astype(np.float64)
+    K = np.repeat(O.bf16_bits_to_f32(kb).astype(np.float64), hq // hkv, axis=0)
+    ref = O.ref.build_profiles(Q, K, np.zeros_like(K), grid)
+    for h in range(hq):
+        assert np.abs(curves[h].recovery - ref[h]).max() < 1e-12
+        assert curves[h].recovery[-1] == pytest.approx(1.0, abs=1e-9)
+
+
+def test_layer_work_counts_selected_tiles():
+    # 1 head, 4 query blocks, causal: visible 1,2,3,4; k=2 -> 1+2+2+2 = 7 tiles
+    tiles, flops = P.layer_work(1, 1, 512, [256], causal=True)
+    assert tiles == 7 and flops == 4 * 128 * 128 * 128 * 7
+    tiles, _ = P.layer_work(2, 1, 512, [512, 1], causal=False)
+    assert tiles == 16 + 4
