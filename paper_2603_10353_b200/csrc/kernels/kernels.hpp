@@ -12,6 +12,7 @@ constexpr int kHeadDim = 128;   // d
 constexpr int kBlock = 128;     // bq = bk
 constexpr int kPoolSplit = 16;  // interleaved row groups of the pooled sum
 constexpr int kMaxHeads = 256;  // per-launch k-block table lives in the kernel parameters
+constexpr int kMaxSelected = 2048;  // selected key blocks per query tile staged in smem (256K tokens)
 
 // Per-q-head table passed in kernel parameters.
 struct HeadTable {

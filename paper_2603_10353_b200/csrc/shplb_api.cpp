@@ -295,6 +295,8 @@ void build_tiles(shplb_ctx* ctx, const shplb_layer_shape* s, const std::vector<i
 void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const void* k,
             const void* v, const int32_t* idx, const int32_t* cnt, int64_t kmax, void* out,
             cudaStream_t st) {
+    if (kmax > kern::kMaxSelected)
+        throw NotSupported("more than " + std::to_string(kern::kMaxSelected) + " key blocks per query block");
     kern::FaParams p;
     std::memset(&p, 0, sizeof p);
     p.tm_q = make_tmap(q, s->num_q_heads, s->seq_len);
