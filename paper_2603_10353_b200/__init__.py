@@ -4,13 +4,13 @@ Host API over libshplb.so (C ABI: include/shplb.h). See DESIGN.md.
 """
 from ._native import (CudaError, InvalidArgument, LogicError, NotSupported, ShplbError, build,
                       lib)
-from .api import (BLOCK, HEAD_DIM, BudgetAllocation, Context, LoadReport, RecoveryCurve,
+from .api import (BLOCK, BLOCK_Q, HEAD_DIM, BudgetAllocation, Context, LoadReport, RecoveryCurve,
                   SimulationResult, barrier, default_budget_grid, greedy_assign, imbalance,
                   layer_work, maxmin_allocate, naive_assign, profile_curves, simulate,
                   uniform_allocate)
 
 __all__ = [
-    "BLOCK", "HEAD_DIM", "BudgetAllocation", "Context", "CudaError", "InvalidArgument",
+    "BLOCK", "BLOCK_Q", "HEAD_DIM", "BudgetAllocation", "Context", "CudaError", "InvalidArgument",
     "LoadReport", "LogicError", "NotSupported", "RecoveryCurve", "ShplbError", "SimulationResult",
     "barrier", "build", "default_budget_grid", "greedy_assign", "imbalance", "layer_work", "lib",
     "maxmin_allocate", "naive_assign", "profile_curves", "simulate", "uniform_allocate",

@@ -11,7 +11,7 @@ import os
 import subprocess
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libshplb.so")
+LIB_PATH = os.environ.get("SHPLB_LIB") or os.path.join(PKG_DIR, "lib", "libshplb.so")
 CSRC_DIR = os.path.join(PKG_DIR, "csrc")
 
 # Every symbol include/shplb.h declares (checked by the CPU test suite).

@@ -23,7 +23,8 @@ import numpy as np
 
 from ._native import (LayerShape, MaxminDiag, check, lib)
 
-BLOCK = 128
+BLOCK = 128      # key block (pooling and K/V tile): 128 keys
+BLOCK_Q = 256    # default query block: two 128-row halves share every K/V tile
 HEAD_DIM = 128
 
 
@@ -194,8 +195,8 @@ def barrier(device_latency) -> SimulationResult:
 # ---------------------------------------------------------------------------
 
 def _shape(num_q_heads, num_kv_heads, seq_len, causal, validate=False, kv_map=None,
-           head_dim=HEAD_DIM) -> LayerShape:
-    sh = LayerShape(num_q_heads, num_kv_heads, seq_len, head_dim, BLOCK, BLOCK, int(causal), 0,
+           head_dim=HEAD_DIM, block_q=BLOCK_Q) -> LayerShape:
+    sh = LayerShape(num_q_heads, num_kv_heads, seq_len, head_dim, block_q, BLOCK, int(causal), 0,
                     int(validate), None)
     if kv_map is not None:
         m = _i32(kv_map)
@@ -260,28 +261,30 @@ class Context:
         return buf[:n.value].copy()
 
     # -- kernel 1 ---------------------------------------------------------
-    def block_scores(self, q, k, causal=True, stream=None, validate=False, out=None, kv_map=None):
+    def block_scores(self, q, k, causal=True, stream=None, validate=False, out=None, kv_map=None,
+                     block_q=BLOCK_Q):
         import torch
         hq, n, d = q.shape
         hkv = k.shape[0]
-        nb = (n + BLOCK - 1) // BLOCK
+        nqb, nkb = (n + block_q - 1) // block_q, (n + BLOCK - 1) // BLOCK
         if out is None:
-            out = torch.empty((hq, nb, nb), dtype=torch.float32, device=q.device)
-        sh = _shape(hq, hkv, n, causal, validate, kv_map, d)
+            out = torch.empty((hq, nqb, nkb), dtype=torch.float32, device=q.device)
+        sh = _shape(hq, hkv, n, causal, validate, kv_map, d, block_q)
         check(lib().shplb_block_scores(self._h, C.byref(sh), _dev_ptr(q, "q", torch.bfloat16),
                                        _dev_ptr(k, "k", torch.bfloat16),
                                        _dev_ptr(out, "scores", torch.float32), _stream_ptr(stream)))
         return out
 
     # -- kernel 2 ---------------------------------------------------------
-    def select_blocks(self, scores, k_blocks, n, causal=True, kmax=None, stream=None):
+    def select_blocks(self, scores, k_blocks, n, causal=True, kmax=None, stream=None,
+                      block_q=BLOCK_Q):
         import torch
         hq, nqb, _ = scores.shape
         kb = _i64(k_blocks)
         kmax = int(kb.max()) if kmax is None else int(kmax)
         idx = torch.empty((hq, nqb, kmax), dtype=torch.int32, device=scores.device)
         cnt = torch.empty((hq, nqb), dtype=torch.int32, device=scores.device)
-        sh = _shape(hq, 1, n, causal)
+        sh = _shape(hq, 1, n, causal, block_q=block_q)
         sh.num_kv_heads = 1
         check(lib().shplb_select_blocks(self._h, C.byref(sh), _dev_ptr(scores, "scores", torch.float32),
                                         _ptr(kb), kmax, _dev_ptr(idx, "idx"), _dev_ptr(cnt, "cnt"),
@@ -290,12 +293,12 @@ class Context:
 
     # -- kernel 3 ---------------------------------------------------------
     def block_sparse_attention(self, q, k, v, idx, cnt, causal=True, stream=None, out=None,
-                               kv_map=None):
+                               kv_map=None, block_q=BLOCK_Q):
         import torch
         hq, n, d = q.shape
         if out is None:
             out = torch.empty_like(q)
-        sh = _shape(hq, k.shape[0], n, causal, kv_map=kv_map, head_dim=d)
+        sh = _shape(hq, k.shape[0], n, causal, kv_map=kv_map, head_dim=d, block_q=block_q)
         check(lib().shplb_block_sparse_attention(
             self._h, C.byref(sh), _dev_ptr(q, "q", torch.bfloat16), _dev_ptr(k, "k", torch.bfloat16),
             _dev_ptr(v, "v", torch.bfloat16), _dev_ptr(idx, "idx", torch.int32),
@@ -305,7 +308,7 @@ class Context:
 
     # -- the layer: kernels 1+2 fused, then 3 -----------------------------
     def sparse_attention_layer(self, q, k, v, budgets_tokens, causal=True, stream=None, out=None,
-                               validate=False, kv_map=None):
+                               validate=False, kv_map=None, block_q=BLOCK_Q):
         """sparse_attention for every head with its own token budget."""
         import torch
         hq, n, d = q.shape
@@ -315,7 +318,8 @@ class Context:
         if b.size != hq:
             from ._native import InvalidArgument
             raise InvalidArgument(f"need one budget per query head ({hq}), got {b.size}")
-        sh = _shape(hq, k.shape[0], n, causal, validate, kv_map, d)
+        sh = _shape(hq, k.shape[0], n, causal, validate, kv_map, d, block_q)
+        self._last_block_q = block_q
         check(lib().shplb_sparse_attention_layer(
             self._h, C.byref(sh), _dev_ptr(q, "q", torch.bfloat16), _dev_ptr(k, "k", torch.bfloat16),
             _dev_ptr(v, "v", torch.bfloat16), _ptr(b), _dev_ptr(out, "out", torch.bfloat16),
@@ -323,7 +327,7 @@ class Context:
         return out
 
     def sparse_attention_layer_host(self, q, k, v, budgets_tokens, causal=True, out=None,
-                                    stream=None, kv_map=None):
+                                    stream=None, kv_map=None, block_q=BLOCK_Q):
         """The layer call on HOST bf16 tensors (pinned for async DMA): copy in,
         kernels 1-3, copy out, synchronise (shplb_sparse_attention_layer_host)."""
         import torch
@@ -335,7 +339,8 @@ class Context:
         if out is None:
             out = torch.empty_like(q)
         b = _i64(budgets_tokens)
-        sh = _shape(hq, k.shape[0], n, causal, False, kv_map, d)
+        sh = _shape(hq, k.shape[0], n, causal, False, kv_map, d, block_q)
+        self._last_block_q = block_q
         check(lib().shplb_sparse_attention_layer_host(
             self._h, C.byref(sh), C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()),
             C.c_void_p(v.data_ptr()), _ptr(b), C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
@@ -346,7 +351,8 @@ class Context:
         import torch
         ip, cp, km = C.c_void_p(), C.c_void_p(), C.c_int64()
         check(lib().shplb_last_selection(self._h, C.byref(ip), C.byref(cp), C.byref(km)))
-        nqb = (seq_len + BLOCK - 1) // BLOCK
+        bq = getattr(self, "_last_block_q", BLOCK_Q)
+        nqb = (seq_len + bq - 1) // bq
         kmax = int(km.value)
         idx = torch.empty((num_q_heads, nqb, kmax), dtype=torch.int32, device=f"cuda:{self.device}")
         cnt = torch.empty((num_q_heads, nqb), dtype=torch.int32, device=f"cuda:{self.device}")
@@ -356,9 +362,11 @@ class Context:
         return idx, cnt
 
 
-def layer_work(num_q_heads, num_kv_heads, seq_len, budgets_tokens, causal=True, kv_map=None):
-    """(selected tiles, algorithmic FLOPs 4*d*bq*bk*tiles) of one layer call."""
-    sh = _shape(num_q_heads, num_kv_heads, seq_len, causal, kv_map=kv_map)
+def layer_work(num_q_heads, num_kv_heads, seq_len, budgets_tokens, causal=True, kv_map=None,
+               block_q=BLOCK_Q):
+    """(128x128 tiles, algorithmic FLOPs 4*d*128*128*tiles) of one layer call, before
+    selection: selected key blocks x live 128-row query halves (include/shplb.h)."""
+    sh = _shape(num_q_heads, num_kv_heads, seq_len, causal, kv_map=kv_map, block_q=block_q)
     b = _i64(budgets_tokens)
     t, f = C.c_int64(), C.c_double()
     check(lib().shplb_layer_work(C.byref(sh), _ptr(b), C.byref(t), C.byref(f)))

@@ -25,9 +25,11 @@ namespace {
 
 constexpr int kPoolThreads = 256;  // 16 row groups x 16 column groups of 8 columns
 
-// One CTA pools one 128-row block of one head. Thread (g, cg) sums rows
-// g, g+16, ... (ascending) of columns 8cg..8cg+7 with 16-byte loads; the 16
-// group partials per column are then added in ascending group order.
+// One CTA pools one kRows-row block (128 or 256) of one head. Thread (g, cg)
+// sums rows g, g+16, ... (ascending) of columns 8cg..8cg+7 with 16-byte loads
+// (all kRows/16 loads in flight); the 16 group partials per column are then
+// added in ascending group order.
+template <int kRows>
 __global__ void __launch_bounds__(kPoolThreads) pool_kernel(const __nv_bfloat16* __restrict__ x,
                                                             int64_t n, float* __restrict__ out) {
     __shared__ float part[kPoolSplit][kHeadDim + 4];
@@ -36,13 +38,13 @@ __global__ void __launch_bounds__(kPoolThreads) pool_kernel(const __nv_bfloat16*
     const int64_t nb = gridDim.x;
     const int g = threadIdx.x >> 4;
     const int cg = threadIdx.x & 15;
-    const int64_t t0 = b * kBlock;
-    const int cnt = static_cast<int>(min(static_cast<int64_t>(kBlock), n - t0));
+    const int64_t t0 = b * kRows;
+    const int cnt = static_cast<int>(min(static_cast<int64_t>(kRows), n - t0));
     const __nv_bfloat16* base = x + (head * n + t0) * kHeadDim + cg * 8;
 
-    uint4 v[kBlock / kPoolSplit];
+    uint4 v[kRows / kPoolSplit];
 #pragma unroll
-    for (int s = 0; s < kBlock / kPoolSplit; ++s) {
+    for (int s = 0; s < kRows / kPoolSplit; ++s) {
         const int t = g + s * kPoolSplit;
         v[s] = t < cnt ? __ldg(reinterpret_cast<const uint4*>(base + static_cast<int64_t>(t) * kHeadDim))
                        : make_uint4(0, 0, 0, 0);
@@ -51,7 +53,7 @@ __global__ void __launch_bounds__(kPoolThreads) pool_kernel(const __nv_bfloat16*
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
 #pragma unroll
-    for (int s = 0; s < kBlock / kPoolSplit; ++s) {
+    for (int s = 0; s < kRows / kPoolSplit; ++s) {
         if (g + s * kPoolSplit < cnt) {
             const uint32_t w[4] = {v[s].x, v[s].y, v[s].z, v[s].w};
 #pragma unroll
@@ -73,9 +75,11 @@ __global__ void __launch_bounds__(kPoolThreads) pool_kernel(const __nv_bfloat16*
     }
 }
 
-__device__ __forceinline__ int64_t visible_blocks(int64_t qb, int64_t n, int64_t nkb, bool causal) {
+// Key blocks (of kBlock keys) visible to query block qb of bq rows.
+__device__ __forceinline__ int64_t visible_blocks(int64_t qb, int64_t n, int64_t nkb, int bq,
+                                                  bool causal) {
     if (!causal) return nkb;
-    const int64_t last = min((qb + 1) * kBlock, n) - 1;
+    const int64_t last = min((qb + 1) * bq, n) - 1;
     return min(last / kBlock + 1, nkb);
 }
 
@@ -133,7 +137,7 @@ constexpr int kChunk = 64;        // key blocks per shared-memory chunk
 // selects two rows.
 __global__ void __launch_bounds__(kSelThreads)
     score_select_kernel(const float* __restrict__ qp, const float* __restrict__ kp, int hq,
-                        int hkv, int64_t n, int64_t nqb, int64_t nkb, int causal, float scale,
+                        int hkv, int64_t n, int64_t nqb, int64_t nkb, int bq, int causal, float scale,
                         HeadTable ht, int64_t kmax, float* __restrict__ scores_out, int select,
                         int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
     extern __shared__ __align__(16) float smem[];
@@ -153,7 +157,7 @@ __global__ void __launch_bounds__(kSelThreads)
         const int r = f / kHeadDim, c = f % kHeadDim;
         Qs[c * kRowsPerCta + r] = r < rows ? qp[((int64_t)h * nqb + qb0 + r) * kHeadDim + c] : 0.0f;
     }
-    const int64_t vis_max = visible_blocks(qb0 + rows - 1, n, nkb, causal != 0);
+    const int64_t vis_max = visible_blocks(qb0 + rows - 1, n, nkb, bq, causal != 0);
 
     const int rp = tid & 7;   // rows 2rp, 2rp+1
     const int kq = tid >> 3;  // key blocks 2kq, 2kq+1 of the chunk
@@ -185,7 +189,7 @@ __global__ void __launch_bounds__(kSelThreads)
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             const int r = 2 * rp + i;
-            const int64_t vis = visible_blocks(qb0 + r, n, nkb, causal != 0);
+            const int64_t vis = visible_blocks(qb0 + r, n, nkb, bq, causal != 0);
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int64_t kb = kc + 2 * kq + j;
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(kSelThreads)
     const int warp = tid >> 5;
     for (int r = warp; r < rows; r += kSelThreads / 32) {
         const int64_t qb = qb0 + r;
-        const int vis = static_cast<int>(visible_blocks(qb, n, nkb, causal != 0));
+        const int vis = static_cast<int>(visible_blocks(qb, n, nkb, bq, causal != 0));
         const int kk = min(ht.k[h], vis);
         warp_select_row(S + r * nkb_pad, vis, kk, kmax, idx + ((int64_t)h * nqb + qb) * kmax);
         if ((tid & 31) == 0) cnt[(int64_t)h * nqb + qb] = kk;
@@ -216,13 +220,13 @@ __global__ void __launch_bounds__(kSelThreads)
 // Standalone selector: one warp per (head, query block) row of a global score matrix.
 __global__ void __launch_bounds__(kSelThreads)
     select_kernel(const float* __restrict__ scores, int hq, int64_t n, int64_t nqb, int64_t nkb,
-                  int causal, HeadTable ht, int64_t kmax, int32_t* __restrict__ idx,
+                  int bq, int causal, HeadTable ht, int64_t kmax, int32_t* __restrict__ idx,
                   int32_t* __restrict__ cnt) {
     const int64_t row = static_cast<int64_t>(blockIdx.x) * (kSelThreads / 32) + (threadIdx.x >> 5);
     if (row >= (int64_t)hq * nqb) return;
     const int h = static_cast<int>(row / nqb);
     const int64_t qb = row % nqb;
-    const int vis = static_cast<int>(visible_blocks(qb, n, nkb, causal != 0));
+    const int vis = static_cast<int>(visible_blocks(qb, n, nkb, bq, causal != 0));
     const int kk = min(ht.k[h], vis);
     warp_select_row(scores + row * nkb, vis, kk, kmax, idx + row * kmax);
     if ((threadIdx.x & 31) == 0) cnt[row] = kk;
@@ -239,10 +243,13 @@ __global__ void check_finite_kernel(const uint16_t* __restrict__ x, int64_t coun
 
 }  // namespace
 
-void launch_pool(const void* x, int heads, int64_t n, float* out, cudaStream_t s) {
-    const int64_t nb = (n + kBlock - 1) / kBlock;
-    pool_kernel<<<dim3(static_cast<unsigned>(nb), heads), kPoolThreads, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(x), n, out);
+void launch_pool(const void* x, int heads, int64_t n, int rows, float* out, cudaStream_t s) {
+    const int64_t nb = (n + rows - 1) / rows;
+    const dim3 grid(static_cast<unsigned>(nb), heads);
+    if (rows == 256)
+        pool_kernel<256><<<grid, kPoolThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(x), n, out);
+    else
+        pool_kernel<128><<<grid, kPoolThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(x), n, out);
 }
 
 static size_t score_select_smem(int64_t nkb) {
@@ -250,27 +257,27 @@ static size_t score_select_smem(int64_t nkb) {
     return sizeof(float) * (kHeadDim * kRowsPerCta + kHeadDim * kChunk + kRowsPerCta * nkb_pad);
 }
 
-void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n,
+void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n, int bq,
                          bool causal, float scale, const HeadTable& ht, int64_t kmax,
                          float* scores_out, bool select, int32_t* idx, int32_t* cnt,
                          cudaStream_t s) {
-    const int64_t nqb = (n + kBlock - 1) / kBlock, nkb = nqb;
+    const int64_t nqb = (n + bq - 1) / bq, nkb = (n + kBlock - 1) / kBlock;
     const size_t smem = score_select_smem(nkb);
     cudaFuncSetAttribute(score_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>((nqb + kRowsPerCta - 1) / kRowsPerCta), hq);
-    score_select_kernel<<<grid, kSelThreads, smem, s>>>(qp, kp, hq, hkv, n, nqb, nkb, causal ? 1 : 0,
+    score_select_kernel<<<grid, kSelThreads, smem, s>>>(qp, kp, hq, hkv, n, nqb, nkb, bq, causal ? 1 : 0,
                                                         scale, ht, kmax, scores_out, select ? 1 : 0,
                                                         idx, cnt);
 }
 
-void launch_select_from_scores(const float* scores, int hq, int64_t n, bool causal,
+void launch_select_from_scores(const float* scores, int hq, int64_t n, int bq, bool causal,
                                const HeadTable& ht, int64_t kmax, int32_t* idx, int32_t* cnt,
                                cudaStream_t s) {
-    const int64_t nqb = (n + kBlock - 1) / kBlock, nkb = nqb;
+    const int64_t nqb = (n + bq - 1) / bq, nkb = (n + kBlock - 1) / kBlock;
     const int64_t rows = (int64_t)hq * nqb;
     const unsigned grid = static_cast<unsigned>((rows + (kSelThreads / 32) - 1) / (kSelThreads / 32));
-    select_kernel<<<grid, kSelThreads, 0, s>>>(scores, hq, n, nqb, nkb, causal ? 1 : 0, ht, kmax,
+    select_kernel<<<grid, kSelThreads, 0, s>>>(scores, hq, n, nqb, nkb, bq, causal ? 1 : 0, ht, kmax,
                                                idx, cnt);
 }
 

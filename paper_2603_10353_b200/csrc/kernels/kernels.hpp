@@ -20,20 +20,21 @@ struct HeadTable {
     int32_t kv[kMaxHeads];  // kv head read by this q head
 };
 
-// Kernel 1: x [heads][n][128] bf16 -> out [heads][ceil(n/128)][128] fp32 block means.
-void launch_pool(const void* x, int heads, int64_t n, float* out, cudaStream_t s);
+// Kernel 1: x [heads][n][128] bf16 -> out [heads][ceil(n/rows)][128] fp32 block means
+// (rows = 128 or 256).
+void launch_pool(const void* x, int heads, int64_t n, int rows, float* out, cudaStream_t s);
 
 // Kernel 2 (fused score + select): pooled q [hq][nqb][128], pooled k
 // [hkv][nkb][128]; q head h scores against pooled kv head ht.kv[h]. scores_out (nullable) receives the full score matrix
 // [hq][nqb][nkb] (-inf where causally invisible). With select=true, idx/cnt
 // receive the per-(head, q block) top-k block lists.
-void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n,
+void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n, int bq,
                          bool causal, float scale, const HeadTable& ht, int64_t kmax,
                          float* scores_out, bool select, int32_t* idx, int32_t* cnt,
                          cudaStream_t s);
 
 // Kernel 2 (standalone): selection from a precomputed score matrix.
-void launch_select_from_scores(const float* scores, int hq, int64_t n, bool causal,
+void launch_select_from_scores(const float* scores, int hq, int64_t n, int bq, bool causal,
                                const HeadTable& ht, int64_t kmax, int32_t* idx, int32_t* cnt,
                                cudaStream_t s);
 
@@ -49,6 +50,7 @@ struct FaParams {
     int64_t kmax;
     int64_t n;
     int32_t hq, hkv, nqb;
+    int32_t bq;  // query block rows: 256 (two 128-row halves share each K/V tile) or 128
     int32_t causal;
     float scale_log2;  // (1/sqrt(d)) * log2(e)
     HeadTable heads;   // kv head of each q head (k unused)

@@ -67,6 +67,38 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uin
         : "memory");
 }
 
+// Warp-uniform TMA issue: one elected lane arms `bar` with `bytes` and starts
+// the two 64-column chunk loads of a 128-row x 128-col bf16 tile.
+__device__ __forceinline__ void tma_load_tile_warp(void* dst, const CUtensorMap* m, uint64_t* bar,
+                                                   uint32_t bytes, int32_t row, int32_t plane) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%2], %3;\n\t"
+        "@e cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {0, %4, %5}], [%2];\n\t"
+        "@e cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%6], [%1, {64, %4, %5}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(bytes), "r"(row), "r"(plane),
+        "r"(smem_u32(dst) + 16384)
+        : "memory");
+}
+
+// Same, without arming the barrier (a second tile on an already-armed barrier).
+__device__ __forceinline__ void tma_load_tile_noarm_warp(void* dst, const CUtensorMap* m, uint64_t* bar,
+                                                         int32_t row, int32_t plane) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {0, %3, %4}], [%2];\n\t"
+        "@e cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%5], [%1, {64, %3, %4}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(row), "r"(plane),
+        "r"(smem_u32(dst) + 16384)
+        : "memory");
+}
+
 // Make this thread's generic-proxy shared-memory writes visible to the async
 // proxy (tensor core operand reads).
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -117,6 +149,108 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Warp index the compiler can prove warp-uniform (values derived from it go to
+// uniform registers, branches on it need no divergence handling).
+__device__ __forceinline__ int warp_index_uniform() {
+    return __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x) >> 5, 0);
+}
+
+// One 128x128x128 bf16 product = 8 tcgen05.mma (K = 16 each) issued by one
+// elected lane from a single asm block; descriptors advance by plain adds.
+//   SS, K-major SW128 A and B: k-step kk starts (kk/4)*16 KB + (kk%4)*32 B in,
+//     i.e. descriptor start field +2 per step, +1018 from kk=3 to kk=4.
+__device__ __forceinline__ void mma_tile_ss_kmajor(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                   uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a, b;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.u32 t, 0, 0;\n\t"
+        "mov.b64 a, %1;\n\tmov.b64 b, %2;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, p;\n\t"
+        "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, a, 1018;\n\tadd.s64 b, b, 1018;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+//   TS: A from TMEM (+8 columns per k-step), B MN-major SW128 (+2 KB = +128
+//     in the start field per k-step of 16 keys).
+__device__ __forceinline__ void mma_tile_ts_mnmajor(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                    uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b64 b;\n\t.reg .b32 a;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.u32 t, 0, 0;\n\t"
+        "mov.b32 a, %1;\n\tmov.b64 b, %2;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, p;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Warp-uniform variants: every lane of the warp executes the statement and
+// elect.sync picks the one lane that issues, inside the same asm block. With
+// the lane choice hidden from the compiler's control flow, ptxas emits a plain
+// UTCHMMA/UTCBAR instead of wrapping each one in an ELECT/BRA.U.ANY loop
+// (which cost ~110 cycles per MMA when issued from a `lane == 0` branch).
+__device__ __forceinline__ void mma_bf16_ss_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                 uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_bf16_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                 uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            smem_u32(bar))
         : "memory");
 }
 
@@ -222,9 +356,29 @@ __device__ __forceinline__ void setmaxnreg_dec() {
 // ----------------------------------------------------------------- math --
 
 __device__ __forceinline__ float ex2(float x) {
+#ifdef SHPLB_DIAG_FAKE_EXP  // dev-only diagnostic: take MUFU off the path
+    return x * 1.0001f;
+#else
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+#endif
+}
+
+// 2^x on the FMA/ALU pipes (no MUFU): round-to-nearest split x = j + f with
+// the 1.5*2^23 magic constant, cubic minimax 2^f on [-0.5, 0.5] (max relative
+// error 1.4e-4, far below bf16's 3.9e-3), exponent added in the integer
+// domain. x is clamped at -125 (2^-125 ~ 2e-38): callers use it only where no
+// element is masked to -inf.
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -125.0f);
+    const float t = __fadd_rn(x, 12582912.0f);
+    const float j = __fsub_rn(t, 12582912.0f);
+    const float f = __fsub_rn(x, j);
+    float p = __fmaf_rn(0.05546969920f, f, 0.24239382148f);
+    p = __fmaf_rn(p, f, 0.69318938255f);
+    p = __fmaf_rn(p, f, 0.99993973970f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

@@ -83,11 +83,19 @@ CUtensorMap make_tmap(const void* base, int64_t heads, int64_t n) {
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-int64_t visible_blocks(int64_t qb, int64_t n, bool causal) {
+// Key blocks (of 128 keys) visible to query block qb of bq rows.
+int64_t visible_blocks(int64_t qb, int64_t n, int64_t bq, bool causal) {
     const int64_t nkb = cdiv(n, kern::kBlock);
     if (!causal) return nkb;
-    const int64_t last = std::min((qb + 1) * kern::kBlock, n) - 1;
+    const int64_t last = std::min((qb + 1) * bq, n) - 1;
     return std::min(last / kern::kBlock + 1, nkb);
+}
+
+// Query halves (128-row tiles of kernel 3) of block qb that hold rows < n.
+int64_t live_halves(int64_t qb, int64_t n, int64_t bq) {
+    int64_t c = 0;
+    for (int64_t hf = 0; hf < bq / kern::kBlock; ++hf) c += qb * bq + hf * kern::kBlock < n;
+    return c;
 }
 
 void check_shape(const shplb_layer_shape* s) {
@@ -104,8 +112,8 @@ void check_shape(const shplb_layer_shape* s) {
         throw NotSupported("at most " + std::to_string(kern::kMaxHeads) + " query heads per call");
     if (s->head_dim != kern::kHeadDim)
         throw NotSupported("head_dim " + std::to_string(s->head_dim) + " not supported (kernels are built for 128)");
-    if (s->block_q != kern::kBlock || s->block_k != kern::kBlock)
-        throw NotSupported("block sizes must be 128 x 128");
+    if ((s->block_q != 128 && s->block_q != 256) || s->block_k != kern::kBlock)
+        throw NotSupported("block sizes must be block_q in {128, 256}, block_k = 128");
     if (s->kind != SHPLB_BLOCK_TOPK) throw NotSupported("selection kind not supported");
     if (s->seq_len > (int64_t(1) << 26)) throw NotSupported("seq_len too large");
 }
@@ -247,15 +255,15 @@ void mark(shplb_ctx* ctx, int slot, cudaStream_t st) {
 void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const void* k,
                     const kern::HeadTable& kb, int64_t kmax, float* scores_out, bool select,
                     int32_t* idx, int32_t* cnt, cudaStream_t st) {
-    const int64_t nb = cdiv(s->seq_len, kern::kBlock);
-    grow(ctx->qp, ctx->qp_bytes, sizeof(float) * s->num_q_heads * nb * kern::kHeadDim);
-    grow(ctx->kp, ctx->kp_bytes, sizeof(float) * s->num_kv_heads * nb * kern::kHeadDim);
+    const int64_t nqb = cdiv(s->seq_len, s->block_q), nkb = cdiv(s->seq_len, kern::kBlock);
+    grow(ctx->qp, ctx->qp_bytes, sizeof(float) * s->num_q_heads * nqb * kern::kHeadDim);
+    grow(ctx->kp, ctx->kp_bytes, sizeof(float) * s->num_kv_heads * nkb * kern::kHeadDim);
     if (select) mark(ctx, 0, st);
-    kern::launch_pool(q, s->num_q_heads, s->seq_len, ctx->qp, st);
-    kern::launch_pool(k, s->num_kv_heads, s->seq_len, ctx->kp, st);
+    kern::launch_pool(q, s->num_q_heads, s->seq_len, s->block_q, ctx->qp, st);
+    kern::launch_pool(k, s->num_kv_heads, s->seq_len, kern::kBlock, ctx->kp, st);
     if (select) mark(ctx, 1, st);
     const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(s->head_dim)));
-    kern::launch_score_select(ctx->qp, ctx->kp, s->num_q_heads, s->num_kv_heads, s->seq_len,
+    kern::launch_score_select(ctx->qp, ctx->kp, s->num_q_heads, s->num_kv_heads, s->seq_len, s->block_q,
                               s->causal != 0, scale, kb, kmax, scores_out, select, idx, cnt, st);
     check_launch(ctx, 3);
     if (select) mark(ctx, 2, st);
@@ -264,21 +272,23 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
 // Kernel-3 work list: every (head, query block) tile, heaviest first (LPT), so
 // the hardware block scheduler hands out long tiles before short ones.
 void build_tiles(shplb_ctx* ctx, const shplb_layer_shape* s, const std::vector<int32_t>& kblocks) {
-    std::vector<int64_t> key = {s->seq_len, s->causal};
+    std::vector<int64_t> key = {s->seq_len, s->causal, s->block_q, s->num_q_heads};
     key.insert(key.end(), kblocks.begin(), kblocks.end());
     auto it = ctx->work_lists.find(key);
     if (it != ctx->work_lists.end()) {
         ctx->current = &it->second;
         return;
     }
-    const int64_t nqb = cdiv(s->seq_len, kern::kBlock);
+    const int64_t nqb = cdiv(s->seq_len, s->block_q);
     std::vector<int32_t> tiles;
     std::vector<int32_t> work;
     tiles.reserve(static_cast<size_t>(s->num_q_heads * nqb));
     for (int h = 0; h < s->num_q_heads; ++h)
         for (int64_t qb = 0; qb < nqb; ++qb) {
             tiles.push_back((h << 20) | static_cast<int32_t>(qb));
-            work.push_back(static_cast<int32_t>(std::min<int64_t>(kblocks[h], visible_blocks(qb, s->seq_len, s->causal != 0))));
+            work.push_back(static_cast<int32_t>(
+                std::min<int64_t>(kblocks[h], visible_blocks(qb, s->seq_len, s->block_q, s->causal != 0)) *
+                live_halves(qb, s->seq_len, s->block_q)));
         }
     std::vector<size_t> order(tiles.size());
     std::iota(order.begin(), order.end(), size_t{0});
@@ -310,7 +320,8 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     p.n = s->seq_len;
     p.hq = s->num_q_heads;
     p.hkv = s->num_kv_heads;
-    p.nqb = static_cast<int32_t>(cdiv(s->seq_len, kern::kBlock));
+    p.nqb = static_cast<int32_t>(cdiv(s->seq_len, s->block_q));
+    p.bq = s->block_q;
     p.causal = s->causal;
     fill_kv_map(s, p.heads);
     p.scale_log2 = static_cast<float>((1.0 / std::sqrt(static_cast<double>(s->head_dim))) * 1.4426950408889634);
@@ -432,7 +443,8 @@ int shplb_select_blocks(shplb_ctx* ctx, const shplb_layer_shape* shape, const fl
         }
         if (kmax < need) throw InvalidArgument("kmax " + std::to_string(kmax) + " < largest k " + std::to_string(need));
         DeviceGuard g(ctx->device);
-        kern::launch_select_from_scores(scores, shape->num_q_heads, shape->seq_len, shape->causal != 0,
+        kern::launch_select_from_scores(scores, shape->num_q_heads, shape->seq_len, shape->block_q,
+                                        shape->causal != 0,
                                         kb, kmax, idx_out, cnt_out, static_cast<cudaStream_t>(stream));
         check_launch(ctx);
     });
@@ -475,7 +487,7 @@ int shplb_sparse_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape,
         DeviceGuard g(ctx->device);
         auto st = static_cast<cudaStream_t>(stream);
         if (shape->validate) validate_inputs(ctx, shape, q, k, v, st);
-        const int64_t nqb = cdiv(shape->seq_len, kern::kBlock);
+        const int64_t nqb = cdiv(shape->seq_len, shape->block_q);
         grow(ctx->idx, ctx->idx_bytes, sizeof(int32_t) * shape->num_q_heads * nqb * kmax);
         grow(ctx->cnt, ctx->cnt_bytes, sizeof(int32_t) * shape->num_q_heads * nqb);
         build_tiles(ctx, shape, kbl);
@@ -552,11 +564,12 @@ int shplb_layer_work(const shplb_layer_shape* shape, const int64_t* budgets_toke
         check_shape(shape);
         std::vector<int32_t> kbl;
         budgets_to_blocks(shape, budgets_tokens, kbl);
-        const int64_t nqb = cdiv(shape->seq_len, kern::kBlock);
-        int64_t tiles = 0;
+        const int64_t nqb = cdiv(shape->seq_len, shape->block_q);
+        int64_t tiles = 0;  // (128-row query half, key block) tiles, upper bound (see header)
         for (int h = 0; h < shape->num_q_heads; ++h)
             for (int64_t qb = 0; qb < nqb; ++qb)
-                tiles += std::min<int64_t>(kbl[h], visible_blocks(qb, shape->seq_len, shape->causal != 0));
+                tiles += std::min<int64_t>(kbl[h], visible_blocks(qb, shape->seq_len, shape->block_q, shape->causal != 0)) *
+                         live_halves(qb, shape->seq_len, shape->block_q);
         if (selected_tiles_out) *selected_tiles_out = tiles;
         if (flops_out)
             *flops_out = 4.0 * shape->head_dim * double(kern::kBlock) * double(kern::kBlock) * double(tiles);

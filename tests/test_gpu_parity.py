@@ -37,31 +37,31 @@ def _scores_equal(a: np.ndarray, b: np.ndarray) -> bool:
     return np.array_equal(a.view(np.uint32), b.view(np.uint32))
 
 
-def run_case(ctx, spec: LayerSpec, k_blocks, causal=True):
+def run_case(ctx, spec: LayerSpec, k_blocks, causal=True, bq=256):
     q, k, v = make_layer(spec, "cpu")
     qb, kb, vb = bf16_bits(q), bf16_bits(k), bf16_bits(v)
     k_blocks = np.asarray(k_blocks, np.int64)
     nkb = (spec.seq_len + 127) // 128
     kmax = int(min(nkb, k_blocks.max()))
-    sc_o, idx_o, cnt_o, out_o = O.layer(qb, kb, vb, k_blocks, causal=causal, kmax=kmax)
+    sc_o, idx_o, cnt_o, out_o = O.layer(qb, kb, vb, k_blocks, bq=bq, causal=causal, kmax=kmax)
     qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
 
-    sc = ctx.block_scores(qd, kd, causal=causal)
+    sc = ctx.block_scores(qd, kd, causal=causal, block_q=bq)
     torch.cuda.synchronize()
     assert _scores_equal(sc.cpu().numpy(), sc_o), "kernel 1 scores differ from the oracle"
 
-    idx, cnt = ctx.select_blocks(sc, k_blocks, spec.seq_len, causal=causal, kmax=kmax)
+    idx, cnt = ctx.select_blocks(sc, k_blocks, spec.seq_len, causal=causal, kmax=kmax, block_q=bq)
     torch.cuda.synchronize()
     assert np.array_equal(cnt.cpu().numpy(), cnt_o), "kernel 2 counts differ"
     assert np.array_equal(idx.cpu().numpy(), idx_o), "kernel 2 block sets differ"
 
-    out = ctx.block_sparse_attention(qd, kd, vd, idx, cnt, causal=causal)
+    out = ctx.block_sparse_attention(qd, kd, vd, idx, cnt, causal=causal, block_q=bq)
     torch.cuda.synchronize()
     mx, rel = _errors(out, out_o)
     assert mx <= MAX_ABS and rel <= MEAN_REL, f"kernel 3: max-abs {mx:.3e}, mean-rel {rel:.3e}"
 
     budgets = np.minimum(k_blocks * 128, spec.seq_len)
-    out2 = ctx.sparse_attention_layer(qd, kd, vd, budgets, causal=causal)
+    out2 = ctx.sparse_attention_layer(qd, kd, vd, budgets, causal=causal, block_q=bq)
     torch.cuda.synchronize()
     idx2, cnt2 = ctx.last_selection(spec.num_q_heads, spec.seq_len)
     assert np.array_equal(cnt2.cpu().numpy(), cnt_o)
@@ -70,24 +70,28 @@ def run_case(ctx, spec: LayerSpec, k_blocks, causal=True):
     return mx, rel
 
 
+@pytest.mark.parametrize("bq", [256, 128])
 @pytest.mark.parametrize("causal", [True, False])
-def test_small_gqa_layer(cuda_ctx, causal):
+def test_small_gqa_layer(cuda_ctx, causal, bq):
     spec = LayerSpec(num_q_heads=4, num_kv_heads=2, seq_len=1024, seed=1)
-    run_case(cuda_ctx, spec, [1, 3, 8, 5], causal=causal)
+    run_case(cuda_ctx, spec, [1, 3, 8, 5], causal=causal, bq=bq)
 
 
-@pytest.mark.parametrize("n", [1, 100, 128, 129, 1000, 1536])
-def test_ragged_lengths(cuda_ctx, n):
+@pytest.mark.parametrize("bq", [256, 128])
+@pytest.mark.parametrize("n", [1, 100, 128, 129, 256, 300, 1000, 1536])
+def test_ragged_lengths(cuda_ctx, n, bq):
     spec = LayerSpec(num_q_heads=2, num_kv_heads=1, seq_len=n, seed=7 + n)
     nkb = (n + 127) // 128
-    run_case(cuda_ctx, spec, [1, max(1, nkb // 2 + 1)], causal=True)
-    run_case(cuda_ctx, spec, [nkb, 1], causal=False)
+    run_case(cuda_ctx, spec, [1, max(1, nkb // 2 + 1)], causal=True, bq=bq)
+    run_case(cuda_ctx, spec, [nkb, 1], causal=False, bq=bq)
 
 
-def test_mha_and_wide_gqa(cuda_ctx):
-    run_case(cuda_ctx, LayerSpec(num_q_heads=3, num_kv_heads=3, seq_len=768, seed=3), [2, 6, 1])
+@pytest.mark.parametrize("bq", [256, 128])
+def test_mha_and_wide_gqa(cuda_ctx, bq):
+    run_case(cuda_ctx, LayerSpec(num_q_heads=3, num_kv_heads=3, seq_len=768, seed=3), [2, 6, 1],
+             bq=bq)
     run_case(cuda_ctx, LayerSpec(num_q_heads=8, num_kv_heads=1, seq_len=640, seed=4),
-             [1, 2, 3, 4, 5, 5, 2, 1])
+             [1, 2, 3, 4, 5, 5, 2, 1], bq=bq)
 
 
 def test_full_budget_equals_dense(cuda_ctx):
@@ -111,11 +115,13 @@ def test_full_budget_equals_dense(cuda_ctx):
         assert mx <= MAX_ABS and rel <= MEAN_REL, (h, mx, rel)
 
 
-def test_single_kept_block_is_block_softmax(cuda_ctx):
+@pytest.mark.parametrize("bq", [256, 128])
+def test_single_kept_block_is_block_softmax(cuda_ctx, bq):
     """k = 1: each query block keeps exactly one key block (cf. 'budget one keeps
-    the argmax key', test_attention.cpp:128-141, at block granularity)."""
+    the argmax key', test_attention.cpp:128-141, at block granularity). With
+    bq = 256 and a future-half block kept, the first half's rows are zero."""
     spec = LayerSpec(num_q_heads=2, num_kv_heads=2, seq_len=512, seed=5)
-    run_case(cuda_ctx, spec, [1, 1], causal=True)
+    run_case(cuda_ctx, spec, [1, 1], causal=True, bq=bq)
 
 
 def test_ties_break_toward_lower_block(cuda_ctx):
@@ -128,9 +134,9 @@ def test_ties_break_toward_lower_block(cuda_ctx):
         k[:, b * 128:(b + 1) * 128] = k[:, 0:128]
     qb, kb, vb = bf16_bits(q), bf16_bits(k), bf16_bits(v)
     k_blocks = np.array([3, 2], np.int64)
-    sc_o, idx_o, cnt_o, out_o = O.layer(qb, kb, vb, k_blocks, causal=False, kmax=3)
-    sc = cuda_ctx.block_scores(q.cuda(), k.cuda(), causal=False)
-    idx, cnt = cuda_ctx.select_blocks(sc, k_blocks, 1024, causal=False, kmax=3)
+    sc_o, idx_o, cnt_o, out_o = O.layer(qb, kb, vb, k_blocks, bq=128, causal=False, kmax=3)
+    sc = cuda_ctx.block_scores(q.cuda(), k.cuda(), causal=False, block_q=128)
+    idx, cnt = cuda_ctx.select_blocks(sc, k_blocks, 1024, causal=False, kmax=3, block_q=128)
     torch.cuda.synchronize()
     assert np.array_equal(idx.cpu().numpy(), idx_o)
     assert (idx_o[0, :, :3] == np.array([0, 1, 2])).all()
@@ -182,11 +188,12 @@ def test_deterministic(cuda_ctx):
     assert torch.equal(a, c)
 
 
-def test_c1_shape_two_heads_full_oracle(cuda_ctx):
+@pytest.mark.parametrize("bq", [256, 128])
+def test_c1_shape_two_heads_full_oracle(cuda_ctx, bq):
     """Llama-3-8B-shaped (d=128) 8K prefill, two q heads of one GQA group,
     heterogeneous budgets; full oracle comparison."""
     spec = LayerSpec(num_q_heads=2, num_kv_heads=1, seq_len=8192, seed=2603)
-    run_case(cuda_ctx, spec, [4, 24], causal=True)
+    run_case(cuda_ctx, spec, [4, 24], causal=True, bq=bq)
 
 
 @pytest.mark.slow
@@ -203,8 +210,8 @@ def test_c3_size_sampled_rows(cuda_ctx):
     torch.cuda.synchronize()
     idx, cnt = cuda_ctx.last_selection(32, n)
     idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
-    nqb = n // 128
-    vis = np.arange(1, nqb + 1)
+    nqb = n // 256
+    vis = 2 * np.arange(1, nqb + 1)  # a 256-row block sees 2 more key blocks per step
     kb = (budgets + 127) // 128
     assert np.array_equal(cnt, np.minimum(kb[:, None], vis[None, :]))
     for h in rng.choice(32, 4, replace=False):
@@ -212,14 +219,14 @@ def test_c3_size_sampled_rows(cuda_ctx):
         qbits, kbits, vbits = bf16_bits(q[h]), bf16_bits(k[g]), bf16_bits(v[g])
         kp = O.pool_blocks(kbits, 128)
         qbs = sorted(set(rng.choice(nqb, 3, replace=False).tolist() + [nqb - 1]))
-        sc = O.pooled_scores_rows(qbits, kp, qbs)
+        sc = O.pooled_scores_rows(qbits, kp, qbs, bq=256)
         for r, qbk in enumerate(qbs):
             c = cnt[h, qbk]
             sel = idx[h, qbk, :c]
-            assert (np.diff(sel) > 0).all() and sel.min() >= 0 and sel.max() <= qbk
-            want = np.sort(O.topk_row(sc[r, :qbk + 1].astype(np.float64), c))
+            assert (np.diff(sel) > 0).all() and sel.min() >= 0 and sel.max() <= 2 * qbk + 1
+            want = np.sort(O.topk_row(sc[r, :2 * qbk + 2].astype(np.float64), c))
             assert np.array_equal(sel, want), (h, qbk)
-            rows = [qbk * 128, qbk * 128 + 77, qbk * 128 + 127]
+            rows = [qbk * 256, qbk * 256 + 77, qbk * 256 + 128, qbk * 256 + 255]
             ref = O.sparse_rows(qbits, kbits, vbits, rows, sel.tolist())
             mx, rel = _errors(out[h, rows], ref)
             assert mx <= MAX_ABS and rel <= MEAN_REL, (h, qbk, mx, rel)

@@ -219,7 +219,12 @@ def test_profile_curves_match_reference_build_profiles():
 
 def test_layer_work_counts_selected_tiles():
     # 1 head, 4 query blocks, causal: visible 1,2,3,4; k=2 -> 1+2+2+2 = 7 tiles
-    tiles, flops = P.layer_work(1, 1, 512, [256], causal=True)
+    tiles, flops = P.layer_work(1, 1, 512, [256], causal=True, block_q=128)
     assert tiles == 7 and flops == 4 * 128 * 128 * 128 * 7
-    tiles, _ = P.layer_work(2, 1, 512, [512, 1], causal=False)
+    tiles, _ = P.layer_work(2, 1, 512, [512, 1], causal=False, block_q=128)
     assert tiles == 16 + 4
+    # bq = 256: 2 query blocks x 2 live halves; visible key blocks 2 and 4, k = 2
+    tiles, _ = P.layer_work(1, 1, 512, [256], causal=True, block_q=256)
+    assert tiles == 2 * 2 + 2 * 2
+    tiles, _ = P.layer_work(1, 1, 300, [300], causal=True, block_q=256)  # 2nd block: 1 live half
+    assert tiles == 2 * 2 + 3 * 1

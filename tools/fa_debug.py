@@ -23,7 +23,7 @@ def case(ctx, hq, hkv, n, kblocks, causal, seed=1):
     kblocks = np.asarray(kblocks, np.int64)
     nkb = (n + 127) // 128
     kmax = int(min(nkb, kblocks.max()))
-    sc_o, idx_o, cnt_o, out_o = O.layer(qb, kb, vb, kblocks, causal=causal, kmax=kmax)
+    sc_o, idx_o, cnt_o, out_o = O.layer(qb, kb, vb, kblocks, bq=256, causal=causal, kmax=kmax)
     qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
     sc = ctx.block_scores(qd, kd, causal=causal)
     torch.cuda.synchronize()

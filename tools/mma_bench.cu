@@ -1,0 +1,101 @@
+// Microbenchmark (dev tool): sustained tcgen05.mma throughput per SM for the
+// operand modes kernel 3 uses. One CTA per SM, one thread issues `iters`
+// MMAs back to back (commit + wait every 8 to bound the queue), operands
+// resident in shared memory / TMEM (contents irrelevant), 148 CTAs.
+//   mode 0: SS  M128 N128 K16 (A, B from smem)          - QK^T
+//   mode 1: TS  M128 N128 K16 (A from TMEM, B smem)     - P.V
+//   mode 2: SS  M128 N256 K16
+//   mode 3: SS  alternating two A tiles, same B         - S_A / S_B of one K tile
+//   mode 4: SS + TMA-like smem writes by other warps (st.shared 16 B loop)
+// Prints achieved TFLOP/s (2*M*N*K per MMA) and cycles per MMA.
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2603_10353_b200/csrc/kernels tools/mma_bench.cu -o /tmp/mma_bench
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#include "ptx.cuh"
+
+using namespace shplb::ptx;
+
+__global__ void __launch_bounds__(256, 1) mma_kernel(int mode, int iters, unsigned long long* cycles) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(8) uint64_t bar[2];
+    const int warp = warp_index_uniform();
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc<512>(&tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base;
+    const uint32_t a0 = smem_u32(smem), a1 = smem_u32(smem + 32768), b = smem_u32(smem + 65536);
+    const uint32_t n = (mode == 2) ? 256 : 128;
+    const uint32_t idesc = idesc_bf16_f32(128, n, 0, mode == 1 ? 1 : 0);
+    volatile int stop = 0;
+    if (warp == 1) {  // whole warp, elected lane issues (warp-uniform control flow)
+        const long long t0 = clock64();
+        const uint64_t bd = umma_desc_sw128(b, 16, 1024);
+        const uint64_t vd = umma_desc_sw128(b, 16384, 1024);
+        const uint64_t ad0 = umma_desc_sw128(a0, 16, 1024), ad1 = umma_desc_sw128(a1, 16, 1024);
+        for (int grp = 0; grp < (iters >> 3); ++grp) {  // 8 MMAs per group, committed to bar[grp & 1]
+            if (grp >= 2) mbar_wait(&bar[grp & 1], ((grp - 2) >> 1) & 1);
+            if (mode == 1) {
+                mma_tile_ts_mnmajor(tmem + 256, tmem + 384, vd, idesc, 1u);
+            } else {
+                mma_tile_ss_kmajor(tmem, (mode == 3 && (grp & 1)) ? ad1 : ad0, bd, idesc, 1u);
+            }
+            mma_commit_warp(&bar[grp & 1]);  // at most 2 groups in flight
+        }
+        const int last = (iters >> 3) - 1;  // iters is a multiple of 8
+        mbar_wait(&bar[last & 1], (last >> 1) & 1);
+        if (last >= 1) mbar_wait(&bar[(last - 1) & 1], ((last - 1) >> 1) & 1);
+        const long long t1 = clock64();
+        if ((threadIdx.x & 31) == 0) cycles[blockIdx.x] = static_cast<unsigned long long>(t1 - t0);
+        stop = 1;
+    } else if (mode == 4 && warp >= 2) {
+        // Background smem writes (stand-in for TMA fills): 6 warps x 16 B stores.
+        uint4* dst = reinterpret_cast<uint4*>(smem + 98304);
+        uint4 v = make_uint4(threadIdx.x, 1, 2, 3);
+        for (int i = 0; i < iters * 4; ++i) dst[(threadIdx.x + i * 192) & 2047] = v;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+int main(int argc, char** argv) {
+    const int iters = argc > 1 ? atoi(argv[1]) : 20000;
+    unsigned long long* d;
+    cudaMalloc(&d, 148 * sizeof(unsigned long long));
+    cudaFuncSetAttribute(mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const char* names[] = {"SS M128N128", "TS M128N128", "SS M128N256", "SS alt-A  ", "SS+stores  "};
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    for (int mode = 0; mode < 5; ++mode) {
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        mma_kernel<<<148, 256, 200 * 1024>>>(mode, 1000, d);  // warm-up
+        cudaEventRecord(e0);
+        mma_kernel<<<148, 256, 200 * 1024>>>(mode, iters, d);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        unsigned long long h[148];
+        cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+        double avg = 0;
+        for (int i = 0; i < 148; ++i) avg += h[i];
+        avg /= 148;
+        const double n = mode == 2 ? 256 : 128;
+        const double flops = 2.0 * 128 * n * 16 * iters * 148;
+        printf("%s  %8.1f TFLOP/s  %6.1f cycles/MMA (floor %d)  err=%s\n", names[mode],
+               flops / (ms * 1e-3) / 1e12, avg / iters, mode == 2 ? 128 : 64,
+               cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+}
