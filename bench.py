@@ -413,11 +413,12 @@ def main():
         ms, stages, launches, out_local = time_device(ctx, ql, kl, vl, bl, kv_map, args.steps,
                                                       args.warmup, world, stream)
         clocks = sampler.stop() if sampler else None
-        tiles, flops = P.layer_work(len(heads), len(kv_needed), n, bl, causal=True, kv_map=kv_map)
+        tiles, flops = ctx.last_selection_work()  # exact tiles of the last timed call
         per_rank = allgather_float(ms, world)
         per_rank_k3 = allgather_float(float(stages[2]), world)
         res = {"ms": max(per_rank), "per_rank_ms": per_rank, "stages": stages, "launches": launches,
                "clocks": clocks, "flops_local": flops, "heads": heads,
+               "flops_total": sum(allgather_float(flops, world)),
                "bubble": P.barrier(per_rank).bubble_fraction,
                "k3_bubble": P.barrier(per_rank_k3).bubble_fraction,
                "load_imbalance": P.imbalance(budgets, plan, world).imbalance}
@@ -432,7 +433,7 @@ def main():
         torch.cuda.empty_cache()
 
     g = results["greedy"]
-    _, flops_total = P.layer_work(hq, args.kv_heads, n, budgets, causal=True)
+    flops_total = g["flops_total"]
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -476,7 +477,8 @@ def main():
                      "peak_source": f"{peaks_src} bf16 dense "
                                     f"{'sustained' if 'bf16_tflops_sustained' in peaks else 'burst'}",
                      "flops_per_launch": g["flops_local"],
-                     "flops_formula": "4*d*bq*bk*selected_tiles (diagonal tiles counted in full)",
+                     "flops_formula": "4*d*128*128*computed (query half, key block) tiles, counted "
+                                      "from the selection (diagonal tiles counted in full)",
                      "traffic": traffic},
         "gpu_launches": g["launches"],
         "clocks": g["clocks"],

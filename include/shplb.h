@@ -221,10 +221,18 @@ int shplb_last_selection(const shplb_ctx* ctx, const int32_t** idx, const int32_
 int shplb_copy_last_selection(const shplb_ctx* ctx, int32_t* idx_dst, int64_t idx_elems,
                               int32_t* cnt_dst, int64_t cnt_elems, void* stream);
 
-/* Algorithmic work of one layer call, for roofline accounting:
- * selected (head, q-block, k-block) tiles, and the FLOPs 4*d*bq*bk*tiles. */
+/* Algorithmic work of one layer call before selection, for roofline accounting
+ * (DESIGN.md §5): 128x128 (query half, key block) tiles = per query block
+ * min(k_h, visible key blocks) x query halves holding rows, and FLOPs
+ * 4*d*128*128*tiles. An upper bound by at most one tile per query block: a
+ * kept key block entirely in the causal future of the first half is skipped. */
 int shplb_layer_work(const shplb_layer_shape* shape, const int64_t* budgets_tokens,
                      int64_t* selected_tiles_out, double* flops_out);
+
+/* Exact work of the last layer call on this context: the (query half, key
+ * block) tiles kernel 3 computed, counted from the selection (copies it to the
+ * host; synchronises the device). FLOPs = 4*d*128*128*tiles. */
+int shplb_last_selection_work(const shplb_ctx* ctx, int64_t* tiles_out, double* flops_out);
 
 #ifdef __cplusplus
 }

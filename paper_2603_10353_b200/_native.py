@@ -26,7 +26,7 @@ EXPORTS = (
     "shplb_block_scores", "shplb_select_blocks", "shplb_block_sparse_attention",
     "shplb_sparse_attention_layer", "shplb_sparse_attention_layer_host",
     "shplb_last_selection", "shplb_copy_last_selection",
-    "shplb_layer_work",
+    "shplb_layer_work", "shplb_last_selection_work",
 )
 
 SHPLB_OK = 0
@@ -144,6 +144,7 @@ def lib() -> C.CDLL:
     L.shplb_last_selection.argtypes = [vp, P(vp), P(vp), P(i64)]
     L.shplb_copy_last_selection.argtypes = [vp, vp, i64, vp, i64, vp]
     L.shplb_layer_work.argtypes = [P(LayerShape), vp, P(i64), P(f64)]
+    L.shplb_last_selection_work.argtypes = [vp, P(i64), P(f64)]
     _lib = L
     return L
 

@@ -346,6 +346,12 @@ class Context:
             C.c_void_p(v.data_ptr()), _ptr(b), C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out
 
+    def last_selection_work(self):
+        """(tiles, FLOPs) kernel 3 computed in the last layer call (exact; syncs)."""
+        t, f = C.c_int64(), C.c_double()
+        check(lib().shplb_last_selection_work(self._h, C.byref(t), C.byref(f)))
+        return int(t.value), float(f.value)
+
     def last_selection(self, num_q_heads: int, seq_len: int):
         """(idx, cnt) of the last layer call as torch views over the context workspace."""
         import torch

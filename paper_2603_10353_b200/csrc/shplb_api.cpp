@@ -174,9 +174,13 @@ struct shplb_ctx {
     size_t cnt_bytes = 0;
     int32_t* flag = nullptr;
     void* host_io = nullptr;  // device staging for shplb_sparse_attention_layer_host
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;  // its H2D / D2H copy streams
+    std::vector<cudaEvent_t> chunk_events;
     size_t host_io_bytes = 0;
     int64_t last_kmax = 0;
     int64_t last_rows = 0;  // Hq * nqb of the last layer call
+    int64_t last_n = 0, last_nqb = 0;
+    int32_t last_bq = 0, last_causal = 0;
     // Kernel-3 work lists, one per (seq_len, causal, blocks-per-head) seen.
     // Never overwritten, so an in-flight launch never sees its list change.
     struct WorkList {
@@ -371,6 +375,9 @@ int shplb_ctx_destroy(shplb_ctx* ctx) {
         for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
         cudaFree(ctx->flag);
         cudaFree(ctx->host_io);
+        if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
+        if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
+        for (cudaEvent_t e : ctx->chunk_events) cudaEventDestroy(e);
         delete ctx;
     });
 }
@@ -496,6 +503,10 @@ int shplb_sparse_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape,
         mark(ctx, 3, st);
         ctx->last_kmax = kmax;
         ctx->last_rows = shape->num_q_heads * nqb;
+        ctx->last_n = shape->seq_len;
+        ctx->last_nqb = nqb;
+        ctx->last_bq = shape->block_q;
+        ctx->last_causal = shape->causal;
     });
 }
 
@@ -522,13 +533,74 @@ int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* s
         }
         auto* base = static_cast<uint8_t*>(ctx->host_io);
         auto st = static_cast<cudaStream_t>(stream);
-        SHPLB_CUDA(cudaMemcpyAsync(base + q_off, q_host, qb, cudaMemcpyHostToDevice, st));
-        SHPLB_CUDA(cudaMemcpyAsync(base + k_off, k_host, kb, cudaMemcpyHostToDevice, st));
-        SHPLB_CUDA(cudaMemcpyAsync(base + v_off, v_host, kb, cudaMemcpyHostToDevice, st));
-        rc = shplb_sparse_attention_layer(ctx, shape, base + q_off, base + k_off, base + v_off,
-                                          budgets_tokens, base + o_off, stream);
-        if (rc != SHPLB_OK) return;  // message already recorded
-        SHPLB_CUDA(cudaMemcpyAsync(out_host, base + o_off, qb, cudaMemcpyDeviceToHost, st));
+        // Pipeline by KV-head chunks (standard GQA grouping only): chunk c's
+        // H2D copies on a copy stream overlap chunk c-1's kernels on the
+        // caller's stream, whose D2H copy runs on a second copy stream (the
+        // two PCIe directions are independent). Compute stays serial on one
+        // stream, so the context workspace is reused safely.
+        // A chunk is a run of kv heads [g0, g1) plus the q heads reading them;
+        // that q range is contiguous when the kv map is non-decreasing (the
+        // standard grouping, and every head-parallel shard built by rank_shard).
+        const int32_t hkv = shape->num_kv_heads, hq = shape->num_q_heads;
+        kern::HeadTable map{};
+        fill_kv_map(shape, map);
+        bool monotone = true;
+        for (int32_t h = 1; h < hq; ++h) monotone &= map.kv[h] >= map.kv[h - 1];
+        const int32_t chunks = monotone ? std::min<int32_t>(hkv, 8) : 1;
+        auto q_begin = [&](int32_t g) {  // first q head whose kv head is >= g
+            int32_t h = 0;
+            while (h < hq && map.kv[h] < g) ++h;
+            return h;
+        };
+        if (!ctx->copy_in) {
+            SHPLB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
+            SHPLB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+        }
+        while (ctx->chunk_events.size() < 3 * static_cast<size_t>(chunks) + 1) {
+            cudaEvent_t e;
+            SHPLB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ctx->chunk_events.push_back(e);
+        }
+        cudaEvent_t start = ctx->chunk_events[0];
+        SHPLB_CUDA(cudaEventRecord(start, st));  // copies may not overtake earlier work on `st`
+        SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_in, start, 0));
+        SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_out, start, 0));
+        const size_t row_bytes = sizeof(uint16_t) * shape->seq_len * shape->head_dim;  // one head
+        for (int32_t c = 0; c < chunks; ++c) {
+            const int32_t g0 = monotone ? hkv * c / chunks : 0, g1 = monotone ? hkv * (c + 1) / chunks : hkv;
+            const int32_t h0 = monotone ? q_begin(g0) : 0, h1 = monotone ? q_begin(g1) : hq;
+            if (h1 == h0) continue;  // kv heads no q head reads: nothing to compute or copy
+            std::vector<int32_t> sub(static_cast<size_t>(h1 - h0));
+            for (int32_t h = h0; h < h1; ++h) sub[h - h0] = map.kv[h] - g0;
+            cudaEvent_t in_done = ctx->chunk_events[1 + 3 * c], comp_done = ctx->chunk_events[2 + 3 * c];
+            SHPLB_CUDA(cudaMemcpyAsync(base + q_off + h0 * row_bytes, q_host + h0 * row_bytes / 2,
+                                       (h1 - h0) * row_bytes, cudaMemcpyHostToDevice, ctx->copy_in));
+            SHPLB_CUDA(cudaMemcpyAsync(base + k_off + g0 * row_bytes, k_host + g0 * row_bytes / 2,
+                                       (g1 - g0) * row_bytes, cudaMemcpyHostToDevice, ctx->copy_in));
+            SHPLB_CUDA(cudaMemcpyAsync(base + v_off + g0 * row_bytes, v_host + g0 * row_bytes / 2,
+                                       (g1 - g0) * row_bytes, cudaMemcpyHostToDevice, ctx->copy_in));
+            SHPLB_CUDA(cudaEventRecord(in_done, ctx->copy_in));
+            SHPLB_CUDA(cudaStreamWaitEvent(st, in_done, 0));
+            shplb_layer_shape cs = *shape;
+            cs.num_q_heads = h1 - h0;
+            cs.num_kv_heads = g1 - g0;
+            cs.kv_head_of_q = sub.data();
+            rc = shplb_sparse_attention_layer(ctx, &cs, base + q_off + h0 * row_bytes,
+                                              base + k_off + g0 * row_bytes, base + v_off + g0 * row_bytes,
+                                              budgets_tokens + h0, base + o_off + h0 * row_bytes, stream);
+            if (rc != SHPLB_OK) {  // message already recorded; drain before returning
+                cudaStreamSynchronize(ctx->copy_in);
+                cudaStreamSynchronize(st);
+                return;
+            }
+            SHPLB_CUDA(cudaEventRecord(comp_done, st));
+            SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_out, comp_done, 0));
+            SHPLB_CUDA(cudaMemcpyAsync(out_host + h0 * row_bytes / 2, base + o_off + h0 * row_bytes,
+                                       (h1 - h0) * row_bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+        }
+        cudaEvent_t out_done = ctx->chunk_events[3];
+        SHPLB_CUDA(cudaEventRecord(out_done, ctx->copy_out));
+        SHPLB_CUDA(cudaStreamWaitEvent(st, out_done, 0));  // `stream` completes after the last D2H
         SHPLB_CUDA(cudaStreamSynchronize(st));
     });
     return rc != SHPLB_OK ? rc : err;
@@ -541,6 +613,34 @@ int shplb_last_selection(const shplb_ctx* ctx, const int32_t** idx, const int32_
         if (idx) *idx = ctx->idx;
         if (cnt) *cnt = ctx->cnt;
         if (kmax) *kmax = ctx->last_kmax;
+    });
+}
+
+int shplb_last_selection_work(const shplb_ctx* ctx, int64_t* tiles_out, double* flops_out) {
+    return guarded([&] {
+        require(ctx != nullptr && ctx->last_kmax > 0, "no layer call on this context yet");
+        DeviceGuard g(ctx->device);
+        SHPLB_CUDA(cudaDeviceSynchronize());
+        std::vector<int32_t> idx(static_cast<size_t>(ctx->last_rows * ctx->last_kmax));
+        std::vector<int32_t> cnt(static_cast<size_t>(ctx->last_rows));
+        SHPLB_CUDA(cudaMemcpy(idx.data(), ctx->idx, sizeof(int32_t) * idx.size(), cudaMemcpyDeviceToHost));
+        SHPLB_CUDA(cudaMemcpy(cnt.data(), ctx->cnt, sizeof(int32_t) * cnt.size(), cudaMemcpyDeviceToHost));
+        // Same rule as kernel 3's `active`: a half computes a kept block iff it
+        // holds rows and (causal) sees the block's first key.
+        int64_t tiles = 0;
+        const int64_t bk = kern::kBlock, halves = ctx->last_bq / bk;
+        for (int64_t row = 0; row < ctx->last_rows; ++row) {
+            const int64_t row0 = (row % ctx->last_nqb) * ctx->last_bq;
+            for (int64_t j = 0; j < cnt[row]; ++j) {
+                const int64_t key0 = static_cast<int64_t>(idx[row * ctx->last_kmax + j]) * bk;
+                for (int64_t hf = 0; hf < halves; ++hf) {
+                    const int64_t first = row0 + hf * bk;
+                    if (first < ctx->last_n && (!ctx->last_causal || key0 <= first + bk - 1)) ++tiles;
+                }
+            }
+        }
+        if (tiles_out) *tiles_out = tiles;
+        if (flops_out) *flops_out = 4.0 * kern::kHeadDim * double(bk) * double(bk) * double(tiles);
     });
 }
 

@@ -177,6 +177,28 @@ def test_errors_match_reference_messages(cuda_ctx):
                                         v[:, :, :64].contiguous(), [128, 128])
 
 
+@pytest.mark.parametrize("hkv", [1, 3, 8])
+def test_host_buffer_entry_matches_device_call(cuda_ctx, hkv):
+    """shplb_sparse_attention_layer_host (pinned host buffers, KV-head-chunked
+    copy/compute pipeline) returns exactly the device-buffer layer result."""
+    spec = LayerSpec(num_q_heads=2 * hkv, num_kv_heads=hkv, seq_len=1100, seed=30 + hkv)
+    q, k, v = make_layer(spec, "cpu")
+    budgets = np.array([128 * (1 + (h % 5)) for h in range(2 * hkv)])
+    dev = cuda_ctx.sparse_attention_layer(q.cuda(), k.cuda(), v.cuda(), budgets)
+    torch.cuda.synchronize()
+    qh, kh, vh = (t.pin_memory() for t in (q, k, v))
+    host = cuda_ctx.sparse_attention_layer_host(qh, kh, vh, budgets,
+                                                out=torch.empty_like(q).pin_memory())
+    assert torch.equal(host, dev.cpu())
+    if hkv >= 3:  # a head-parallel shard: q heads 1, 2, 5 read kv heads 0, 1, 2 (monotone map)
+        heads, kvs = [1, 2, 5], [0, 1, 2]
+        shard = cuda_ctx.sparse_attention_layer_host(
+            q[heads].contiguous().pin_memory(), k[kvs].contiguous().pin_memory(),
+            v[kvs].contiguous().pin_memory(), budgets[heads], kv_map=[0, 1, 2],
+            out=torch.empty((3,) + tuple(q.shape[1:]), dtype=q.dtype).pin_memory())
+        assert torch.equal(shard, dev.cpu()[heads])
+
+
 def test_deterministic(cuda_ctx):
     """Bit-identical results for identical inputs (test_attention.cpp:315-324)."""
     spec = LayerSpec(num_q_heads=4, num_kv_heads=2, seq_len=2048, seed=8)
