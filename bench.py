@@ -61,7 +61,13 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="target CPU time of the bounded reference sample")
+    p.add_argument("--debug-one-device", action="store_true",
+                   help="debug only: run every rank on cuda:0 with gloo (exercise the N>1 path "
+                        "on a 1-GPU box; timings are not meaningful)")
     return p.parse_args()
+
+
+DEBUG_GLOO = False  # set by --debug-one-device: collectives on CPU tensors over gloo
 
 
 def load_peaks():
@@ -133,14 +139,22 @@ class ClockSampler:
 # distributed plumbing
 # ---------------------------------------------------------------------------
 
-def dist_setup(n_gpus):
+def dist_setup(n_gpus, debug_one_device=False):
     import torch
+    global DEBUG_GLOO
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != n_gpus:
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}: launch N>1 under torchrun")
-    if world > 1:
+    if world > 1 and debug_one_device:
+        import torch.distributed as dist
+        DEBUG_GLOO = True
+        local = 0
+        torch.cuda.set_device(0)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+    elif world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -161,7 +175,7 @@ def allgather_float(x: float, world):
         return [x]
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if DEBUG_GLOO else "cuda")
     out = [torch.zeros_like(t) for _ in range(world)]
     dist.all_gather(out, t)
     return [float(o.item()) for o in out]
@@ -192,7 +206,8 @@ def make_budgets(q, k, args, world, rank):
     if world > 1:
         import torch
         import torch.distributed as dist
-        t = torch.from_numpy(budgets).cuda()
+        t = torch.from_numpy(budgets)
+        t = t if DEBUG_GLOO else t.cuda()
         dist.broadcast(t, 0)
         budgets = t.cpu().numpy()
     return budgets, total, info
@@ -202,13 +217,13 @@ def make_budgets(q, k, args, world, rank):
 # timed loops
 # ---------------------------------------------------------------------------
 
-def time_device(ctx, q, k, v, budgets, kv_map, steps, warmup, world, stream):
+def time_device(ctx, q, k, v, budgets, kv_map, steps, warmup, world, stream, ranges=None):
     import torch
     out = torch.empty_like(q)
     with torch.cuda.stream(stream):
         for _ in range(warmup):
             ctx.sparse_attention_layer(q, k, v, budgets, causal=True, out=out, kv_map=kv_map,
-                                       stream=stream)
+                                       stream=stream, q_block_range=ranges)
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
@@ -218,7 +233,7 @@ def time_device(ctx, q, k, v, budgets, kv_map, steps, warmup, world, stream):
     e0.record(stream)
     for _ in range(steps):
         ctx.sparse_attention_layer(q, k, v, budgets, causal=True, out=out, kv_map=kv_map,
-                                   stream=stream)
+                                   stream=stream, q_block_range=ranges)
     e1.record(stream)
     torch.cuda.synchronize()
     launches = ctx.launches - launches0
@@ -260,15 +275,19 @@ def time_e2e(ctx, q, k, v, budgets, kv_map, steps, warmup, world, stream):
 
 def time_gather(out_local, plan, world):
     """Device time (max over ranks) of reassembling the layer output [Hq, n, d]
-    from every rank's heads: one NCCL all-gather over NVLink + reorder."""
+    from every rank's heads (or head segments): one NCCL all-gather over
+    NVLink + reorder."""
     import torch
-    from paper_2603_10353_b200.head_parallel import gather_heads
-    gather_heads(out_local, plan, world)  # warm-up (communicator, buffers)
+    from paper_2603_10353_b200.head_parallel import gather_heads, gather_segments
+    gather = gather_heads if isinstance(plan, np.ndarray) else gather_segments
+    if DEBUG_GLOO:
+        out_local = out_local.cpu()
+    gather(out_local, plan, world)  # warm-up (communicator, buffers)
     torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    full = gather_heads(out_local, plan, world)
+    full = gather(out_local, plan, world)
     e1.record()
     torch.cuda.synchronize()
     del full
@@ -384,10 +403,10 @@ def main():
     import torch
 
     import paper_2603_10353_b200 as P
-    from paper_2603_10353_b200.head_parallel import rank_shard
+    from paper_2603_10353_b200.head_parallel import rank_segments, rank_shard
     from paper_2603_10353_b200.workload import LayerSpec, make_layer
 
-    world, rank, local = dist_setup(args.gpus)
+    world, rank, local = dist_setup(args.gpus, args.debug_one_device)
     peaks, peaks_src = load_peaks()
     spec = LayerSpec(num_q_heads=args.q_heads, num_kv_heads=args.kv_heads, seq_len=args.seq_len,
                      seed=args.seed)
@@ -401,9 +420,14 @@ def main():
     plans = {"greedy": P.greedy_assign(budgets, world)}
     if world > 1:
         plans["naive"] = P.naive_assign(budgets, world)
+        plans["split"] = P.split_assign(budgets, world, n)
     results = {}
     for name, plan in plans.items():
-        shard = rank_shard(plan, rank, group, budgets)
+        if name == "split":
+            shard = rank_segments(plan, rank, group, budgets)
+            ranges = shard.q_block_range
+        else:
+            shard, ranges = rank_shard(plan, rank, group, budgets), None
         heads, kv_needed, kv_map, bl = shard.heads, shard.kv_heads, shard.kv_map, shard.budgets
         ql = q[heads].contiguous()
         kl, vl = k[kv_needed].contiguous(), v[kv_needed].contiguous()
@@ -411,7 +435,7 @@ def main():
         if sampler:
             sampler.start()
         ms, stages, launches, out_local = time_device(ctx, ql, kl, vl, bl, kv_map, args.steps,
-                                                      args.warmup, world, stream)
+                                                      args.warmup, world, stream, ranges)
         clocks = sampler.stop() if sampler else None
         tiles, flops = ctx.last_selection_work()  # exact tiles of the last timed call
         per_rank = allgather_float(ms, world)
@@ -421,7 +445,8 @@ def main():
                "flops_total": sum(allgather_float(flops, world)),
                "bubble": P.barrier(per_rank).bubble_fraction,
                "k3_bubble": P.barrier(per_rank_k3).bubble_fraction,
-               "load_imbalance": P.imbalance(budgets, plan, world).imbalance}
+               "load_imbalance": (float(plan.loads.max() * world / plan.loads.sum()) if name == "split"
+                                  else P.imbalance(budgets, plan, world).imbalance)}
         if world > 1:
             res["gather_ms"] = time_gather(out_local, plan, world)
         if name == "greedy" and not args.no_e2e:
@@ -493,6 +518,13 @@ def main():
                                  "per_rank_ms": [round(x, 3) for x in nv["per_rank_ms"]],
                                  "load_imbalance": round(nv["load_imbalance"], 4)}
         line["speedup_vs_even_hp"] = round(nv["ms"] / g["ms"], 4)
+        spl = results["split"]
+        line["split_subhead"] = {"ms": round(spl["ms"], 3), "bubble": round(spl["bubble"], 4),
+                                 "per_rank_ms": [round(x, 3) for x in spl["per_rank_ms"]],
+                                 "speedup_vs_even_hp": round(nv["ms"] / spl["ms"], 4),
+                                 "gather_ms": round(spl["gather_ms"], 3),
+                                 "plan": "sub-head balancer (shplb_plan_split), an extension "
+                                         "beyond the reference's whole-head greedy_assign"}
         line["gather_ms"] = round(g["gather_ms"], 3)
         line["value_with_gather"] = round(g["ms"] + g["gather_ms"], 3)
         line["load_imbalance"] = round(g["load_imbalance"], 4)

@@ -102,6 +102,23 @@ int shplb_plan_naive(const int64_t* budgets, int32_t num_heads, int32_t devices,
 int shplb_plan_greedy(const int64_t* budgets, int32_t num_heads, int32_t devices,
                       int32_t* device_of_head);
 
+/* Sub-head balancer (an extension beyond greedy_assign,
+ * partitioner.cpp:164-183). Whole-head placement cannot balance 32 or 28
+ * heads over 8 GPUs under max-min budgets; this plan lets a head's query
+ * blocks be split across devices. Cost of query block qb of head h =
+ * min(ceil(b_h/128), visible key blocks(qb)) x (query halves holding rows),
+ * the 128x128 tiles kernel 3 computes for it. Heads are laid out in LPT order
+ * (cost desc, index asc) and cut McNaughton-style at the running target
+ * ceil(total/D): device d receives a contiguous run of (head, [qb_begin,
+ * qb_end)) segments, at most D-1 heads are split, and every load is within
+ * one query block's cost of total/D. Outputs up to max_segments segments
+ * (seg_device/head/qb_begin/qb_end), *n_segments, and per-device costs
+ * loads_out[devices] in tiles. */
+int shplb_plan_split(const int64_t* budgets, int32_t num_heads, int64_t seq_len, int32_t block_q,
+                     int32_t causal, int32_t devices, int32_t max_segments, int32_t* seg_device,
+                     int32_t* seg_head, int32_t* seg_qb_begin, int32_t* seg_qb_end,
+                     int32_t* n_segments, int64_t* loads_out);
+
 /* imbalance(budgets, assignment) (partitioner.hpp:50, partitioner.cpp:236-266):
  * loads[devices], total, I = max*D/total, argmax device. */
 int shplb_imbalance(const int64_t* budgets, int32_t num_heads, const int32_t* device_of_head,
@@ -163,6 +180,11 @@ typedef struct {
      * head parallelism holds an arbitrary subset of q heads and only the kv
      * heads they need, so its local map is not the contiguous grouping. */
     const int32_t* kv_head_of_q;
+    /* Optional host int32 [num_q_heads][2]: the half-open range of query blocks
+     * [begin, end) of each q head this call computes (output rows outside it
+     * are left untouched). NULL = every query block. Used by the sub-head
+     * balancer (shplb_plan_split), which splits heavy heads across ranks. */
+    const int32_t* q_block_range;
 } shplb_layer_shape;
 
 /* Kernel 1 — block-importance estimator. Mean-pools q/k blocks (fp32,

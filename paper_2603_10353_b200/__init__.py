@@ -7,11 +7,12 @@ from ._native import (CudaError, InvalidArgument, LogicError, NotSupported, Shpl
 from .api import (BLOCK, BLOCK_Q, HEAD_DIM, BudgetAllocation, Context, LoadReport, RecoveryCurve,
                   SimulationResult, barrier, default_budget_grid, greedy_assign, imbalance,
                   layer_work, maxmin_allocate, naive_assign, profile_curves, simulate,
-                  uniform_allocate)
+                  split_assign, uniform_allocate)
 
 __all__ = [
     "BLOCK", "BLOCK_Q", "HEAD_DIM", "BudgetAllocation", "Context", "CudaError", "InvalidArgument",
     "LoadReport", "LogicError", "NotSupported", "RecoveryCurve", "ShplbError", "SimulationResult",
     "barrier", "build", "default_budget_grid", "greedy_assign", "imbalance", "layer_work", "lib",
-    "maxmin_allocate", "naive_assign", "profile_curves", "simulate", "uniform_allocate",
+    "maxmin_allocate", "naive_assign", "profile_curves", "simulate", "split_assign",
+    "uniform_allocate",
 ]

@@ -167,6 +167,34 @@ def imbalance(budgets, device_of_head, devices: int) -> LoadReport:
 
 
 @dataclass
+class SplitPlan:
+    """Sub-head plan (shplb_plan_split): segment i puts query blocks
+    [qb_begin[i], qb_end[i]) of head `head[i]` on `device[i]`."""
+    device: np.ndarray
+    head: np.ndarray
+    qb_begin: np.ndarray
+    qb_end: np.ndarray
+    loads: np.ndarray  # per-device cost in 128x128 tiles
+
+
+def split_assign(budgets, devices: int, seq_len: int, block_q: int = BLOCK_Q,
+                 causal: bool = True) -> SplitPlan:
+    """Sub-head balancer: whole heads in index order, cut at query-block
+    boundaries so every device's tile cost is within half a query block of
+    total/devices (at most devices-1 heads are split)."""
+    b = _i64(budgets)
+    cap = b.size + devices
+    dev, hd, qb0, qb1 = (np.empty(cap, np.int32) for _ in range(4))
+    loads = np.empty(devices, np.int64)
+    ns = C.c_int32()
+    check(lib().shplb_plan_split(_ptr(b), b.size, seq_len, block_q, int(causal), devices, cap,
+                                 _ptr(dev), _ptr(hd), _ptr(qb0), _ptr(qb1), C.byref(ns),
+                                 _ptr(loads)))
+    k = ns.value
+    return SplitPlan(dev[:k].copy(), hd[:k].copy(), qb0[:k].copy(), qb1[:k].copy(), loads)
+
+
+@dataclass
 class SimulationResult:
     """simulator.hpp:20-25."""
     device_latency: np.ndarray
@@ -195,13 +223,17 @@ def barrier(device_latency) -> SimulationResult:
 # ---------------------------------------------------------------------------
 
 def _shape(num_q_heads, num_kv_heads, seq_len, causal, validate=False, kv_map=None,
-           head_dim=HEAD_DIM, block_q=BLOCK_Q) -> LayerShape:
+           head_dim=HEAD_DIM, block_q=BLOCK_Q, q_block_range=None) -> LayerShape:
     sh = LayerShape(num_q_heads, num_kv_heads, seq_len, head_dim, block_q, BLOCK, int(causal), 0,
-                    int(validate), None)
+                    int(validate), None, None)
     if kv_map is not None:
         m = _i32(kv_map)
         sh._kv_map_keepalive = m  # the C struct only borrows the pointer
         sh.kv_head_of_q = m.ctypes.data
+    if q_block_range is not None:
+        r = _i32(np.asarray(q_block_range).reshape(-1))
+        sh._range_keepalive = r
+        sh.q_block_range = r.ctypes.data
     return sh
 
 
@@ -308,7 +340,7 @@ class Context:
 
     # -- the layer: kernels 1+2 fused, then 3 -----------------------------
     def sparse_attention_layer(self, q, k, v, budgets_tokens, causal=True, stream=None, out=None,
-                               validate=False, kv_map=None, block_q=BLOCK_Q):
+                               validate=False, kv_map=None, block_q=BLOCK_Q, q_block_range=None):
         """sparse_attention for every head with its own token budget."""
         import torch
         hq, n, d = q.shape
@@ -318,7 +350,7 @@ class Context:
         if b.size != hq:
             from ._native import InvalidArgument
             raise InvalidArgument(f"need one budget per query head ({hq}), got {b.size}")
-        sh = _shape(hq, k.shape[0], n, causal, validate, kv_map, d, block_q)
+        sh = _shape(hq, k.shape[0], n, causal, validate, kv_map, d, block_q, q_block_range)
         self._last_block_q = block_q
         check(lib().shplb_sparse_attention_layer(
             self._h, C.byref(sh), _dev_ptr(q, "q", torch.bfloat16), _dev_ptr(k, "k", torch.bfloat16),
@@ -327,7 +359,7 @@ class Context:
         return out
 
     def sparse_attention_layer_host(self, q, k, v, budgets_tokens, causal=True, out=None,
-                                    stream=None, kv_map=None, block_q=BLOCK_Q):
+                                    stream=None, kv_map=None, block_q=BLOCK_Q, q_block_range=None):
         """The layer call on HOST bf16 tensors (pinned for async DMA): copy in,
         kernels 1-3, copy out, synchronise (shplb_sparse_attention_layer_host)."""
         import torch
@@ -339,7 +371,7 @@ class Context:
         if out is None:
             out = torch.empty_like(q)
         b = _i64(budgets_tokens)
-        sh = _shape(hq, k.shape[0], n, causal, False, kv_map, d, block_q)
+        sh = _shape(hq, k.shape[0], n, causal, False, kv_map, d, block_q, q_block_range)
         self._last_block_q = block_q
         check(lib().shplb_sparse_attention_layer_host(
             self._h, C.byref(sh), C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()),

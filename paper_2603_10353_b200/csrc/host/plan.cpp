@@ -71,6 +71,68 @@ extern "C" int shplb_plan_greedy(const int64_t* budgets, int32_t num_heads, int3
     });
 }
 
+extern "C" int shplb_plan_split(const int64_t* budgets, int32_t num_heads, int64_t seq_len,
+                                int32_t block_q, int32_t causal, int32_t devices,
+                                int32_t max_segments, int32_t* seg_device, int32_t* seg_head,
+                                int32_t* seg_qb_begin, int32_t* seg_qb_end, int32_t* n_segments,
+                                int64_t* loads_out) {
+    return guarded([&] {
+        check_budgets(budgets, num_heads);
+        if (devices < 1) throw InvalidArgument("need at least one device");
+        if (seq_len < 1) throw InvalidArgument("K must hold at least one key token");
+        if (block_q != 128 && block_q != 256) throw InvalidArgument("block_q must be 128 or 256");
+        require(seg_device && seg_head && seg_qb_begin && seg_qb_end && n_segments && loads_out,
+                "null output pointer");
+        constexpr int64_t bk = 128;
+        const int64_t nqb = (seq_len + block_q - 1) / block_q, nkb = (seq_len + bk - 1) / bk;
+        // Tiles kernel 3 computes for (head h, query block qb) before selection
+        // (include/shplb.h, shplb_layer_work).
+        auto cost = [&](int32_t h, int64_t qb) -> int64_t {
+            int64_t vis = nkb;
+            if (causal) vis = std::min(nkb, (std::min((qb + 1) * block_q, seq_len) - 1) / bk + 1);
+            const int64_t k = std::min(nkb, (budgets[h] + bk - 1) / bk);
+            int64_t halves = 0;
+            for (int64_t hf = 0; hf < block_q / bk; ++hf) halves += qb * block_q + hf * bk < seq_len;
+            return std::min(k, vis) * halves;
+        };
+        int64_t total = 0;
+        for (int32_t h = 0; h < num_heads; ++h)
+            for (int64_t qb = 0; qb < nqb; ++qb) total += cost(h, qb);
+        // Walk heads in index order (GQA groups stay contiguous, so ranks need
+        // few kv heads); device d takes the units whose cost midpoint falls in
+        // [d*total/D, (d+1)*total/D) of the running prefix, so every load is
+        // within half a query block's cost of total/D.
+        std::fill(loads_out, loads_out + devices, 0);
+        int32_t nseg = 0, d = 0;
+        int64_t prefix = 0;
+        auto emit = [&](int32_t h, int64_t b, int64_t e) {
+            if (e <= b) return;
+            if (nseg >= max_segments) throw InvalidArgument("max_segments too small for the split plan");
+            seg_device[nseg] = d;
+            seg_head[nseg] = h;
+            seg_qb_begin[nseg] = static_cast<int32_t>(b);
+            seg_qb_end[nseg] = static_cast<int32_t>(e);
+            ++nseg;
+        };
+        for (int32_t h = 0; h < num_heads; ++h) {
+            int64_t begin = 0;
+            for (int64_t qb = 0; qb < nqb; ++qb) {
+                const int64_t c = cost(h, qb);
+                // Midpoint of this unit, in units of total/D (scaled by 2*devices to stay integral).
+                while (d < devices - 1 && (2 * prefix + c) * devices >= 2 * total * (d + 1)) {
+                    emit(h, begin, qb);
+                    begin = qb;
+                    ++d;
+                }
+                prefix += c;
+                loads_out[d] += c;
+            }
+            emit(h, begin, nqb);
+        }
+        *n_segments = nseg;
+    });
+}
+
 extern "C" int shplb_imbalance(const int64_t* budgets, int32_t num_heads,
                                const int32_t* device_of_head, int32_t devices, int64_t* loads_out,
                                int64_t* total_out, double* imbalance_out, int32_t* argmax_out) {

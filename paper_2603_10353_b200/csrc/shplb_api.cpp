@@ -276,24 +276,33 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
 // Kernel-3 work list: every (head, query block) tile, heaviest first (LPT), so
 // the hardware block scheduler hands out long tiles before short ones.
 void build_tiles(shplb_ctx* ctx, const shplb_layer_shape* s, const std::vector<int32_t>& kblocks) {
+    const int64_t nqb = cdiv(s->seq_len, s->block_q);
     std::vector<int64_t> key = {s->seq_len, s->causal, s->block_q, s->num_q_heads};
     key.insert(key.end(), kblocks.begin(), kblocks.end());
+    if (s->q_block_range) key.insert(key.end(), s->q_block_range, s->q_block_range + 2 * s->num_q_heads);
     auto it = ctx->work_lists.find(key);
     if (it != ctx->work_lists.end()) {
         ctx->current = &it->second;
         return;
     }
-    const int64_t nqb = cdiv(s->seq_len, s->block_q);
     std::vector<int32_t> tiles;
     std::vector<int32_t> work;
     tiles.reserve(static_cast<size_t>(s->num_q_heads * nqb));
-    for (int h = 0; h < s->num_q_heads; ++h)
-        for (int64_t qb = 0; qb < nqb; ++qb) {
+    for (int h = 0; h < s->num_q_heads; ++h) {
+        const int64_t qb_lo = s->q_block_range ? s->q_block_range[2 * h] : 0;
+        const int64_t qb_hi = s->q_block_range ? s->q_block_range[2 * h + 1] : nqb;
+        if (qb_lo < 0 || qb_hi > nqb || qb_lo > qb_hi) {
+            throw InvalidArgument("head " + std::to_string(h) + ": query block range [" +
+                                  std::to_string(qb_lo) + ", " + std::to_string(qb_hi) +
+                                  ") out of [0, " + std::to_string(nqb) + "]");
+        }
+        for (int64_t qb = qb_lo; qb < qb_hi; ++qb) {
             tiles.push_back((h << 20) | static_cast<int32_t>(qb));
             work.push_back(static_cast<int32_t>(
                 std::min<int64_t>(kblocks[h], visible_blocks(qb, s->seq_len, s->block_q, s->causal != 0)) *
                 live_halves(qb, s->seq_len, s->block_q)));
         }
+    }
     std::vector<size_t> order(tiles.size());
     std::iota(order.begin(), order.end(), size_t{0});
     std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return work[a] > work[b]; });
@@ -329,7 +338,7 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     p.causal = s->causal;
     fill_kv_map(s, p.heads);
     p.scale_log2 = static_cast<float>((1.0 / std::sqrt(static_cast<double>(s->head_dim))) * 1.4426950408889634);
-    kern::launch_fa(p, ctx->current->num_tiles, st);
+    if (ctx->current->num_tiles > 0) kern::launch_fa(p, ctx->current->num_tiles, st);
     check_launch(ctx);
 }
 
@@ -585,6 +594,7 @@ int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* s
             cs.num_q_heads = h1 - h0;
             cs.num_kv_heads = g1 - g0;
             cs.kv_head_of_q = sub.data();
+            if (shape->q_block_range) cs.q_block_range = shape->q_block_range + 2 * h0;
             rc = shplb_sparse_attention_layer(ctx, &cs, base + q_off + h0 * row_bytes,
                                               base + k_off + g0 * row_bytes, base + v_off + g0 * row_bytes,
                                               budgets_tokens + h0, base + o_off + h0 * row_bytes, stream);

@@ -12,7 +12,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import paper_2603_10353_b200 as P
-from paper_2603_10353_b200.head_parallel import gather_heads, head_counts, rank_shard
+from paper_2603_10353_b200.head_parallel import (gather_heads, gather_segments, head_counts,
+                                                  rank_segments, rank_shard)
 
 
 def _free_port():
@@ -55,6 +56,19 @@ def _worker(rank, world, port, budgets, results):
             assert res.barrier_latency == float(rep.loads.max())
             if rank == 0:
                 results[name] = (res.barrier_latency, res.bubble_fraction, head_counts(plan, world))
+        # sub-head plan: rows of a split head come from different ranks
+        n, bq = 1000, 256
+        sp = P.split_assign(b, world, n, block_q=bq)
+        seg = rank_segments(sp, rank, group, b)
+        local = torch.full((len(seg.heads), n, 2), -1.0)
+        for i, h in enumerate(seg.heads):
+            r0, r1 = seg.q_block_range[i] * bq
+            local[i, r0:min(r1, n)] = h * 10000 + torch.arange(r0, min(r1, n))[:, None].float()
+        full = gather_segments(local, sp, world, block_q=bq)
+        want = (torch.arange(hq)[:, None] * 10000 + torch.arange(n)[None, :]).float()[..., None]
+        assert torch.equal(full, want.expand(hq, n, 2))
+        if rank == 0:
+            results["split_heads"] = len(sp.head) - len(set(sp.head.tolist()))
     finally:
         dist.destroy_process_group()
 
@@ -70,3 +84,4 @@ def test_head_parallel_world2_gloo():
     assert n_counts == [6, 6]            # even HP splits by head count
     assert g_T <= n_T and g_bub <= n_bub  # the balancer never does worse here
     assert g_T == max(P.imbalance(budgets, P.greedy_assign(budgets, 2), 2).loads)
+    assert results["split_heads"] <= 1  # at most D-1 heads are split

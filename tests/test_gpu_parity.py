@@ -252,3 +252,28 @@ def test_c3_size_sampled_rows(cuda_ctx):
             ref = O.sparse_rows(qbits, kbits, vbits, rows, sel.tolist())
             mx, rel = _errors(out[h, rows], ref)
             assert mx <= MAX_ABS and rel <= MEAN_REL, (h, qbk, mx, rel)
+
+
+@pytest.mark.parametrize("bq", [256, 128])
+def test_split_plan_shards_reassemble_the_layer(cuda_ctx, bq):
+    """Sub-head plan: every rank computes only its heads' query-block ranges;
+    stitching the ranks' rows back together gives exactly the whole-layer call."""
+    from paper_2603_10353_b200.head_parallel import rank_segments
+    spec = LayerSpec(num_q_heads=6, num_kv_heads=2, seq_len=2000, seed=41)
+    q, k, v = (t.cuda() for t in make_layer(spec, "cpu"))
+    budgets = np.array([128, 1024, 384, 2000, 256, 768], np.int64)
+    full = cuda_ctx.sparse_attention_layer(q, k, v, budgets, block_q=bq)
+    sp = P.split_assign(budgets, 4, 2000, block_q=bq)
+    got = torch.zeros_like(full)
+    for r in range(4):
+        seg = rank_segments(sp, r, 3, budgets)
+        if not seg.heads:
+            continue
+        part = cuda_ctx.sparse_attention_layer(
+            q[seg.heads].contiguous(), k[seg.kv_heads].contiguous(), v[seg.kv_heads].contiguous(),
+            seg.budgets, kv_map=seg.kv_map, q_block_range=seg.q_block_range, block_q=bq)
+        for i, h in enumerate(seg.heads):
+            r0, r1 = seg.q_block_range[i] * bq
+            got[h, r0:r1] = part[i, r0:r1]
+    torch.cuda.synchronize()
+    assert torch.equal(got, full)

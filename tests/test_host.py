@@ -228,3 +228,43 @@ def test_layer_work_counts_selected_tiles():
     assert tiles == 2 * 2 + 2 * 2
     tiles, _ = P.layer_work(1, 1, 300, [300], causal=True, block_q=256)  # 2nd block: 1 live half
     assert tiles == 2 * 2 + 3 * 1
+
+
+# ------------------------------------------------------- sub-head plan ----
+
+@pytest.mark.parametrize("seed", range(12))
+def test_split_plan_covers_every_block_once_and_balances(seed):
+    rng = np.random.default_rng(seed)
+    hq = int(rng.integers(1, 40))
+    n = int(rng.choice([1000, 8192, 65536, 131072]))
+    bq = int(rng.choice([128, 256]))
+    D = int(rng.integers(1, 9))
+    budgets = (rng.integers(1, max(2, n // 128 + 1), hq) * 128).clip(128, n)
+    sp = P.split_assign(budgets, D, n, block_q=bq)
+    nqb = (n + bq - 1) // bq
+    covered = np.zeros((hq, nqb), np.int32)
+    for d, h, b, e in zip(sp.device, sp.head, sp.qb_begin, sp.qb_end):
+        assert 0 <= d < D and b < e
+        covered[h, b:e] += 1
+    assert (covered == 1).all()
+    # contiguous wrap-around: device index never decreases along the head order
+    assert (np.diff(sp.device) >= 0).all()
+    split_heads = len(sp.head) - len(set(sp.head.tolist()))
+    assert split_heads <= D - 1
+    # every load within one query block's cost of total/D
+    tiles, _ = P.layer_work(hq, 1, n, budgets, block_q=bq, kv_map=[0] * hq)
+    assert sp.loads.sum() == tiles
+    kb = np.minimum((budgets + 127) // 128, (n + 127) // 128)
+    unit_max = int(kb.max()) * (bq // 128)
+    assert np.abs(sp.loads - tiles / D).max() <= unit_max
+
+
+def test_split_plan_beats_whole_head_plans():
+    # many floor heads + a few heavy ones over 8 devices
+    budgets = np.array([128] * 18 + [1344, 3840, 4096, 4352, 4544, 4736, 5760, 6592, 6592,
+                                     6656, 7104, 7232, 8000, 8192], np.int64) * 16
+    sp = P.split_assign(budgets, 8, 131072)
+    g = P.greedy_assign(budgets, 8)
+    tiles_per_head = [P.layer_work(1, 1, 131072, [b], kv_map=[0])[0] for b in budgets]
+    g_loads = np.bincount(g, weights=tiles_per_head, minlength=8)
+    assert sp.loads.max() / sp.loads.mean() < 1.01 < g_loads.max() / g_loads.mean()
