@@ -37,6 +37,7 @@
 // TMEM (512 columns): S/P half 0 [0,128), S/P half 1 [128,256),
 //                     O half 0 [256,384), O half 1 [384,512).
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -63,23 +64,34 @@ constexpr uint32_t kTmemCols = 512;
 __host__ __device__ constexpr uint32_t col_s(int h) { return static_cast<uint32_t>(h) * 128u; }
 __host__ __device__ constexpr uint32_t col_o(int h) { return 256u + static_cast<uint32_t>(h) * 128u; }
 constexpr float kRescaleThreshold = 8.0f;  // log2 domain: rescale when max grows by > 2^8
-#ifndef SHPLB_EMU_PERIOD
-#define SHPLB_EMU_PERIOD 0
+#ifndef SHPLB_EMU_PAIRS
+#define SHPLB_EMU_PAIRS 0
 #endif
-// Every kEmuPeriod-th exp pair on the FMA pipe (0 = all on MUFU). Measured
-// slower on B200 with one query tile per K/V load (the kernel was not
-// MUFU-bound); kept as a tuning knob.
-constexpr int kEmuPeriod = SHPLB_EMU_PERIOD;
+// Exponential pairs (of every 16) computed by the FMA-pipe polynomial instead
+// of MUFU ex2, in blocks without masked keys (0 = all on MUFU).
+constexpr int kEmuPairs = SHPLB_EMU_PAIRS;
+static_assert(kEmuPairs >= 0 && kEmuPairs <= 16, "SHPLB_EMU_PAIRS out of range");
 
-constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, 0, 0);  // A=Q K-major, B=K K-major
+constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, 0, 0);   // A=Q K-major, B=K K-major
+constexpr uint32_t kIdescQK64 = idesc_bf16_f32(128, 64, 0, 0);   // same, 64 keys of K
+#ifndef SHPLB_SPLIT_S
+#define SHPLB_SPLIT_S 0
+#endif
+constexpr bool kSplitS = SHPLB_SPLIT_S != 0;  // S as two N=64 halves with separate commits
+#ifndef SHPLB_P_CHUNKS
+#define SHPLB_P_CHUNKS 1
+#endif
+// P handed to the MMA warp in this many pieces (1, 2 or 4 quarters of keys).
+constexpr int kPChunks = SHPLB_P_CHUNKS;
+static_assert(kPChunks == 1 || kPChunks == 2 || kPChunks == 4, "SHPLB_P_CHUNKS must be 1, 2 or 4");
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 128, 0, 1);  // A=P (TMEM), B=V MN-major
 
 struct __align__(8) Barriers {
     uint64_t q_full;
     uint64_t k_full[2], k_empty[2];
     uint64_t v_full[2], v_empty[2];
-    uint64_t s_full[2];   // per half: S of its next block is in TMEM
-    uint64_t p_full[2];   // per half: P written (and O rescaled) -> PV may run
+    uint64_t s_full[2][2];  // per half, per 64-key column half: S of its next block is in TMEM
+    uint64_t p_full[2][4];  // per half, per 32-key quarter: P written (and O rescaled) -> PV may run
     uint64_t pv_done[2];  // per half: its last issued PV has completed
     uint32_t tmem_base;
 };
@@ -104,7 +116,19 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t tile_addr, int kk) {
     return umma_desc_sw128(tile_addr + kk * 2048, kChunkBytes, 1024);
 }
 
+#ifdef SHPLB_TRACE  // dev-only: per-block clock64 timeline of one CTA, printed at exit
+constexpr int kTraceBlocks = 48;
+#define TRACE(j, e, cond) \
+    do { if ((cond) && (j) >= 0 && (j) < kTraceBlocks) trace[(j)][(e)] = clock64(); } while (0)
+#else
+#define TRACE(j, e, cond) do { } while (0)
+#endif
+
 __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_constant__ FaParams p) {
+#ifdef SHPLB_TRACE
+    __shared__ long long trace[kTraceBlocks][16];
+    for (int i = threadIdx.x; i < kTraceBlocks * 16; i += kThreads) trace[i / 16][i % 16] = 0;
+#endif
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Barriers* bar = reinterpret_cast<Barriers*>(smem + kSmemBar);
@@ -142,8 +166,8 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
             mbar_init(&bar->k_empty[i], 1);
             mbar_init(&bar->v_full[i], 1);
             mbar_init(&bar->v_empty[i], 1);
-            mbar_init(&bar->s_full[i], 1);
-            mbar_init(&bar->p_full[i], 128);
+            for (int c = 0; c < 2; ++c) mbar_init(&bar->s_full[i][c], 1);
+            for (int c = 0; c < 4; ++c) mbar_init(&bar->p_full[i][c], 128);
             mbar_init(&bar->pv_done[i], 1);
         }
         fence_mbar_init();
@@ -174,9 +198,11 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
                 mbar_wait(&bar->k_empty[st], ph ^ 1);
                 tma_load_tile_warp(smem + kSmemK + st * kTileBytes, &p.tm_k, &bar->k_full[st],
                                    kTileBytes, key0, g);
+                TRACE(j, 11, (threadIdx.x & 31) == 0);
                 mbar_wait(&bar->v_empty[st], ph ^ 1);
                 tma_load_tile_warp(smem + kSmemV + st * kTileBytes, &p.tm_v, &bar->v_full[st],
                                    kTileBytes, key0, g);
+                TRACE(j, 12, (threadIdx.x & 31) == 0);
             }
         }
       } else if (warp == 9) {
@@ -188,18 +214,50 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
                                        umma_desc_sw128(sV + kTileBytes, kChunkBytes, 1024)};
             mbar_wait(&bar->q_full, 0);
             int done[2] = {0, 0};  // blocks each half has issued PV for
-            auto issue_s = [&](int hf, int j) {  // S_hf = Q_hf K_j^T
+            // S_hf = Q_hf K_j^T as two N = 64 products (keys 0-63, 64-127 of
+            // the block; K rows 64.. start 8 KB into each d chunk), each with
+            // its own commit, so the softmax loads and reduces the first 64
+            // columns while the tensor pipe computes the second.
+            auto issue_s = [&](int hf, int j) {
                 mbar_wait(&bar->k_full[j & 1], (j >> 1) & 1);
+                TRACE(j - 1, 9, hf == 0 && (threadIdx.x & 31) == 0);
                 tc_fence_after();
-                mma_tile_ss_kmajor(tmem + col_s(hf), qdesc[hf], kdesc[j & 1], kIdescQK, 0u);
-                mma_commit_warp(&bar->s_full[hf]);
+                if (kSplitS) {
+                    for (int c = 0; c < 2; ++c) {
+                        mma_tile_ss_kmajor(tmem + col_s(hf) + 64u * c, qdesc[hf], kdesc[j & 1] + 512u * c,
+                                           kIdescQK64, 0u);
+                        mma_commit_warp(&bar->s_full[hf][c]);
+                    }
+                } else {
+                    mma_tile_ss_kmajor(tmem + col_s(hf), qdesc[hf], kdesc[j & 1], kIdescQK, 0u);
+                    TRACE(j - 1, hf == 0 ? 10 : 14, (threadIdx.x & 31) == 0);
+                    mma_commit_warp(&bar->s_full[hf][0]);
+                    mma_commit_warp(&bar->s_full[hf][1]);
+                }
             };
-            auto issue_pv = [&](int hf, int j) {  // O_hf += P_hf V_j
+            // O_hf += P_hf V_j, in kPChunks pieces each issued as soon as the
+            // softmax has stored that piece of P.
+            auto issue_pv = [&](int hf, int j) {
                 mbar_wait(&bar->v_full[j & 1], (j >> 1) & 1);
-                mbar_wait(&bar->p_full[hf], done[hf] & 1);
-                tc_fence_after();
-                mma_tile_ts_mnmajor(tmem + col_o(hf), tmem + col_s(hf), vdesc[j & 1], kIdescPV,
-                                    done[hf] > 0 ? 1u : 0u);
+                TRACE(j, 6, hf == 0 && (threadIdx.x & 31) == 0);
+                if (kPChunks == 1) {
+                    mbar_wait(&bar->p_full[hf][0], done[hf] & 1);
+                    TRACE(j, 7, hf == 0 && (threadIdx.x & 31) == 0);
+                    tc_fence_after();
+                    mma_tile_ts_mnmajor(tmem + col_o(hf), tmem + col_s(hf), vdesc[j & 1], kIdescPV,
+                                        done[hf] > 0 ? 1u : 0u);
+                } else {
+                    for (int c = 0; c < 4; ++c) {
+                        if (c % (4 / kPChunks) == 0) {
+                            mbar_wait(&bar->p_full[hf][c / (4 / kPChunks)], done[hf] & 1);
+                            if (c == 0) TRACE(j, 7, hf == 0 && (threadIdx.x & 31) == 0);
+                            tc_fence_after();
+                        }
+                        mma_pair_ts_mnmajor(tmem + col_o(hf), tmem + col_s(hf) + 16u * c, vdesc[j & 1] + 256u * c,
+                                            kIdescPV, (done[hf] > 0 || c > 0) ? 1u : 0u);
+                    }
+                }
+                TRACE(j, hf == 0 ? 8 : 13, (threadIdx.x & 31) == 0);
                 mma_commit_warp(&bar->pv_done[hf]);
                 ++done[hf];
             };
@@ -214,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
                 }
                 mma_commit_warp(&bar->v_empty[j & 1]);
                 if (next) mma_commit_warp(&bar->k_empty[(j + 1) & 1]);
+                TRACE(j, 15, (threadIdx.x & 31) == 0);
             }
         }
       }
@@ -234,40 +293,38 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
         for (int j = 0; j < nsel; ++j) {
             if (!active(hf, j)) continue;
             const int64_t key0 = static_cast<int64_t>(sel[j]) * kBlock;
-            mbar_wait(&bar->s_full[hf], it & 1);
-            tc_fence_after();
+            // S arrives in two 64-column halves (separate commits): mask and
+            // reduce the first while the tensor pipe computes the second. Row
+            // max with 8 independent chains (ptxas fuses them into FMNMX3);
+            // keys past the query (causal) or past the sequence end are -inf.
+            uint32_t sv[kBlock];
+            float* s = reinterpret_cast<float*>(sv);
+            const bool need_mask = key0 + kBlock - 1 > lim;
+            float mx8[8];
+#pragma unroll
+            for (int hc = 0; hc < 2; ++hc) {
+                uint32_t(&ca)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[hc * 64]);
+                uint32_t(&cb)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[hc * 64 + 32]);
+                mbar_wait(&bar->s_full[hf][hc], it & 1);
+                tc_fence_after();
+                if (hc == 0) TRACE(j, 3 * hf + 0, r == 0);
+                tmem_ld32(s_addr + hc * 64, ca);
+                tmem_ld32(s_addr + hc * 64 + 32, cb);
+                tmem_wait_ld();
+                if (need_mask) {
+#pragma unroll
+                    for (int c = hc * 64; c < hc * 64 + 64; ++c)
+                        if (key0 + c > lim) s[c] = -INFINITY;
+                }
+#pragma unroll
+                for (int c = hc * 64; c < hc * 64 + 64; ++c) mx8[c & 7] = c < 8 ? s[c] : fmaxf(mx8[c & 7], s[c]);
+            }
 #ifdef SHPLB_DIAG_SKIP_SOFTMAX  // dev-only diagnostic: MMA/TMA pipeline alone
             tc_fence_before();
-            mbar_arrive(&bar->p_full[hf]);
+            for (int c = 0; c < kPChunks; ++c) mbar_arrive(&bar->p_full[hf][c]);
             ++it;
             continue;
 #endif
-            uint32_t sv[kBlock];
-            {
-                uint32_t(&c0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[0]);
-                uint32_t(&c1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[32]);
-                uint32_t(&c2)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[64]);
-                uint32_t(&c3)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[96]);
-                tmem_ld32(s_addr + 0, c0);
-                tmem_ld32(s_addr + 32, c1);
-                tmem_ld32(s_addr + 64, c2);
-                tmem_ld32(s_addr + 96, c3);
-                tmem_wait_ld();
-            }
-            float* s = reinterpret_cast<float*>(sv);
-            // Mask keys past the query (causal) or past the sequence end; row
-            // max with 8 independent chains (ptxas fuses them into FMNMX3).
-            const bool need_mask = key0 + kBlock - 1 > lim;
-            if (need_mask) {
-#pragma unroll
-                for (int c = 0; c < kBlock; ++c)
-                    if (key0 + c > lim) s[c] = -INFINITY;
-            }
-            float mx8[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) mx8[e] = s[e];
-#pragma unroll
-            for (int c = 8; c < kBlock; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
             const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                      fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
             const float mx = mraw * sl2;  // scale > 0 commutes with max
@@ -291,43 +348,46 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
                 }
             }
             const float msub = (m == -INFINITY) ? 0.0f : m;
-            float sum4[4] = {0.f, 0.f, 0.f, 0.f};
-            // Warp-uniform: both paths issue warp-collective tcgen05.st.
-            if (kEmuPeriod > 0 && !__any_sync(0xffffffffu, need_mask)) {
-                // MUFU ex2 and the FMA-pipe polynomial share the exponentials.
+            // x = s*scale_log2 - m and the row sum run on packed pairs
+            // (FFMA2/FADD2). With kPChunks > 1, P is handed to the MMA warp in
+            // pieces (p_full[hf][c]) so P.V can start while later keys are
+            // still being exponentiated; a piece's tcgen05.st is waited for
+            // only after the next quarter's exponentials are issued.
+            // Blocks with no masked lane in the warp may send kEmuPairs of
+            // every 16 pairs to the FMA-pipe polynomial instead of MUFU.
+            const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-msub, -msub);
+            float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            const bool emu_blk = kEmuPairs > 0 && !__any_sync(0xffffffffu, need_mask);
+            TRACE(j, 3 * hf + 1, r == 0);
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {  // four 32-key quarters -> 16 packed columns each
-                    uint32_t pk[16];
+            for (int c = 0; c < 4; ++c) {  // four 32-key quarters -> 16 packed columns each
+                uint32_t pk[16];
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const float x0 = fmaf(s[c * 32 + 2 * e], sl2, -msub);
-                        const float x1 = fmaf(s[c * 32 + 2 * e + 1], sl2, -msub);
-                        const bool emu = kEmuPeriod > 0 && (e % (kEmuPeriod > 0 ? kEmuPeriod : 1)) == kEmuPeriod - 1;
-                        const float p0 = emu ? ex2_poly(x0) : ex2(x0);
-                        const float p1 = emu ? ex2_poly(x1) : ex2(x1);
-                        sum4[e & 3] += p0 + p1;
-                        pk[e] = pack_bf16x2(p0, p1);
+                for (int e = 0; e < 16; ++e) {
+                    const float2 x = ffma2(make_float2(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]), sc2, nm2);
+                    float2 pe;
+                    if (emu_blk && ((e * kEmuPairs) & 15) < kEmuPairs) {
+                        pe = ex2_poly2(x);
+                    } else {
+                        pe.x = ex2(x.x);
+                        pe.y = ex2(x.y);
                     }
-                    tmem_st16(s_addr + c * 16, pk);
+                    sum2[e & 1] = fadd2(sum2[e & 1], pe);
+                    pk[e] = pack_bf16x2(pe.x, pe.y);
                 }
-            } else {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const float p0 = ex2(fmaf(s[c * 32 + 2 * e], sl2, -msub));
-                        const float p1 = ex2(fmaf(s[c * 32 + 2 * e + 1], sl2, -msub));
-                        sum4[e & 3] += p0 + p1;
-                        pk[e] = pack_bf16x2(p0, p1);
-                    }
-                    tmem_st16(s_addr + c * 16, pk);
+                if (kPChunks > 1 && c > 0 && c % (4 / kPChunks) == 0) {
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive(&bar->p_full[hf][c / (4 / kPChunks) - 1]);
                 }
+                tmem_st16(s_addr + c * 16, pk);
             }
-            l = l * alpha + ((sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
+            const float2 sum = fadd2(sum2[0], sum2[1]);
+            l = l * alpha + (sum.x + sum.y);
             tmem_wait_st();
+            TRACE(j, 3 * hf + 2, r == 0);
             tc_fence_before();
-            mbar_arrive(&bar->p_full[hf]);
+            mbar_arrive(&bar->p_full[hf][kPChunks - 1]);
             ++it;
         }
 
@@ -368,6 +428,18 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem);
     }
+#ifdef SHPLB_TRACE
+    if (blockIdx.x == SHPLB_TRACE && threadIdx.x == 0) {
+        const long long t0 = trace[0][0];
+        printf("TRACE cta %d nsel %d\n", blockIdx.x, nsel);
+        for (int j = 0; j < kTraceBlocks && j < nsel; ++j)
+            printf("TRACE j %d v %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", j,
+                   trace[j][0] - t0, trace[j][1] - t0, trace[j][2] - t0, trace[j][3] - t0,
+                   trace[j][4] - t0, trace[j][5] - t0, trace[j][6] - t0, trace[j][7] - t0,
+                   trace[j][8] - t0, trace[j][9] - t0, trace[j][10] - t0, trace[j][11] - t0,
+                   trace[j][12] - t0, trace[j][13] - t0, trace[j][14] - t0, trace[j][15] - t0);
+    }
+#endif
 }
 
 }  // namespace

@@ -152,6 +152,15 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         : "memory");
 }
 
+// Named barriers (ids 1..15; 0 is __syncthreads). `count` threads take part:
+// the arriving side does not wait, the syncing side waits for all of them.
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // Warp index the compiler can prove warp-uniform (values derived from it go to
 // uniform registers, branches on it need no divergence handling).
 __device__ __forceinline__ int warp_index_uniform() {
@@ -212,6 +221,23 @@ __device__ __forceinline__ void mma_tile_ts_mnmajor(uint32_t d_tmem, uint32_t a_
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
         "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Two k-steps (32 keys) of the TS product above: A columns a_tmem, a_tmem+8;
+// B k-steps b_desc, b_desc+128.
+__device__ __forceinline__ void mma_pair_ts_mnmajor(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                    uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b64 b;\n\t.reg .b32 a;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.u32 t, 0, 0;\n\t"
+        "mov.b32 a, %1;\n\tmov.b64 b, %2;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, p;\n\t"
         "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
@@ -379,6 +405,56 @@ __device__ __forceinline__ float ex2_poly(float x) {
     p = __fmaf_rn(p, f, 0.69318938255f);
     p = __fmaf_rn(p, f, 0.99993973970f);
     return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2: two lanes' worth of fp32 work per
+// issue slot). The pair lives in two 32-bit registers that ptxas allocates as
+// one 64-bit pair, so the movs below vanish.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return d;
+}
+
+// ex2_poly on a pair with packed FFMA2/FADD2: 2 clamps, 3 packed adds, 3
+// packed FMAs and 2 exponent merges for two exponentials (vs 2 MUFU issues,
+// each of which holds the SMSP's 4-lane MUFU for 8 cycles).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -125.0f);
+    x.y = fmaxf(x.y, -125.0f);
+    const float2 magic = make_float2(12582912.0f, 12582912.0f);
+    const float2 t = fadd2(x, magic);
+    const float2 j = fsub2(t, magic);
+    const float2 f = fsub2(x, j);
+    float2 p = ffma2(make_float2(0.05546969920f, 0.05546969920f), f,
+                     make_float2(0.24239382148f, 0.24239382148f));
+    p = ffma2(p, f, make_float2(0.69318938255f, 0.69318938255f));
+    p = ffma2(p, f, make_float2(0.99993973970f, 0.99993973970f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
