@@ -195,10 +195,17 @@ def make_budgets(q, k, args, world, rank):
     if rank == 0:
         t0 = time.time()
         rows = q[:, n - args.calib_rows:, :]
-        curves = P.profile_curves(bf16_bits(rows), bf16_bits(k), P.default_budget_grid(n, 128))
+        grid = P.default_budget_grid(n, 128)
+        if getattr(q, "is_cuda", False):  # GPU profiler (shplb_profile_curves)
+            pctx = P.Context(q.device.index or 0)
+            curves = pctx.profile_curves(rows.contiguous(), k, grid)
+            pctx.close()
+        else:
+            curves = P.profile_curves(bf16_bits(rows), bf16_bits(k), grid)
         alloc = P.maxmin_allocate(curves, total, quantum=128, floor=128)
         budgets = alloc.budgets.astype(np.int64)
-        info = {"calibration_rows": args.calib_rows, "profile_s": round(time.time() - t0, 2),
+        info = {"calibration_rows": args.calib_rows, "profile_s": round(time.time() - t0, 3),
+                "profiler": "gpu" if getattr(q, "is_cuda", False) else "host",
                 "transfers": alloc.transfers, "min_recovery_uniform": alloc.min_recovery_start,
                 "min_recovery_maxmin": alloc.min_recovery_end}
     else:

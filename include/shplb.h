@@ -35,6 +35,9 @@ typedef enum {
     SHPLB_NOT_SUPPORTED = 5     /* shape or policy the kernels do not implement */
 } shplb_status;
 
+/* Opaque per-device context (owns device workspace); see shplb_ctx_create. */
+typedef struct shplb_ctx shplb_ctx;
+
 /* Message of the last failed call on this thread ("" after success). */
 const char* shplb_last_error(void);
 /* Library version string, e.g. "shplb-b200 0.1.0 sm_100a". */
@@ -87,6 +90,18 @@ int shplb_recovery_at(int64_t n_points, const int64_t* curve_budgets,
 int shplb_profile_curves_host(const uint16_t* q_rows, const uint16_t* k, int32_t num_q_heads,
                               int32_t num_kv_heads, int64_t n_rows, int64_t n_k, int32_t d,
                               const int64_t* grid, int64_t n_grid, double* recovery_out);
+
+/* The same profile on the GPU: build_profiles +
+ * recovery_ratio PerQueryTopK (profiler.cpp:157-196, attention.cpp:151-184)
+ * as sm_100a kernels — fp64 dot products of the calibration rows against
+ * every key, a per-row descending sort, fp64 prefix masses at the grid
+ * points, mean over rows. q_rows / k are DEVICE bf16 pointers (layouts as
+ * above); grid is host int64, recovery_out host double [num_q_heads][n_grid].
+ * Runs on `stream` and synchronises it. Same validation and messages as the
+ * host version; agrees with it (and the reference) to rounding. */
+int shplb_profile_curves(shplb_ctx* ctx, const void* q_rows, const void* k, int32_t num_q_heads,
+                         int32_t num_kv_heads, int64_t n_rows, int64_t n_k, int32_t d,
+                         const int64_t* grid, int64_t n_grid, double* recovery_out, void* stream);
 
 /* ======================================================================
  * Head -> GPU plan   (reference: proj/include/headbal/partitioner.hpp)
@@ -142,8 +157,6 @@ int shplb_barrier(const double* device_latency, int32_t devices, double* barrier
 /* ======================================================================
  * Block-sparse attention on sm_100a  (reference: proj/include/headbal/attention.hpp)
  * ====================================================================== */
-
-typedef struct shplb_ctx shplb_ctx;
 
 /* One context per CUDA device (rank). Owns the device workspace. */
 int shplb_ctx_create(int device, shplb_ctx** ctx_out);

@@ -292,6 +292,26 @@ class Context:
         check(lib().shplb_ctx_read_timing(self._h, _ptr(buf), max_calls, C.byref(n)))
         return buf[:n.value].copy()
 
+    # -- offline profiler (GPU) ---------------------------------------------
+    def profile_curves(self, q_rows, k, grid, stream=None) -> list[RecoveryCurve]:
+        """PerQueryTopK recovery curves on the GPU (shplb_profile_curves;
+        build_profiles + recovery_ratio, profiler.cpp:157-196,
+        attention.cpp:151-184). q_rows: bf16 CUDA [Hq, rows, d] (the
+        calibration rows), k: bf16 CUDA [Hkv, n_k, d]. Same results as the
+        host profile_curves() to rounding."""
+        import torch
+        q_rows = q_rows.contiguous()
+        k = k.contiguous()
+        _dev_ptr(q_rows, "q_rows", torch.bfloat16)
+        _dev_ptr(k, "k", torch.bfloat16)
+        grid = _i64(grid)
+        hq, rows, d = q_rows.shape
+        hkv, n_k, _ = k.shape
+        out = np.empty((hq, grid.size), np.float64)
+        check(lib().shplb_profile_curves(self._h, q_rows.data_ptr(), k.data_ptr(), hq, hkv, rows, n_k, d,
+                                         _ptr(grid), grid.size, _ptr(out), _stream_ptr(stream)))
+        return [RecoveryCurve(grid.copy(), out[h].copy(), n_k) for h in range(hq)]
+
     # -- kernel 1 ---------------------------------------------------------
     def block_scores(self, q, k, causal=True, stream=None, validate=False, out=None, kv_map=None,
                      block_q=BLOCK_Q):

@@ -2,7 +2,8 @@
 
 Calibration rows (the last `rows` query rows of every head, which see the
 whole context) are profiled into PerQueryTopK recovery curves on the grid
-{0, 128, ..., n} (build_profiles, profiler.cpp:157-196, host C++), and the
+{0, 128, ..., n} (build_profiles, profiler.cpp:157-196: on the GPU profiler
+when q/k are CUDA tensors and a context is given, else host C++), and the
 max-min allocator (allocator.cpp:97-186) shifts budget from sparse to dense
 heads starting from the uniform split of B = fraction * Hq * n tokens, in
 128-token quanta with a 128-token floor, so every budget is a whole number of
@@ -19,15 +20,21 @@ from .workload import bf16_bits
 
 
 def maxmin_budgets(q, k, fraction: float = 0.25, rows: int = 16, quantum: int = 128,
-                   floor: int = 128):
-    """q [Hq, n, d], k [Hkv, n, d] bf16 (any device) -> (budgets int64 [Hq], info dict)."""
+                   floor: int = 128, ctx=None):
+    """q [Hq, n, d], k [Hkv, n, d] bf16 (any device) -> (budgets int64 [Hq], info dict).
+    With ctx (an api.Context) and CUDA tensors the curves come from the GPU
+    profiler, otherwise from the host one."""
     hq, n, _ = q.shape
     total = int(round(fraction * hq * n))
     t0 = time.time()
-    curves = api.profile_curves(bf16_bits(q[:, n - rows:, :]), bf16_bits(k),
-                                api.default_budget_grid(n, 128))
+    grid = api.default_budget_grid(n, 128)
+    if ctx is not None and getattr(q, "is_cuda", False):
+        curves = ctx.profile_curves(q[:, n - rows:, :], k, grid)
+    else:
+        curves = api.profile_curves(bf16_bits(q[:, n - rows:, :]), bf16_bits(k), grid)
     alloc = api.maxmin_allocate(curves, total, quantum=quantum, floor=floor)
     info = {"total_tokens": total, "calibration_rows": rows,
+            "profiler": "gpu" if ctx is not None and getattr(q, "is_cuda", False) else "host",
             "profile_s": round(time.time() - t0, 2), "transfers": alloc.transfers,
             "min_recovery_uniform": alloc.min_recovery_start,
             "min_recovery_maxmin": alloc.min_recovery_end}

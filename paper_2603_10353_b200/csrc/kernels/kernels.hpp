@@ -57,6 +57,18 @@ struct FaParams {
 };
 void launch_fa(const FaParams& p, int num_tiles, cudaStream_t s);
 
+// GPU recovery-curve profiler (profiler.cu). q_rows bf16 [hq][n_rows][128],
+// k bf16 [hkv][n_k][128]; units = hq * n_rows.
+void launch_profile_scores(const void* q_rows, const void* k, int hq, int hkv, int64_t n_rows,
+                           int64_t n_k, double scale, double* scores, cudaStream_t s);
+size_t profile_sort_temp_bytes(int64_t units, int64_t n_k);
+void launch_profile_sort(const double* in, double* out, int64_t units, int64_t n_k, int64_t* offsets,
+                         void* temp, size_t temp_bytes, cudaStream_t s);
+void launch_profile_prefix(const double* sorted, int64_t units, int64_t n_k, const int64_t* grid,
+                           int64_t n_grid, double* mass, cudaStream_t s);
+void launch_profile_rows(const double* mass, int hq, int64_t n_rows, const int64_t* grid, int64_t n_grid,
+                         double* recovery, cudaStream_t s);
+
 // Validation: sets *flag to 1 if any element of x (count elements, bf16) is not finite.
 void launch_check_finite(const void* x, int64_t count, int32_t* flag, cudaStream_t s);
 

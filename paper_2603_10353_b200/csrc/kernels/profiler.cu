@@ -1,0 +1,195 @@
+// GPU recovery-curve profiler: the offline input of the
+// per-head budget table, moved from the host to the B200.
+//
+// Restates build_profiles + recovery_ratio for PerQueryTopK
+// (proj/src/profiler.cpp:157-196, proj/src/attention.cpp:151-184): for every
+// calibration row of every head, the dense softmax weights over all n_k keys
+// (dense_attention, attention.cpp:84-114: max-subtracted, fp64), then at each
+// grid budget k the mass of the k largest weights, averaged over rows.
+//
+//   P1 profile_scores_kernel  s[unit][j] = (q_i . k_j) / sqrt(d) in fp64. bf16
+//      operands are exact in fp64 and each DFMA rounds once, so the dot is the
+//      reference's fp64 dot up to summation order (exact for bf16 data whose
+//      products span < 53 bits). A 128-key tile of K is staged transposed in
+//      shared memory and reused by every calibration row of the GQA group.
+//   P2 segmented radix sort of each unit's scores, descending (CUB, the one
+//      library primitive here; the weights are a monotone map of the scores,
+//      so sorting scores sorts weights).
+//   P3 profile_prefix_kernel  one CTA per unit: Z = sum exp(s - s_max) and the
+//      running top-k mass at every grid point (block scan in fp64).
+//   P4 profile_rows_kernel    recovery[h][g] = sum over rows (ascending) / rows.
+//
+// Results agree with the host restatement and the reference to rounding
+// (the reference itself sums the top-k in nth_element's arbitrary order).
+#include <cstdint>
+
+#include <cub/device/device_segmented_radix_sort.cuh>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+
+namespace shplb::kern {
+namespace {
+
+constexpr int kProfKeys = 128;     // keys per P1 tile
+constexpr int kProfRows = 16;      // calibration rows per P1 pass over the tile
+constexpr int kProfThreads = 256;  // P1: thread = key (t % 128), rows t/128 + 2i
+constexpr int kPrefixThreads = 1024;
+
+__global__ void __launch_bounds__(kProfThreads) profile_scores_kernel(
+    const __nv_bfloat16* __restrict__ q_rows, const __nv_bfloat16* __restrict__ k, int hq, int hkv,
+    int64_t n_rows, int64_t n_k, double scale, double* __restrict__ scores) {
+    // Dynamic shared memory: K tile transposed kt[c][key] (padded rows), then
+    // the current batch of query rows qs[row][c]; fp64 (bf16 is exact in it).
+    extern __shared__ double prof_smem[];
+    auto kt = reinterpret_cast<double(*)[kProfKeys + 1]>(prof_smem);
+    auto qs = reinterpret_cast<double(*)[kHeadDim]>(prof_smem + kHeadDim * (kProfKeys + 1));
+    const int g = blockIdx.y;
+    const int64_t key0 = static_cast<int64_t>(blockIdx.x) * kProfKeys;
+    const int group = hq / hkv;
+    // Stage K[g][key0 .. key0+128) transposed (16-byte loads: 8 bf16 per thread step).
+    for (int e = threadIdx.x; e < kProfKeys * (kHeadDim / 8); e += kProfThreads) {
+        const int key = e / (kHeadDim / 8), c8 = (e % (kHeadDim / 8)) * 8;
+        uint4 w = make_uint4(0, 0, 0, 0);
+        if (key0 + key < n_k)
+            w = *reinterpret_cast<const uint4*>(k + (static_cast<int64_t>(g) * n_k + key0 + key) * kHeadDim + c8);
+        const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&w);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) kt[c8 + u][key] = static_cast<double>(__bfloat162float(b[u]));
+    }
+    const int key = threadIdx.x % kProfKeys;
+    const int64_t rows_total = static_cast<int64_t>(group) * n_rows;  // q heads g*group.. , all rows
+    for (int64_t r0 = 0; r0 < rows_total; r0 += kProfRows) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < kProfRows * kHeadDim; e += kProfThreads) {
+            const int64_t r = r0 + e / kHeadDim;
+            const int c = e % kHeadDim;
+            double x = 0.0;
+            if (r < rows_total) {
+                const int64_t unit = static_cast<int64_t>(g) * group * n_rows + r;  // = h*n_rows + i
+                x = static_cast<double>(__bfloat162float(q_rows[unit * kHeadDim + c]));
+            }
+            qs[e / kHeadDim][c] = x;
+        }
+        __syncthreads();
+        if (key0 + key >= n_k) continue;
+        for (int rr = threadIdx.x / kProfKeys; rr < kProfRows; rr += kProfThreads / kProfKeys) {
+            const int64_t r = r0 + rr;
+            if (r >= rows_total) break;
+            double acc = 0.0;
+#pragma unroll 16
+            for (int c = 0; c < kHeadDim; ++c) acc = fma(qs[rr][c], kt[c][key], acc);
+            const int64_t unit = static_cast<int64_t>(g) * group * n_rows + r;
+            scores[unit * n_k + key0 + key] = acc * scale;
+        }
+    }
+}
+
+// Per unit (one CTA): sorted-descending scores s -> mass[unit][g] = (sum of the
+// first grid[g] weights) where weight = exp(s - s[0]) / Z.
+__global__ void __launch_bounds__(kPrefixThreads) profile_prefix_kernel(
+    const double* __restrict__ sorted, int64_t n_k, const int64_t* __restrict__ grid, int64_t n_grid,
+    double* __restrict__ mass) {
+    __shared__ double part[kPrefixThreads];
+    const int64_t unit = blockIdx.x;
+    const double* s = sorted + unit * n_k;
+    const double m = s[0];
+    const int64_t per = (n_k + kPrefixThreads - 1) / kPrefixThreads;
+    const int64_t lo = threadIdx.x * per, hi = min(lo + per, n_k);
+    double local = 0.0;
+    for (int64_t i = lo; i < hi; ++i) local += exp(s[i] - m);
+    part[threadIdx.x] = local;
+    __syncthreads();
+    // Exclusive scan of the per-thread sums (Hillis-Steele on a copy; fp64).
+    for (int off = 1; off < kPrefixThreads; off <<= 1) {
+        const double add = threadIdx.x >= off ? part[threadIdx.x - off] : 0.0;
+        __syncthreads();
+        part[threadIdx.x] += add;
+        __syncthreads();
+    }
+    const double z = part[kPrefixThreads - 1];
+    double run = part[threadIdx.x] - local;  // exclusive prefix
+    const double inv = 1.0 / z;
+    // First grid point past lo (grid is strictly increasing; entries are counts).
+    int64_t a = 0, b = n_grid;
+    while (a < b) {
+        const int64_t mid = (a + b) / 2;
+        if (grid[mid] <= lo) a = mid + 1; else b = mid;
+    }
+    int64_t gi = a;
+    if (threadIdx.x == 0 && n_grid > 0 && grid[0] == 0) mass[unit * n_grid] = 0.0;
+    for (int64_t i = lo; i < hi && gi < n_grid; ++i) {
+        run += exp(s[i] - m);
+        if (grid[gi] == i + 1) {
+            mass[unit * n_grid + gi] = run * inv;
+            ++gi;
+        }
+    }
+}
+
+__global__ void profile_rows_kernel(const double* __restrict__ mass, int hq, int64_t n_rows,
+                                    const int64_t* __restrict__ grid, int64_t n_grid,
+                                    double* __restrict__ recovery) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<int64_t>(hq) * n_grid) return;
+    const int64_t h = t / n_grid, gi = t % n_grid;
+    double total = 0.0;
+    for (int64_t i = 0; i < n_rows; ++i) total += mass[(h * n_rows + i) * n_grid + gi];
+    recovery[t] = grid[gi] == 0 ? 0.0 : total / static_cast<double>(n_rows);
+}
+
+__global__ void segment_offsets_kernel(int64_t* off, int64_t units, int64_t n_k) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t <= units) off[t] = t * n_k;
+}
+
+}  // namespace
+
+void launch_profile_scores(const void* q_rows, const void* k, int hq, int hkv, int64_t n_rows,
+                           int64_t n_k, double scale, double* scores, cudaStream_t s) {
+    constexpr size_t smem = sizeof(double) * (kHeadDim * (kProfKeys + 1) + kProfRows * kHeadDim);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(profile_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+        configured = true;
+    }
+    const dim3 grid(static_cast<unsigned>((n_k + kProfKeys - 1) / kProfKeys), static_cast<unsigned>(hkv));
+    profile_scores_kernel<<<grid, kProfThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(q_rows),
+                                                        static_cast<const __nv_bfloat16*>(k), hq, hkv, n_rows,
+                                                        n_k, scale, scores);
+}
+
+size_t profile_sort_temp_bytes(int64_t units, int64_t n_k) {
+    size_t bytes = 0;
+    cub::DeviceSegmentedRadixSort::SortKeysDescending(nullptr, bytes, static_cast<const double*>(nullptr),
+                                                      static_cast<double*>(nullptr), units * n_k,
+                                                      static_cast<int64_t>(units),
+                                                      static_cast<const int64_t*>(nullptr),
+                                                      static_cast<const int64_t*>(nullptr));
+    return bytes;
+}
+
+void launch_profile_sort(const double* in, double* out, int64_t units, int64_t n_k, int64_t* offsets,
+                         void* temp, size_t temp_bytes, cudaStream_t s) {
+    segment_offsets_kernel<<<static_cast<unsigned>((units + 256) / 256), 256, 0, s>>>(offsets, units, n_k);
+    cub::DeviceSegmentedRadixSort::SortKeysDescending(temp, temp_bytes, in, out, units * n_k,
+                                                      static_cast<int64_t>(units), offsets, offsets + 1, 0,
+                                                      64, s);
+}
+
+void launch_profile_prefix(const double* sorted, int64_t units, int64_t n_k, const int64_t* grid,
+                           int64_t n_grid, double* mass, cudaStream_t s) {
+    profile_prefix_kernel<<<static_cast<unsigned>(units), kPrefixThreads, 0, s>>>(sorted, n_k, grid, n_grid,
+                                                                                  mass);
+}
+
+void launch_profile_rows(const double* mass, int hq, int64_t n_rows, const int64_t* grid, int64_t n_grid,
+                         double* recovery, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(hq) * n_grid;
+    profile_rows_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(mass, hq, n_rows, grid, n_grid,
+                                                                              recovery);
+}
+
+}  // namespace shplb::kern

@@ -177,6 +177,17 @@ struct shplb_ctx {
     cudaStream_t copy_in = nullptr, copy_out = nullptr;  // its H2D / D2H copy streams
     std::vector<cudaEvent_t> chunk_events;
     size_t host_io_bytes = 0;
+    // GPU profiler workspace (shplb_profile_curves)
+    double* prof_scores = nullptr;
+    size_t prof_scores_bytes = 0;
+    double* prof_sorted = nullptr;
+    size_t prof_sorted_bytes = 0;
+    double* prof_mass = nullptr;
+    size_t prof_mass_bytes = 0;
+    int64_t* prof_aux = nullptr;  // segment offsets, then the grid
+    size_t prof_aux_bytes = 0;
+    void* prof_temp = nullptr;
+    size_t prof_temp_bytes = 0;
     int64_t last_kmax = 0;
     int64_t last_rows = 0;  // Hq * nqb of the last layer call
     int64_t last_n = 0, last_nqb = 0;
@@ -384,6 +395,11 @@ int shplb_ctx_destroy(shplb_ctx* ctx) {
         for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
         cudaFree(ctx->flag);
         cudaFree(ctx->host_io);
+        cudaFree(ctx->prof_scores);
+        cudaFree(ctx->prof_sorted);
+        cudaFree(ctx->prof_mass);
+        cudaFree(ctx->prof_aux);
+        cudaFree(ctx->prof_temp);
         if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
         if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
         for (cudaEvent_t e : ctx->chunk_events) cudaEventDestroy(e);
@@ -683,6 +699,70 @@ int shplb_layer_work(const shplb_layer_shape* shape, const int64_t* budgets_toke
         if (selected_tiles_out) *selected_tiles_out = tiles;
         if (flops_out)
             *flops_out = 4.0 * shape->head_dim * double(kern::kBlock) * double(kern::kBlock) * double(tiles);
+    });
+}
+
+int shplb_profile_curves(shplb_ctx* ctx, const void* q_rows, const void* k, int32_t num_q_heads,
+                         int32_t num_kv_heads, int64_t n_rows, int64_t n_k, int32_t d,
+                         const int64_t* grid, int64_t n_grid, double* recovery_out, void* stream) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx is null");
+        require(num_q_heads >= 1 && num_kv_heads >= 1 && num_q_heads % num_kv_heads == 0,
+                "num_q_heads must be a positive multiple of num_kv_heads");
+        require(n_rows >= 1 && n_k >= 1 && d >= 1, "profile needs at least one row, key and dim");
+        require(grid != nullptr && recovery_out != nullptr, "grid / recovery_out is null");
+        // build_profiles' grid checks (profiler.cpp:165-177).
+        if (n_grid < 1) throw InvalidArgument("budget grid is empty");
+        for (int64_t i = 0; i < n_grid; ++i) {
+            if (grid[i] < 0 || grid[i] > n_k) {
+                throw InvalidArgument("budget grid entry " + std::to_string(grid[i]) + " out of [0, " +
+                                      std::to_string(n_k) + "]");
+            }
+            if (i > 0 && grid[i] <= grid[i - 1]) throw InvalidArgument("budget grid must be strictly increasing");
+        }
+        if (grid[n_grid - 1] != n_k) throw InvalidArgument("budget grid must include the full context length");
+        if (d != kern::kHeadDim)
+            throw NotSupported("head_dim " + std::to_string(d) + " not supported (kernels are built for 128)");
+        check_ptr(q_rows, "q_rows");
+        check_ptr(k, "k");
+        DeviceGuard dg(ctx->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int32_t group = num_q_heads / num_kv_heads;
+        const int64_t units_total = int64_t(num_q_heads) * n_rows;
+        // Kv heads per batch: bounded scores + sorted buffers (2 x 8 B per score, <= 4 GiB).
+        const int64_t units_per_kv = int64_t(group) * n_rows;
+        int64_t kv_batch = std::max<int64_t>(1, (int64_t(1) << 32) / (16 * units_per_kv * n_k));
+        kv_batch = std::min<int64_t>(kv_batch, num_kv_heads);
+        const int64_t units_b = kv_batch * units_per_kv;
+        grow(ctx->prof_scores, ctx->prof_scores_bytes, sizeof(double) * units_b * n_k);
+        grow(ctx->prof_sorted, ctx->prof_sorted_bytes, sizeof(double) * units_b * n_k);
+        grow(ctx->prof_mass, ctx->prof_mass_bytes, sizeof(double) * (units_total * n_grid + int64_t(num_q_heads) * n_grid));
+        grow(ctx->prof_aux, ctx->prof_aux_bytes, sizeof(int64_t) * (units_b + 1 + n_grid));
+        const size_t temp = kern::profile_sort_temp_bytes(units_b, n_k);
+        grow(ctx->prof_temp, ctx->prof_temp_bytes, std::max<size_t>(temp, 16));
+        int64_t* offsets = ctx->prof_aux;
+        int64_t* grid_dev = ctx->prof_aux + units_b + 1;
+        double* recovery_dev = ctx->prof_mass + units_total * n_grid;
+        SHPLB_CUDA(cudaMemcpyAsync(grid_dev, grid, sizeof(int64_t) * n_grid, cudaMemcpyHostToDevice, st));
+        const double scale = 1.0 / std::sqrt(static_cast<double>(d));
+        for (int64_t g0 = 0; g0 < num_kv_heads; g0 += kv_batch) {
+            const int64_t nb = std::min<int64_t>(kv_batch, num_kv_heads - g0);
+            const int64_t units = nb * units_per_kv;
+            const auto* qb = static_cast<const uint16_t*>(q_rows) + g0 * units_per_kv * d;
+            const auto* kb = static_cast<const uint16_t*>(k) + g0 * n_k * d;
+            kern::launch_profile_scores(qb, kb, static_cast<int>(nb * group), static_cast<int>(nb), n_rows, n_k,
+                                        scale, ctx->prof_scores, st);
+            kern::launch_profile_sort(ctx->prof_scores, ctx->prof_sorted, units, n_k, offsets, ctx->prof_temp,
+                                      ctx->prof_temp_bytes, st);
+            kern::launch_profile_prefix(ctx->prof_sorted, units, n_k, grid_dev, n_grid,
+                                        ctx->prof_mass + g0 * units_per_kv * n_grid, st);
+            check_launch(ctx, 4);
+        }
+        kern::launch_profile_rows(ctx->prof_mass, num_q_heads, n_rows, grid_dev, n_grid, recovery_dev, st);
+        check_launch(ctx);
+        SHPLB_CUDA(cudaMemcpyAsync(recovery_out, recovery_dev, sizeof(double) * num_q_heads * n_grid,
+                                   cudaMemcpyDeviceToHost, st));
+        SHPLB_CUDA(cudaStreamSynchronize(st));
     });
 }
 

@@ -1,0 +1,85 @@
+"""GPU recovery-curve profiler (shplb_profile_curves) against
+the host restatement and the compiled reference's build_profiles
+(profiler.cpp:157-196, recovery_ratio PerQueryTopK attention.cpp:151-184).
+
+Curves are fp64; the reference sums each top-k in nth_element's arbitrary
+order, so agreement is to rounding (1e-12 absolute). The max-min budget
+table computed from the GPU curves must equal the one from the host curves
+(integer decisions on those curves).
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2603_10353_b200 as P
+from oracle import oracle as O
+from paper_2603_10353_b200.workload import LayerSpec, bf16_bits, make_layer
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def _rand_bf16(rng, shape, scale=1.0):
+    return torch.from_numpy((rng.standard_normal(shape) * scale).astype(np.float32)).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("hq,hkv,rows,n_k,stride", [(4, 2, 6, 300, 32), (8, 8, 3, 1000, 64),
+                                                    (4, 1, 16, 4096, 128), (2, 1, 1, 129, 1)])
+def test_gpu_profile_matches_host(cuda_ctx, hq, hkv, rows, n_k, stride):
+    rng = np.random.default_rng(hq * 1000 + n_k)
+    q = _rand_bf16(rng, (hq, rows, 128)) * torch.from_numpy(
+        rng.uniform(0.05, 0.5, (hq, 1, 1)).astype(np.float32)).to(torch.bfloat16)
+    k = _rand_bf16(rng, (hkv, n_k, 128))
+    grid = P.default_budget_grid(n_k, stride)
+    host = P.profile_curves(bf16_bits(q), bf16_bits(k), grid)
+    gpu = cuda_ctx.profile_curves(q.cuda(), k.cuda(), grid)
+    for h in range(hq):
+        assert np.abs(gpu[h].recovery - host[h].recovery).max() < TOL, f"head {h}"
+        assert gpu[h].recovery[0] == 0.0 and abs(gpu[h].recovery[-1] - 1.0) < 1e-9
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built")
+def test_gpu_profile_matches_reference_build_profiles(cuda_ctx):
+    rng = np.random.default_rng(11)
+    hq, hkv, rows, n_k = 4, 2, 5, 700
+    q = _rand_bf16(rng, (hq, rows, 128), 0.3)
+    k = _rand_bf16(rng, (hkv, n_k, 128))
+    grid = P.default_budget_grid(n_k, 64)
+    gpu = cuda_ctx.profile_curves(q.cuda(), k.cuda(), grid)
+    Q = q.float().numpy().astype(np.float64)
+    K = np.repeat(k.float().numpy().astype(np.float64), hq // hkv, axis=0)
+    ref = O.ref.build_profiles(Q, K, np.zeros_like(K), grid)
+    for h in range(hq):
+        assert np.abs(gpu[h].recovery - ref[h]).max() < TOL
+
+
+def test_gpu_profile_budget_table_equals_host(cuda_ctx):
+    """The bench's calibration (last 16 rows of a structured 8K layer) ->
+    max-min budgets: identical from GPU and host curves."""
+    spec = LayerSpec(num_q_heads=32, num_kv_heads=8, seq_len=8192, seed=2603)
+    q, k, _ = make_layer(spec, "cpu")
+    n = spec.seq_len
+    grid = P.default_budget_grid(n, 128)
+    host = P.profile_curves(bf16_bits(q[:, n - 16:, :]), bf16_bits(k), grid)
+    gpu = cuda_ctx.profile_curves(q[:, n - 16:, :].cuda(), k.cuda(), grid)
+    worst = max(np.abs(g.recovery - h.recovery).max() for g, h in zip(gpu, host))
+    assert worst < TOL
+    total = int(0.25 * 32 * n)
+    a = P.maxmin_allocate(host, total, quantum=128, floor=128).budgets
+    b = P.maxmin_allocate(gpu, total, quantum=128, floor=128).budgets
+    assert np.array_equal(a, b)
+
+
+def test_gpu_profile_errors(cuda_ctx):
+    q = torch.zeros((2, 2, 128), dtype=torch.bfloat16, device="cuda")
+    k = torch.zeros((1, 64, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(P.InvalidArgument, match="budget grid must include the full context length"):
+        cuda_ctx.profile_curves(q, k, [0, 32])
+    with pytest.raises(P.InvalidArgument, match="strictly increasing"):
+        cuda_ctx.profile_curves(q, k, [0, 32, 32, 64])
+    with pytest.raises(P.InvalidArgument, match=r"budget grid entry 65 out of \[0, 64\]"):
+        cuda_ctx.profile_curves(q, k, [0, 65])
+    with pytest.raises(P.InvalidArgument, match="multiple of num_kv_heads"):
+        cuda_ctx.profile_curves(torch.zeros((3, 2, 128), dtype=torch.bfloat16, device="cuda"),
+                                torch.zeros((2, 64, 128), dtype=torch.bfloat16, device="cuda"), [0, 64])
