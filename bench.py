@@ -57,6 +57,10 @@ def parse_args():
     p.add_argument("--budget-fraction", type=float, default=0.25)
     p.add_argument("--calib-rows", type=int, default=16)
     p.add_argument("--seed", type=int, default=2603)
+    p.add_argument("--allocation-json", default=None,
+                   help="budget table from an allocation.json (reference format) instead of profiling")
+    p.add_argument("--assignment-json", default=None,
+                   help="S-HPLB head plan from an assignment.json (reference format) instead of greedy_assign")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -192,6 +196,11 @@ def make_budgets(q, k, args, world, rank):
     n, hq = args.seq_len, args.q_heads
     total = int(round(args.budget_fraction * hq * n))
     info = {}
+    if args.allocation_json:  # a budget table written by the reference CLI (allocator.cpp:240-273)
+        la = P.formats.load_allocation(args.allocation_json)
+        if la.budgets.size != hq:
+            raise SystemExit(f"{args.allocation_json}: {la.budgets.size} budgets for {hq} heads")
+        return la.budgets.astype(np.int64), la.total, {"source": args.allocation_json}
     if rank == 0:
         t0 = time.time()
         rows = q[:, n - args.calib_rows:, :]
@@ -425,6 +434,12 @@ def main():
     stream = torch.cuda.Stream()
 
     plans = {"greedy": P.greedy_assign(budgets, world)}
+    if args.assignment_json:  # a head plan written by the reference CLI (partitioner.cpp:288-334)
+        la = P.formats.load_assignment(args.assignment_json)
+        if la.devices != world or la.device_of_head.size != args.q_heads:
+            raise SystemExit(f"{args.assignment_json}: plan for {la.devices} devices / "
+                             f"{la.device_of_head.size} heads, run has {world} / {args.q_heads}")
+        plans["greedy"] = la.device_of_head.astype(np.int32)
     if world > 1:
         plans["naive"] = P.naive_assign(budgets, world)
         plans["split"] = P.split_assign(budgets, world, n)

@@ -115,6 +115,20 @@ def _load_ref():
         L.ref_simulate.argtypes = [_i64p, C.c_int32, C.c_double, C.c_double, _f64p,
                                    C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.ref_max_threads.restype = C.c_int
+        cp, vp = C.c_char_p, C.c_void_p
+        L.ref_save_allocation.argtypes = [cp, C.c_int32, _i32p, _i32p, _i64p, C.c_int64, C.c_int64]
+        L.ref_load_allocation.argtypes = [cp, C.c_int32, _i32p, _i32p, _i64p, C.POINTER(C.c_int32),
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.ref_save_assignment.argtypes = [cp, C.c_int32, _i32p, _i32p, _i32p, C.c_int32, _i64p,
+                                          C.c_double]
+        L.ref_load_assignment.argtypes = [cp, C.c_int32, C.c_int32, _i32p, _i32p, _i32p,
+                                          C.POINTER(C.c_int32), C.POINTER(C.c_int32), _i64p,
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_double)]
+        L.ref_save_profiles.argtypes = [cp, C.c_int32, _i32p, _i32p, C.c_int64, _i64p, _i64p,
+                                        _f64p, C.c_int, cp, cp]
+        L.ref_load_profiles.argtypes = [cp, C.c_int32, C.c_int64, _i32p, _i32p, _i64p, _i64p,
+                                        _f64p, C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int), vp, vp, C.c_int64]
         _ref = L
     return _ref
 
@@ -431,6 +445,73 @@ class ref:
         _ref_check(_load_ref().ref_simulate(loads, loads.size, alpha, beta, lat, C.byref(b),
                                             C.byref(bub)))
         return lat, float(b.value), float(bub.value)
+
+    # -- file formats (allocator.cpp:223-275, partitioner.cpp:268-336,
+    #    profiler.cpp:300-383) ------------------------------------------------
+    @staticmethod
+    def save_allocation(path, budgets, total, floor, heads=None):
+        budgets = np.ascontiguousarray(budgets, np.int64)
+        n = budgets.size
+        hl = np.asarray(heads if heads is not None else [(0, h) for h in range(n)], np.int32).reshape(n, 2)
+        _ref_check(_load_ref().ref_save_allocation(str(path).encode(), n, np.ascontiguousarray(hl[:, 0]),
+                                                   np.ascontiguousarray(hl[:, 1]), budgets, total, floor))
+
+    @staticmethod
+    def load_allocation(path, max_n=4096):
+        lay, hd = np.empty(max_n, np.int32), np.empty(max_n, np.int32)
+        b = np.empty(max_n, np.int64)
+        n, tot, fl = C.c_int32(), C.c_int64(), C.c_int64()
+        _ref_check(_load_ref().ref_load_allocation(str(path).encode(), max_n, lay, hd, b, C.byref(n),
+                                                   C.byref(tot), C.byref(fl)))
+        k = n.value
+        return b[:k].copy(), list(zip(lay[:k].tolist(), hd[:k].tolist())), int(tot.value), int(fl.value)
+
+    @staticmethod
+    def save_assignment(path, device_of_head, devices, loads, imbalance, heads=None):
+        dev = np.ascontiguousarray(device_of_head, np.int32)
+        n = dev.size
+        hl = np.asarray(heads if heads is not None else [(0, h) for h in range(n)], np.int32).reshape(n, 2)
+        _ref_check(_load_ref().ref_save_assignment(str(path).encode(), n, np.ascontiguousarray(hl[:, 0]),
+                                                   np.ascontiguousarray(hl[:, 1]), dev, devices,
+                                                   np.ascontiguousarray(loads, np.int64), float(imbalance)))
+
+    @staticmethod
+    def load_assignment(path, max_n=4096, max_devices=1024):
+        lay, hd, dev = (np.empty(max_n, np.int32) for _ in range(3))
+        loads = np.empty(max_devices, np.int64)
+        n, nd, tot, imb = C.c_int32(), C.c_int32(), C.c_int64(), C.c_double()
+        _ref_check(_load_ref().ref_load_assignment(str(path).encode(), max_n, max_devices, lay, hd, dev,
+                                                   C.byref(n), C.byref(nd), loads, C.byref(tot), C.byref(imb)))
+        k = n.value
+        return (dev[:k].copy(), list(zip(lay[:k].tolist(), hd[:k].tolist())), int(nd.value),
+                loads[:nd.value].copy(), int(tot.value), float(imb.value))
+
+    @staticmethod
+    def save_profiles(path, budgets_list, recovery_list, context_length, heads=None, kind=0,
+                      request="calibration", task="synthetic"):
+        n = len(budgets_list)
+        offsets = np.zeros(n + 1, np.int64)
+        offsets[1:] = np.cumsum([len(b) for b in budgets_list])
+        pb = np.ascontiguousarray(np.concatenate([np.asarray(b, np.int64) for b in budgets_list]))
+        pr = np.ascontiguousarray(np.concatenate([np.asarray(r, np.float64) for r in recovery_list]))
+        hl = np.asarray(heads if heads is not None else [(0, h) for h in range(n)], np.int32).reshape(n, 2)
+        _ref_check(_load_ref().ref_save_profiles(str(path).encode(), n, np.ascontiguousarray(hl[:, 0]),
+                                                 np.ascontiguousarray(hl[:, 1]), context_length, offsets, pb,
+                                                 pr, kind, request.encode(), task.encode()))
+
+    @staticmethod
+    def load_profiles(path, max_heads=1024, max_points=1 << 22):
+        lay, hd = np.empty(max_heads, np.int32), np.empty(max_heads, np.int32)
+        off = np.zeros(max_heads + 1, np.int64)
+        pb, pr = np.empty(max_points, np.int64), np.empty(max_points, np.float64)
+        n, ctxl, kind = C.c_int32(), C.c_int64(), C.c_int()
+        req, task = C.create_string_buffer(1024), C.create_string_buffer(1024)
+        _ref_check(_load_ref().ref_load_profiles(str(path).encode(), max_heads, max_points, lay, hd, off, pb,
+                                                 pr, C.byref(n), C.byref(ctxl), C.byref(kind), req, task, 1024))
+        k = n.value
+        curves = [(pb[off[h]:off[h + 1]].copy(), pr[off[h]:off[h + 1]].copy()) for h in range(k)]
+        return (curves, list(zip(lay[:k].tolist(), hd[:k].tolist())), int(ctxl.value), int(kind.value),
+                req.value.decode(), task.value.decode())
 
     @staticmethod
     def max_threads() -> int:

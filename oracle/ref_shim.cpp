@@ -13,6 +13,7 @@
 
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -285,6 +286,120 @@ int ref_simulate(const int64_t* loads, int32_t devices, double alpha, double bet
         for (int32_t d = 0; d < devices; ++d) latency_out[d] = s.device_latency[d];
         *barrier_out = s.barrier_latency;
         *bubble_out = s.bubble_fraction;
+    });
+}
+
+// ---- file formats (allocator.cpp:223-275, partitioner.cpp:268-336,
+// profiler.cpp:300-383): the reference's own writers and strict loaders, so
+// the tests can cross-check files both ways.
+
+int ref_save_allocation(const char* path, int32_t n, const int32_t* layers, const int32_t* heads,
+                        const int64_t* budgets, int64_t total, int64_t floor) {
+    return guarded([&] {
+        headbal::BudgetAllocation a;
+        for (int32_t i = 0; i < n; ++i) {
+            a.heads.push_back(headbal::HeadId{layers[i], heads[i]});
+            a.budgets.push_back(budgets[i]);
+        }
+        a.total = total;
+        a.floor = floor;
+        headbal::save_allocation(path, a);
+    });
+}
+
+int ref_load_allocation(const char* path, int32_t max_n, int32_t* layers, int32_t* heads,
+                        int64_t* budgets, int32_t* n_out, int64_t* total, int64_t* floor) {
+    return guarded([&] {
+        const auto a = headbal::load_allocation(path);
+        *n_out = static_cast<int32_t>(a.budgets.size());
+        for (int32_t i = 0; i < *n_out && i < max_n; ++i) {
+            layers[i] = a.heads[i].layer;
+            heads[i] = a.heads[i].head;
+            budgets[i] = a.budgets[i];
+        }
+        *total = a.total;
+        *floor = a.floor;
+    });
+}
+
+int ref_save_assignment(const char* path, int32_t n, const int32_t* layers, const int32_t* heads,
+                        const int32_t* device_of_head, int32_t devices, const int64_t* loads,
+                        double imbalance) {
+    return guarded([&] {
+        headbal::Assignment a;
+        a.num_devices = devices;
+        a.device_of_head.assign(device_of_head, device_of_head + n);
+        headbal::LoadReport r;
+        r.loads.assign(loads, loads + devices);
+        for (long l : r.loads) r.total += l;
+        r.imbalance = imbalance;
+        std::vector<headbal::HeadId> ids;
+        for (int32_t i = 0; i < n; ++i) ids.push_back(headbal::HeadId{layers[i], heads[i]});
+        headbal::save_assignment(path, a, r, ids);
+    });
+}
+
+int ref_load_assignment(const char* path, int32_t max_n, int32_t max_devices, int32_t* layers,
+                        int32_t* heads, int32_t* device_of_head, int32_t* n_out, int32_t* devices_out,
+                        int64_t* loads, int64_t* total, double* imbalance) {
+    return guarded([&] {
+        const auto a = headbal::load_assignment(path);
+        *n_out = static_cast<int32_t>(a.heads.size());
+        for (int32_t i = 0; i < *n_out && i < max_n; ++i) {
+            layers[i] = a.heads[i].layer;
+            heads[i] = a.heads[i].head;
+            device_of_head[i] = a.assignment.device_of_head[i];
+        }
+        *devices_out = a.assignment.num_devices;
+        for (int32_t d = 0; d < a.assignment.num_devices && d < max_devices; ++d) loads[d] = a.report.loads[d];
+        *total = a.report.total;
+        *imbalance = a.report.imbalance;
+    });
+}
+
+int ref_save_profiles(const char* path, int32_t n_heads, const int32_t* layers, const int32_t* heads,
+                      int64_t context_length, const int64_t* offsets, const int64_t* budgets,
+                      const double* recovery, int kind, const char* request, const char* task) {
+    return guarded([&] {
+        const auto curves = to_curves(n_heads, context_length, offsets, budgets, recovery);
+        std::vector<headbal::HeadProfile> ps(static_cast<std::size_t>(n_heads));
+        for (int32_t h = 0; h < n_heads; ++h) {
+            ps[h].curve = curves[h];
+            ps[h].curve.id = headbal::HeadId{layers[h], heads[h]};
+            ps[h].provenance = headbal::Provenance{request, task};
+            ps[h].policy = kind == 0 ? headbal::SelectionKind::PerQueryTopK
+                                     : headbal::SelectionKind::ColumnAggregateTopK;
+        }
+        headbal::save_profiles(path, ps);
+    });
+}
+
+// Points of profile h land at [offsets[h], offsets[h+1]) (offsets sized max_heads+1).
+int ref_load_profiles(const char* path, int32_t max_heads, int64_t max_points, int32_t* layers,
+                      int32_t* heads, int64_t* offsets, int64_t* budgets, double* recovery,
+                      int32_t* n_heads_out, int64_t* context_length, int* kind, char* request,
+                      char* task, int64_t text_cap) {
+    return guarded([&] {
+        const auto ps = headbal::load_profiles(path);
+        *n_heads_out = static_cast<int32_t>(ps.size());
+        int64_t at = 0;
+        for (int32_t h = 0; h < *n_heads_out && h < max_heads; ++h) {
+            layers[h] = ps[h].curve.id.layer;
+            heads[h] = ps[h].curve.id.head;
+            offsets[h] = at;
+            for (const auto& pt : ps[h].curve.points) {
+                if (at < max_points) {
+                    budgets[at] = pt.budget;
+                    recovery[at] = pt.recovery;
+                }
+                ++at;
+            }
+            offsets[h + 1] = at;
+        }
+        *context_length = ps.empty() ? 0 : ps[0].curve.context_length;
+        *kind = ps.empty() || ps[0].policy == headbal::SelectionKind::PerQueryTopK ? 0 : 1;
+        std::snprintf(request, static_cast<size_t>(text_cap), "%s", ps.empty() ? "" : ps[0].provenance.request.c_str());
+        std::snprintf(task, static_cast<size_t>(text_cap), "%s", ps.empty() ? "" : ps[0].provenance.task.c_str());
     });
 }
 

@@ -2,16 +2,18 @@
 
 Host API over libshplb.so (C ABI: include/shplb.h). See DESIGN.md.
 """
-from ._native import (CudaError, InvalidArgument, LogicError, NotSupported, ShplbError, build,
-                      lib)
+from ._native import (CudaError, InvalidArgument, LogicError, NotSupported, ShplbError,
+                      ShplbRuntimeError, build, lib)
 from .api import (BLOCK, BLOCK_Q, HEAD_DIM, BudgetAllocation, Context, LoadReport, RecoveryCurve,
                   SimulationResult, barrier, default_budget_grid, greedy_assign, imbalance,
                   layer_work, maxmin_allocate, naive_assign, profile_curves, simulate,
                   split_assign, uniform_allocate)
+from . import formats  # noqa: E402  (allocation / assignment / profiles JSON, reference layout)
 
 __all__ = [
     "BLOCK", "BLOCK_Q", "HEAD_DIM", "BudgetAllocation", "Context", "CudaError", "InvalidArgument",
-    "LoadReport", "LogicError", "NotSupported", "RecoveryCurve", "ShplbError", "SimulationResult",
+    "LoadReport", "LogicError", "NotSupported", "RecoveryCurve", "ShplbError", "ShplbRuntimeError",
+    "SimulationResult",
     "barrier", "build", "default_budget_grid", "greedy_assign", "imbalance", "layer_work", "lib",
     "maxmin_allocate", "naive_assign", "profile_curves", "simulate", "split_assign",
     "uniform_allocate",

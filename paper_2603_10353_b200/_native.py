@@ -45,6 +45,10 @@ class InvalidArgument(ShplbError, ValueError):
     """The reference's std::invalid_argument (bad shapes, budgets, totals)."""
 
 
+class ShplbRuntimeError(ShplbError):
+    """The reference's std::runtime_error (I/O and file-schema errors)."""
+
+
 class LogicError(ShplbError):
     """The reference's std::logic_error."""
 
@@ -59,7 +63,7 @@ class NotSupported(ShplbError, NotImplementedError):
 
 _ERRORS = {
     SHPLB_INVALID_ARGUMENT: InvalidArgument,
-    SHPLB_RUNTIME_ERROR: ShplbError,
+    SHPLB_RUNTIME_ERROR: ShplbRuntimeError,
     SHPLB_LOGIC_ERROR: LogicError,
     SHPLB_CUDA_ERROR: CudaError,
     SHPLB_NOT_SUPPORTED: NotSupported,
