@@ -235,6 +235,15 @@ int shplb_sparse_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape,
                                  const void* k, const void* v,
                                  const int64_t* budgets_tokens, void* out, void* stream);
 
+/* Dense comparator (the reference's dense_attention_all,
+ * attention.cpp:84-114,204-212, minus the weight matrix): every head attends
+ * to every causally visible key through the same sm_100a kernel 3 (kernels 1
+ * and 2 are skipped; the selection is every visible key block). The
+ * "vs full attention" axis of the paper. With stage timing on, the k1/k2
+ * entries of the call read 0. */
+int shplb_dense_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
+                                const void* k, const void* v, void* out, void* stream);
+
 /* Same layer call on HOST buffers (bf16 bit patterns, same layouts): copies q/k/v
  * host->device into context-owned device memory, runs kernels 1-3, copies out
  * device->host and synchronises the stream. Pinned host memory makes the

@@ -9,6 +9,7 @@ from .api import (BLOCK, BLOCK_Q, HEAD_DIM, BudgetAllocation, Context, LoadRepor
                   layer_work, maxmin_allocate, naive_assign, profile_curves, simulate,
                   split_assign, uniform_allocate)
 from . import formats  # noqa: E402  (allocation / assignment / profiles JSON, reference layout)
+from . import experiments  # noqa: E402  (sweep / skyline on measured latency)
 
 __all__ = [
     "BLOCK", "BLOCK_Q", "HEAD_DIM", "BudgetAllocation", "Context", "CudaError", "InvalidArgument",

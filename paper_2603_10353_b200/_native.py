@@ -24,7 +24,7 @@ EXPORTS = (
     "shplb_ctx_create", "shplb_ctx_destroy", "shplb_ctx_launch_count",
     "shplb_ctx_set_timing", "shplb_ctx_read_timing",
     "shplb_block_scores", "shplb_select_blocks", "shplb_block_sparse_attention",
-    "shplb_sparse_attention_layer", "shplb_sparse_attention_layer_host",
+    "shplb_sparse_attention_layer", "shplb_sparse_attention_layer_host", "shplb_dense_attention_layer",
     "shplb_last_selection", "shplb_copy_last_selection",
     "shplb_layer_work", "shplb_last_selection_work",
 )
@@ -148,6 +148,7 @@ def lib() -> C.CDLL:
                                                vp]
     L.shplb_sparse_attention_layer.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp, vp]
     L.shplb_sparse_attention_layer_host.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp, vp]
+    L.shplb_dense_attention_layer.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp]
     L.shplb_last_selection.argtypes = [vp, P(vp), P(vp), P(i64)]
     L.shplb_copy_last_selection.argtypes = [vp, vp, i64, vp, i64, vp]
     L.shplb_layer_work.argtypes = [P(LayerShape), vp, P(i64), P(f64)]

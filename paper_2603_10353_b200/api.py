@@ -378,6 +378,20 @@ class Context:
             _stream_ptr(stream)))
         return out
 
+    def dense_attention_layer(self, q, k, v, causal=True, stream=None, out=None, validate=False,
+                              kv_map=None, block_q=BLOCK_Q):
+        """Dense comparator (shplb_dense_attention_layer): every head over every
+        causally visible key, through the same sm_100a kernel 3."""
+        import torch
+        hq, n, d = q.shape
+        if out is None:
+            out = torch.empty_like(q)
+        sh = _shape(hq, k.shape[0], n, causal, validate, kv_map, d, block_q, None)
+        check(lib().shplb_dense_attention_layer(
+            self._h, C.byref(sh), _dev_ptr(q, "q", torch.bfloat16), _dev_ptr(k, "k", torch.bfloat16),
+            _dev_ptr(v, "v", torch.bfloat16), _dev_ptr(out, "out", torch.bfloat16), _stream_ptr(stream)))
+        return out
+
     def sparse_attention_layer_host(self, q, k, v, budgets_tokens, causal=True, out=None,
                                     stream=None, kv_map=None, block_q=BLOCK_Q, q_block_range=None):
         """The layer call on HOST bf16 tensors (pinned for async DMA): copy in,

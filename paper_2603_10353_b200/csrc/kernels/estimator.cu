@@ -281,6 +281,26 @@ void launch_select_from_scores(const float* scores, int hq, int64_t n, int bq, b
                                                idx, cnt);
 }
 
+namespace {
+// Dense comparator selection: every causally visible key block, ascending.
+__global__ void dense_selection_kernel(int32_t* idx, int32_t* cnt, int64_t rows, int64_t nqb, int64_t nkb,
+                                       int bq, int64_t n, int causal) {
+    const int64_t row = blockIdx.x;  // (head, query block)
+    if (row >= rows) return;
+    const int64_t qb = row % nqb;
+    const int64_t last = min((qb + 1) * bq, n) - 1;
+    const int64_t vis = causal ? min(last / kBlock + 1, nkb) : nkb;
+    for (int64_t j = threadIdx.x; j < nkb; j += blockDim.x) idx[row * nkb + j] = j < vis ? static_cast<int32_t>(j) : -1;
+    if (threadIdx.x == 0) cnt[row] = static_cast<int32_t>(vis);
+}
+}  // namespace
+
+void launch_dense_selection(int32_t* idx, int32_t* cnt, int hq, int64_t n, int bq, bool causal, cudaStream_t s) {
+    const int64_t nqb = (n + bq - 1) / bq, nkb = (n + kBlock - 1) / kBlock;
+    dense_selection_kernel<<<static_cast<unsigned>(hq * nqb), 256, 0, s>>>(idx, cnt, hq * nqb, nqb, nkb, bq, n,
+                                                                          causal ? 1 : 0);
+}
+
 void launch_check_finite(const void* x, int64_t count, int32_t* flag, cudaStream_t s) {
     check_finite_kernel<<<148 * 8, 256, 0, s>>>(static_cast<const uint16_t*>(x), count, flag);
 }

@@ -69,6 +69,10 @@ void launch_profile_prefix(const double* sorted, int64_t units, int64_t n_k, con
 void launch_profile_rows(const double* mass, int hq, int64_t n_rows, const int64_t* grid, int64_t n_grid,
                          double* recovery, cudaStream_t s);
 
+// Dense comparator: idx [hq][nqb][nkb] = every visible key block ascending
+// (tail -1), cnt [hq][nqb] = visible count.
+void launch_dense_selection(int32_t* idx, int32_t* cnt, int hq, int64_t n, int bq, bool causal, cudaStream_t s);
+
 // Validation: sets *flag to 1 if any element of x (count elements, bf16) is not finite.
 void launch_check_finite(const void* x, int64_t count, int32_t* flag, cudaStream_t s);
 

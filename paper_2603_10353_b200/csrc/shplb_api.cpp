@@ -177,6 +177,12 @@ struct shplb_ctx {
     cudaStream_t copy_in = nullptr, copy_out = nullptr;  // its H2D / D2H copy streams
     std::vector<cudaEvent_t> chunk_events;
     size_t host_io_bytes = 0;
+    // Dense comparator selection (shplb_dense_attention_layer), cached per key.
+    int32_t* dense_idx = nullptr;
+    size_t dense_idx_bytes = 0;
+    int32_t* dense_cnt = nullptr;
+    size_t dense_cnt_bytes = 0;
+    std::vector<int64_t> dense_key;
     // GPU profiler workspace (shplb_profile_curves)
     double* prof_scores = nullptr;
     size_t prof_scores_bytes = 0;
@@ -395,6 +401,8 @@ int shplb_ctx_destroy(shplb_ctx* ctx) {
         for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
         cudaFree(ctx->flag);
         cudaFree(ctx->host_io);
+        cudaFree(ctx->dense_idx);
+        cudaFree(ctx->dense_cnt);
         cudaFree(ctx->prof_scores);
         cudaFree(ctx->prof_sorted);
         cudaFree(ctx->prof_mass);
@@ -532,6 +540,40 @@ int shplb_sparse_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape,
         ctx->last_nqb = nqb;
         ctx->last_bq = shape->block_q;
         ctx->last_causal = shape->causal;
+    });
+}
+
+int shplb_dense_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
+                                const void* k, const void* v, void* out, void* stream) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx is null");
+        check_shape(shape);
+        check_ptr(q, "q");
+        check_ptr(k, "k");
+        check_ptr(v, "v");
+        check_ptr(out, "out");
+        kern::HeadTable ht{};
+        fill_kv_map(shape, ht);
+        DeviceGuard g(ctx->device);
+        auto st = static_cast<cudaStream_t>(stream);
+        if (shape->validate) validate_inputs(ctx, shape, q, k, v, st);
+        const int64_t nqb = cdiv(shape->seq_len, shape->block_q), nkb = cdiv(shape->seq_len, kern::kBlock);
+        const std::vector<int64_t> key = {shape->seq_len, shape->block_q, shape->causal, shape->num_q_heads};
+        if (key != ctx->dense_key) {
+            grow(ctx->dense_idx, ctx->dense_idx_bytes, sizeof(int32_t) * shape->num_q_heads * nqb * nkb);
+            grow(ctx->dense_cnt, ctx->dense_cnt_bytes, sizeof(int32_t) * shape->num_q_heads * nqb);
+            kern::launch_dense_selection(ctx->dense_idx, ctx->dense_cnt, shape->num_q_heads, shape->seq_len,
+                                         shape->block_q, shape->causal != 0, st);
+            check_launch(ctx);
+            ctx->dense_key = key;
+        }
+        build_tiles(ctx, shape, std::vector<int32_t>(static_cast<size_t>(shape->num_q_heads),
+                                                     static_cast<int32_t>(nkb)));
+        mark(ctx, 0, st);
+        mark(ctx, 1, st);
+        mark(ctx, 2, st);
+        run_fa(ctx, shape, q, k, v, ctx->dense_idx, ctx->dense_cnt, nkb, out, st);
+        mark(ctx, 3, st);
     });
 }
 

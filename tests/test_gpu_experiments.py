@@ -1,0 +1,60 @@
+"""Dense comparator (shplb_dense_attention_layer) and the measured sweep /
+skyline drivers."""
+import io
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2603_10353_b200 as P
+from oracle import oracle as O
+from paper_2603_10353_b200 import experiments as X
+from paper_2603_10353_b200.workload import LayerSpec, bf16_bits, make_layer
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n,causal,bq", [(1024, True, 256), (777, True, 128), (640, False, 256)])
+def test_dense_layer_equals_full_budget_sparse_and_oracle(cuda_ctx, n, causal, bq):
+    spec = LayerSpec(num_q_heads=4, num_kv_heads=2, seq_len=n, seed=21)
+    q, k, v = make_layer(spec, "cpu")
+    qd, kd, vd = q.cuda(), k.cuda(), v.cuda()
+    dense = cuda_ctx.dense_attention_layer(qd, kd, vd, causal=causal, block_q=bq)
+    full = cuda_ctx.sparse_attention_layer(qd, kd, vd, np.full(4, n, np.int64), causal=causal, block_q=bq)
+    torch.cuda.synchronize()
+    assert torch.equal(dense, full), "dense comparator differs from the all-blocks sparse layer"
+    nkb = (n + 127) // 128
+    _, _, _, ref = O.layer(bf16_bits(q), bf16_bits(k), bf16_bits(v), np.full(4, nkb, np.int64), bq=bq,
+                           causal=causal, kmax=nkb)
+    g = dense.float().cpu().numpy().astype(np.float64)
+    assert np.abs(g - ref).max() <= 2e-2
+    assert np.abs(g - ref).sum() / np.abs(ref).sum() <= 4e-3
+
+
+def test_measured_sweep_and_skyline_small(cuda_ctx):
+    spec = LayerSpec(num_q_heads=8, num_kv_heads=2, seq_len=2048, seed=5)
+    q, k, v = make_layer(spec, "cuda")
+    n = spec.seq_len
+    curves = cuda_ctx.profile_curves(q[:, n - 16:, :].contiguous(), k, P.default_budget_grid(n, 128))
+    budgets = P.maxmin_allocate(curves, int(0.25 * 8 * n), quantum=128, floor=128).budgets
+    rows = X.measured_sweep(cuda_ctx, {n: (q, k, v, budgets)}, [1, 2], steps=1)
+    assert [(r.degree, r.assigner) for r in rows] == [(1, "naive"), (1, "greedy"), (1, "split"),
+                                                      (2, "naive"), (2, "greedy"), (2, "split")]
+    for r in rows:
+        assert r.barrier_latency > 0 and 0.0 <= r.bubble_fraction < 1.0
+        assert r.barrier_latency == pytest.approx(max(r.per_rank_ms))
+    buf = io.StringIO()
+    X.write_sweep_csv(buf, rows)
+    assert buf.getvalue().splitlines()[0] == ("degree,context_length,allocator,assigner,barrier_latency,"
+                                              "bubble_fraction,imbalance,speedup_vs_naive")
+    pts = X.measured_skyline(cuda_ctx, q, k, v, curves, devices=2, steps=1)
+    assert [(p.allocator) for p in pts] == ["uniform", "maxmin"] * 4
+    full = [p for p in pts if p.total_budget == 8 * n]
+    # all keys kept: the sparse layer is the dense one -> zero error (attention.cpp:186-202)
+    assert all(p.mean_output_error == 0.0 for p in full)
+    # more budget never hurts: error falls monotonically with the total, per allocator
+    for kind in ("uniform", "maxmin"):
+        e = [p.mean_output_error for p in pts if p.allocator == kind]
+        assert all(a >= b for a, b in zip(e, e[1:])), (kind, e)
+    with pytest.raises(P.InvalidArgument, match="infeasible"):
+        X.measured_skyline(cuda_ctx, q, k, v, curves, devices=2, totals=[10])

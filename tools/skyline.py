@@ -1,0 +1,50 @@
+"""Measured sweep and skyline for a BASELINE config; CSVs in
+the reference's columns (write_sweep_csv / write_skyline_csv), latencies in ms.
+
+usage: python tools/skyline.py C3 --out profiles/r01 [--degrees 1 2 4 8] [--steps 3]
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2603_10353_b200 as P  # noqa: E402
+from paper_2603_10353_b200 import experiments as X  # noqa: E402
+from paper_2603_10353_b200.workload import LayerSpec, make_layer  # noqa: E402
+
+CONFIGS = {"C1": (32, 8, 8192), "C2": (32, 8, 32768), "C3": (32, 8, 131072), "C4": (28, 4, 65536),
+           "C5": (64, 8, 131072)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("config", choices=sorted(CONFIGS))
+    ap.add_argument("--out", default="gpurun_out")
+    ap.add_argument("--degrees", type=int, nargs="+", default=[1, 2, 4, 8])
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--calib-rows", type=int, default=16)
+    ap.add_argument("--skyline-devices", type=int, default=8)
+    a = ap.parse_args()
+    hq, hkv, n = CONFIGS[a.config]
+    q, k, v = make_layer(LayerSpec(num_q_heads=hq, num_kv_heads=hkv, seq_len=n, seed=2603), "cuda")
+    ctx = P.Context(0)
+    curves = ctx.profile_curves(q[:, n - a.calib_rows:, :].contiguous(), k, P.default_budget_grid(n, 128))
+    budgets = P.maxmin_allocate(curves, int(round(0.25 * hq * n)), quantum=128, floor=128).budgets
+    os.makedirs(a.out, exist_ok=True)
+    rows = X.measured_sweep(ctx, {n: (q, k, v, budgets)}, a.degrees, steps=a.steps)
+    X.write_sweep_csv(os.path.join(a.out, f"sweep_{a.config}.csv"), rows)
+    for r in rows:
+        print(json.dumps({"kind": "sweep", "config": a.config, **{k_: v_ for k_, v_ in r.__dict__.items()}}),
+              flush=True)
+    pts = X.measured_skyline(ctx, q, k, v, curves, devices=a.skyline_devices, steps=a.steps)
+    X.write_skyline_csv(os.path.join(a.out, f"skyline_{a.config}.csv"), pts)
+    for p in pts:
+        print(json.dumps({"kind": "skyline", "config": a.config, **p.__dict__}), flush=True)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main()
