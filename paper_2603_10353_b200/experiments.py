@@ -37,18 +37,24 @@ def format_double(v: float) -> str:
     return repr(float(v))
 
 
-def _time(fn, steps: int) -> float:
+def _time(fn, steps: int, repeats: int = 3) -> float:
+    """Median over `repeats` of the mean device time of `steps` back-to-back
+    calls (CUDA events), after 2 warm-up calls. The median keeps one
+    transient clock dip from being charged to one rank of a plan."""
     import torch
     for _ in range(2):
         fn()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        fn()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / steps
+    times = []
+    for _ in range(repeats):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / steps)
+    return float(np.median(times))
 
 
 def shard_latency_ms(ctx, q, k, v, shard, steps: int = 3, block_q: int = api.BLOCK_Q) -> float:
