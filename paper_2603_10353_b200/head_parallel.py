@@ -58,33 +58,79 @@ def head_counts(device_of_head, world: int) -> list:
     return [int((plan == r).sum()) for r in range(world)]
 
 
+@dataclass
+class GatherMap:
+    """Where every row of the all-gathered buffer goes. Rank r contributes a
+    buffer of `hmax` head slots (its heads in ascending order, padded); after
+    the all-gather slot r*hmax + i holds its i-th head. Whole heads move with
+    one index copy (src_slots -> dst_heads); heads a sub-head plan split
+    across ranks move as row ranges (slot, head, row0, row1)."""
+    hmax: int
+    num_heads: int
+    src_slots: np.ndarray
+    dst_heads: np.ndarray
+    partial: list
+
+
+def gather_map(plan, world: int, seq_len: int, block_q: int = 256) -> GatherMap:
+    """GatherMap of a whole-head plan (device_of_head array) or a sub-head
+    plan (api.split_assign result)."""
+    src, dst, partial = [], [], []
+    if isinstance(plan, np.ndarray) or isinstance(plan, (list, tuple)):
+        p = np.asarray(plan)
+        hmax = max(1, max(int((p == r).sum()) for r in range(world)))
+        for r in range(world):
+            heads = np.nonzero(p == r)[0]
+            src += [r * hmax + i for i in range(heads.size)]
+            dst += heads.tolist()
+        return GatherMap(hmax, int(p.size), np.asarray(src, np.int64), np.asarray(dst, np.int64), partial)
+    dev = np.asarray(plan.device)
+    hmax = max(1, max(int((dev == r).sum()) for r in range(world)))
+    nqb = -(-seq_len // block_q)
+    for r in range(world):
+        sel = np.nonzero(dev == r)[0]
+        segs = sorted((int(plan.head[i]), int(plan.qb_begin[i]), int(plan.qb_end[i])) for i in sel)
+        for i, (h, b0, b1) in enumerate(segs):
+            if b0 == 0 and b1 >= nqb:
+                src.append(r * hmax + i)
+                dst.append(h)
+            else:
+                partial.append((r * hmax + i, h, b0 * block_q, min(b1 * block_q, seq_len)))
+    return GatherMap(hmax, int(np.asarray(plan.head).max()) + 1, np.asarray(src, np.int64),
+                     np.asarray(dst, np.int64), partial)
+
+
+def apply_gather(recv, full, gm: GatherMap, src_t=None, dst_t=None) -> None:
+    """full[head rows] <- recv[slots] per the map (on the current stream).
+    src_t / dst_t: the index tensors already on recv's device (optional)."""
+    import torch
+    if gm.dst_heads.size:
+        s = src_t if src_t is not None else torch.as_tensor(gm.src_slots, device=recv.device)
+        d = dst_t if dst_t is not None else torch.as_tensor(gm.dst_heads, device=recv.device)
+        full.index_copy_(0, d, recv.index_select(0, s))
+    for slot, h, r0, r1 in gm.partial:
+        full[h, r0:r1].copy_(recv[slot, r0:r1])
+
+
+def _gather(local_out, gm: GatherMap, world: int, group=None):
+    import torch
+    import torch.distributed as dist
+    tail = tuple(local_out.shape[1:])
+    send = torch.zeros((gm.hmax,) + tail, dtype=local_out.dtype, device=local_out.device)
+    send[:local_out.shape[0]] = local_out
+    recv = torch.empty((world * gm.hmax,) + tail, dtype=local_out.dtype, device=local_out.device)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    full = torch.empty((gm.num_heads,) + tail, dtype=local_out.dtype, device=local_out.device)
+    apply_gather(recv, full, gm)
+    return full
+
+
 def gather_segments(local_out, split_plan, world: int, group=None, block_q: int = 256):
     """All-gather for a sub-head plan: rank r's local_out holds its heads
     (ordered like rank_segments(...).heads) with valid rows only inside each
     head's query-block range; returns [Hq, n, ...] with every row taken from
     the rank that computed it."""
-    import torch
-    import torch.distributed as dist
-    dev = np.asarray(split_plan.device)
-    counts = [int((dev == r).sum()) for r in range(world)]
-    hmax = max(counts)
-    hq = int(np.asarray(split_plan.head).max()) + 1
-    n = local_out.shape[1]
-    tail = tuple(local_out.shape[1:])
-    bq = block_q
-    send = torch.zeros((hmax,) + tail, dtype=local_out.dtype, device=local_out.device)
-    send[:local_out.shape[0]] = local_out
-    recv = torch.empty((world * hmax,) + tail, dtype=local_out.dtype, device=local_out.device)
-    dist.all_gather_into_tensor(recv, send, group=group)
-    full = torch.empty((hq,) + tail, dtype=local_out.dtype, device=local_out.device)
-    for r in range(world):
-        sel = np.nonzero(dev == r)[0]
-        order = np.argsort(np.asarray(split_plan.head)[sel], kind="stable")
-        for slot, i in enumerate(sel[order]):
-            h = int(split_plan.head[i])
-            r0, r1 = int(split_plan.qb_begin[i]) * bq, min(n, int(split_plan.qb_end[i]) * bq)
-            full[h, r0:r1] = recv[r * hmax + slot, r0:r1]
-    return full
+    return _gather(local_out, gather_map(split_plan, world, local_out.shape[1], block_q), world, group)
 
 
 def gather_heads(local_out, device_of_head, world: int, group=None):
@@ -93,19 +139,4 @@ def gather_heads(local_out, device_of_head, world: int, group=None):
     Every rank passes its own shard's outputs (rows ordered like
     RankShard.heads). Returns the full tensor on every rank.
     """
-    import torch
-    import torch.distributed as dist
-    plan = np.asarray(device_of_head)
-    counts = head_counts(plan, world)
-    hmax = max(counts)
-    tail = tuple(local_out.shape[1:])
-    send = torch.zeros((hmax,) + tail, dtype=local_out.dtype, device=local_out.device)
-    send[:local_out.shape[0]] = local_out
-    recv = torch.empty((world * hmax,) + tail, dtype=local_out.dtype, device=local_out.device)
-    dist.all_gather_into_tensor(recv, send, group=group)
-    full = torch.empty((plan.size,) + tail, dtype=local_out.dtype, device=local_out.device)
-    for r in range(world):
-        heads = np.nonzero(plan == r)[0]
-        if heads.size:
-            full[torch.as_tensor(heads, device=full.device)] = recv[r * hmax:r * hmax + heads.size]
-    return full
+    return _gather(local_out, gather_map(np.asarray(device_of_head), world, local_out.shape[1]), world, group)
