@@ -8,6 +8,7 @@ import json
 import os
 import sys
 
+import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -27,18 +28,33 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--calib-rows", type=int, default=16)
     ap.add_argument("--skyline-devices", type=int, default=8)
+    ap.add_argument("--requests", type=int, default=1,
+                    help="batched multi-request prefill: R independent requests stacked along the "
+                         "head axis (R*Hq balancer units; each request profiled and allocated on its own)")
+    ap.add_argument("--no-skyline", action="store_true")
     a = ap.parse_args()
     hq, hkv, n = CONFIGS[a.config]
-    q, k, v = make_layer(LayerSpec(num_q_heads=hq, num_kv_heads=hkv, seq_len=n, seed=2603), "cuda")
     ctx = P.Context(0)
-    curves = ctx.profile_curves(q[:, n - a.calib_rows:, :].contiguous(), k, P.default_budget_grid(n, 128))
-    budgets = P.maxmin_allocate(curves, int(round(0.25 * hq * n)), quantum=128, floor=128).budgets
+    qs, ks, vs, bs, cs = [], [], [], [], []
+    for r in range(a.requests):  # heads of request r are [r*hq, (r+1)*hq); GQA grouping is preserved
+        q, k, v = make_layer(LayerSpec(num_q_heads=hq, num_kv_heads=hkv, seq_len=n, seed=2603 + 104729 * r), "cuda")
+        curves = ctx.profile_curves(q[:, n - a.calib_rows:, :].contiguous(), k, P.default_budget_grid(n, 128))
+        bs.append(P.maxmin_allocate(curves, int(round(0.25 * hq * n)), quantum=128, floor=128).budgets)
+        qs.append(q), ks.append(k), vs.append(v), cs.extend(curves)
+    if a.requests > 1:
+        q, k, v = torch.cat(qs), torch.cat(ks), torch.cat(vs)
+        del qs, ks, vs
+    budgets = np.concatenate(bs)
+    tag = a.config if a.requests == 1 else f"{a.config}x{a.requests}"
     os.makedirs(a.out, exist_ok=True)
     rows = X.measured_sweep(ctx, {n: (q, k, v, budgets)}, a.degrees, steps=a.steps)
-    X.write_sweep_csv(os.path.join(a.out, f"sweep_{a.config}.csv"), rows)
+    X.write_sweep_csv(os.path.join(a.out, f"sweep_{tag}.csv"), rows)
     for r in rows:
-        print(json.dumps({"kind": "sweep", "config": a.config, **{k_: v_ for k_, v_ in r.__dict__.items()}}),
-              flush=True)
+        print(json.dumps({"kind": "sweep", "config": tag, "requests": a.requests,
+                          **{k_: v_ for k_, v_ in r.__dict__.items()}}), flush=True)
+    if a.no_skyline:
+        return
+    curves = cs
     pts = X.measured_skyline(ctx, q, k, v, curves, devices=a.skyline_devices, steps=a.steps)
     X.write_skyline_csv(os.path.join(a.out, f"skyline_{a.config}.csv"), pts)
     for p in pts:
