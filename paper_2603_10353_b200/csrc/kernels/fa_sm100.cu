@@ -73,25 +73,28 @@ constexpr int kEmuPairs = SHPLB_EMU_PAIRS;
 static_assert(kEmuPairs >= 0 && kEmuPairs <= 16, "SHPLB_EMU_PAIRS out of range");
 
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, 128, 0, 0);   // A=Q K-major, B=K K-major
-constexpr uint32_t kIdescQK64 = idesc_bf16_f32(128, 64, 0, 0);   // same, 64 keys of K
-#ifndef SHPLB_SPLIT_S
-#define SHPLB_SPLIT_S 0
+#ifndef SHPLB_WARP_ARRIVE
+#define SHPLB_WARP_ARRIVE 1
 #endif
-constexpr bool kSplitS = SHPLB_SPLIT_S != 0;  // S as two N=64 halves with separate commits
-#ifndef SHPLB_P_CHUNKS
-#define SHPLB_P_CHUNKS 1
-#endif
-// P handed to the MMA warp in this many pieces (1, 2 or 4 quarters of keys).
-constexpr int kPChunks = SHPLB_P_CHUNKS;
-static_assert(kPChunks == 1 || kPChunks == 2 || kPChunks == 4, "SHPLB_P_CHUNKS must be 1, 2 or 4");
+// P handoff arrivals: one elected lane per softmax warp (4 per half) after the
+// warp-collective tcgen05.wait::st, instead of all 128 threads.
+constexpr uint32_t kPArrivals = SHPLB_WARP_ARRIVE ? 4u : 128u;
+__device__ __forceinline__ void p_arrive(uint64_t* bar) {
+    if (SHPLB_WARP_ARRIVE) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+    } else {
+        mbar_arrive(bar);
+    }
+}
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, 128, 0, 1);  // A=P (TMEM), B=V MN-major
 
 struct __align__(8) Barriers {
     uint64_t q_full;
     uint64_t k_full[2], k_empty[2];
     uint64_t v_full[2], v_empty[2];
-    uint64_t s_full[2][2];  // per half, per 64-key column half: S of its next block is in TMEM
-    uint64_t p_full[2][4];  // per half, per 32-key quarter: P written (and O rescaled) -> PV may run
+    uint64_t s_full[2];   // per half: S of its next block is in TMEM
+    uint64_t p_full[2];   // per half: P written (and O rescaled) -> PV may run
     uint64_t pv_done[2];  // per half: its last issued PV has completed
     uint32_t tmem_base;
 };
@@ -133,6 +136,8 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Barriers* bar = reinterpret_cast<Barriers*>(smem + kSmemBar);
     int32_t* sel = reinterpret_cast<int32_t*>(smem + kSmemSel);
+    const uint32_t sSel = smem_u32(sel);
+    auto sel_at = [&](int j) { return lds_s32(sSel + 4u * static_cast<uint32_t>(j)); };
     const uint32_t sQ = smem_u32(smem + kSmemQ);
     const uint32_t sK = smem_u32(smem + kSmemK);
     const uint32_t sV = smem_u32(smem + kSmemV);
@@ -156,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
     auto active = [&](int hf, int j) -> bool {
         const int64_t first = row0 + hf * kBlock;
         if (hf >= halves || first >= p.n) return false;
-        return !p.causal || static_cast<int64_t>(sel[j]) * kBlock <= first + kBlock - 1;
+        return !p.causal || static_cast<int64_t>(sel_at(j)) * kBlock <= first + kBlock - 1;
     };
 
     if (threadIdx.x == 0) {
@@ -166,8 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
             mbar_init(&bar->k_empty[i], 1);
             mbar_init(&bar->v_full[i], 1);
             mbar_init(&bar->v_empty[i], 1);
-            for (int c = 0; c < 2; ++c) mbar_init(&bar->s_full[i][c], 1);
-            for (int c = 0; c < 4; ++c) mbar_init(&bar->p_full[i][c], 128);
+            mbar_init(&bar->s_full[i], 1);
+            mbar_init(&bar->p_full[i], kPArrivals);
             mbar_init(&bar->pv_done[i], 1);
         }
         fence_mbar_init();
@@ -194,8 +199,18 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
             for (int j = 0; j < nsel; ++j) {
                 const int st = j & 1;
                 const uint32_t ph = (j >> 1) & 1;
-                const int key0 = sel[j] * kBlock;
+                const int key0 = sel_at(j) * kBlock;
                 mbar_wait(&bar->k_empty[st], ph ^ 1);
+#ifdef SHPLB_DIAG_NO_KV_TMA  // dev-only diagnostic: K/V tiles loaded once, then reused (stale data)
+                if (j >= 2) {
+                    TRACE(j, 11, (threadIdx.x & 31) == 0);
+                    if ((threadIdx.x & 31) == 0) mbar_arrive(&bar->k_full[st]);
+                    mbar_wait(&bar->v_empty[st], ph ^ 1);
+                    TRACE(j, 12, (threadIdx.x & 31) == 0);
+                    if ((threadIdx.x & 31) == 0) mbar_arrive(&bar->v_full[st]);
+                    continue;
+                }
+#endif
                 tma_load_tile_warp(smem + kSmemK + st * kTileBytes, &p.tm_k, &bar->k_full[st],
                                    kTileBytes, key0, g);
                 TRACE(j, 11, (threadIdx.x & 31) == 0);
@@ -208,55 +223,39 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
       } else if (warp == 9) {
         // -------------------------------------------------------- MMA issuer
         if (nsel > 0) {
-            const uint64_t qdesc[2] = {umma_desc_sw128(sQ, 16, 1024), umma_desc_sw128(sQ + kTileBytes, 16, 1024)};
-            const uint64_t kdesc[2] = {umma_desc_sw128(sK, 16, 1024), umma_desc_sw128(sK + kTileBytes, 16, 1024)};
-            const uint64_t vdesc[2] = {umma_desc_sw128(sV, kChunkBytes, 1024),
-                                       umma_desc_sw128(sV + kTileBytes, kChunkBytes, 1024)};
+            // TMEM base re-read here (warp-uniform) so no register has to
+            // survive the setmaxnreg.dec above (it was spilled to the stack
+            // and reloaded before every MMA group).
+            const uint32_t tmem = __shfl_sync(0xffffffffu, static_cast<uint32_t>(lds_s32(smem_u32(&bar->tmem_base))), 0);
+            // Operand descriptors of stage / half s: the base descriptor plus the
+            // tile offset in the 16-byte start-address field (plain adds; an
+            // array indexed by j & 1 would live in local memory and put an
+            // LDL on the issue path).
+            const uint64_t qd0 = umma_desc_sw128(sQ, 16, 1024);
+            const uint64_t kd0 = umma_desc_sw128(sK, 16, 1024);
+            const uint64_t vd0 = umma_desc_sw128(sV, kChunkBytes, 1024);
+            constexpr uint64_t kTileDesc = kTileBytes >> 4;
+            auto qdesc = [&](int hf) { return qd0 + static_cast<uint64_t>(hf) * kTileDesc; };
+            auto kdesc = [&](int st) { return kd0 + static_cast<uint64_t>(st) * kTileDesc; };
+            auto vdesc = [&](int st) { return vd0 + static_cast<uint64_t>(st) * kTileDesc; };
             mbar_wait(&bar->q_full, 0);
             int done[2] = {0, 0};  // blocks each half has issued PV for
-            // S_hf = Q_hf K_j^T as two N = 64 products (keys 0-63, 64-127 of
-            // the block; K rows 64.. start 8 KB into each d chunk), each with
-            // its own commit, so the softmax loads and reduces the first 64
-            // columns while the tensor pipe computes the second.
-            auto issue_s = [&](int hf, int j) {
+            auto issue_s = [&](int hf, int j) {  // S_hf = Q_hf K_j^T
                 mbar_wait(&bar->k_full[j & 1], (j >> 1) & 1);
                 TRACE(j - 1, 9, hf == 0 && (threadIdx.x & 31) == 0);
                 tc_fence_after();
-                if (kSplitS) {
-                    for (int c = 0; c < 2; ++c) {
-                        mma_tile_ss_kmajor(tmem + col_s(hf) + 64u * c, qdesc[hf], kdesc[j & 1] + 512u * c,
-                                           kIdescQK64, 0u);
-                        mma_commit_warp(&bar->s_full[hf][c]);
-                    }
-                } else {
-                    mma_tile_ss_kmajor(tmem + col_s(hf), qdesc[hf], kdesc[j & 1], kIdescQK, 0u);
-                    TRACE(j - 1, hf == 0 ? 10 : 14, (threadIdx.x & 31) == 0);
-                    mma_commit_warp(&bar->s_full[hf][0]);
-                    mma_commit_warp(&bar->s_full[hf][1]);
-                }
+                mma_tile_ss_kmajor(tmem + col_s(hf), qdesc(hf), kdesc(j & 1), kIdescQK, 0u);
+                TRACE(j - 1, hf == 0 ? 10 : 14, (threadIdx.x & 31) == 0);
+                mma_commit_warp(&bar->s_full[hf]);
             };
-            // O_hf += P_hf V_j, in kPChunks pieces each issued as soon as the
-            // softmax has stored that piece of P.
-            auto issue_pv = [&](int hf, int j) {
+            auto issue_pv = [&](int hf, int j) {  // O_hf += P_hf V_j
                 mbar_wait(&bar->v_full[j & 1], (j >> 1) & 1);
                 TRACE(j, 6, hf == 0 && (threadIdx.x & 31) == 0);
-                if (kPChunks == 1) {
-                    mbar_wait(&bar->p_full[hf][0], done[hf] & 1);
-                    TRACE(j, 7, hf == 0 && (threadIdx.x & 31) == 0);
-                    tc_fence_after();
-                    mma_tile_ts_mnmajor(tmem + col_o(hf), tmem + col_s(hf), vdesc[j & 1], kIdescPV,
-                                        done[hf] > 0 ? 1u : 0u);
-                } else {
-                    for (int c = 0; c < 4; ++c) {
-                        if (c % (4 / kPChunks) == 0) {
-                            mbar_wait(&bar->p_full[hf][c / (4 / kPChunks)], done[hf] & 1);
-                            if (c == 0) TRACE(j, 7, hf == 0 && (threadIdx.x & 31) == 0);
-                            tc_fence_after();
-                        }
-                        mma_pair_ts_mnmajor(tmem + col_o(hf), tmem + col_s(hf) + 16u * c, vdesc[j & 1] + 256u * c,
-                                            kIdescPV, (done[hf] > 0 || c > 0) ? 1u : 0u);
-                    }
-                }
+                mbar_wait(&bar->p_full[hf], done[hf] & 1);
+                TRACE(j, 7, hf == 0 && (threadIdx.x & 31) == 0);
+                tc_fence_after();
+                mma_tile_ts_mnmajor(tmem + col_o(hf), tmem + col_s(hf), vdesc(j & 1), kIdescPV,
+                                    done[hf] > 0 ? 1u : 0u);
                 TRACE(j, hf == 0 ? 8 : 13, (threadIdx.x & 31) == 0);
                 mma_commit_warp(&bar->pv_done[hf]);
                 ++done[hf];
@@ -290,104 +289,113 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
         float m = -INFINITY;  // running max, log2 domain (stale by < 2^8)
         float l = 0.0f;       // running denominator relative to m
         int it = 0;           // blocks this half has processed
+        const float2 sc2 = make_float2(sl2, sl2);
+        // One 32-key quarter of P = 2^(S*scale_log2 - msub): packed-pair
+        // FFMA2 / MUFU ex2 (or, for kEmuPairs of every 16 pairs in unmasked
+        // blocks, the FMA-pipe polynomial) / FADD2 row sum, bf16 pairs stored
+        // back over S's first columns (tcgen05.st). With track, the raw row
+        // max of the quarter is folded into mx8 on the ALU pipe meanwhile.
+        auto exp_quarter = [&](const float* s, int c, float msub, bool emu_blk, float2 (&sum2)[2],
+                               float (&mx8)[8], bool track) {
+            const float2 nm2 = make_float2(-msub, -msub);
+            uint32_t pk[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const float a0 = s[c * 32 + 2 * e], a1 = s[c * 32 + 2 * e + 1];
+                if (track) {
+                    mx8[(2 * e) & 7] = fmaxf(mx8[(2 * e) & 7], a0);
+                    mx8[(2 * e + 1) & 7] = fmaxf(mx8[(2 * e + 1) & 7], a1);
+                }
+                const float2 x = ffma2(make_float2(a0, a1), sc2, nm2);
+                float2 pe;
+                if (emu_blk && ((e * kEmuPairs) & 15) < kEmuPairs) {
+                    pe = ex2_poly2(x);
+                } else {
+                    pe.x = ex2(x.x);
+                    pe.y = ex2(x.y);
+                }
+                sum2[e & 1] = fadd2(sum2[e & 1], pe);
+                pk[e] = pack_bf16x2(pe.x, pe.y);
+            }
+            tmem_st16(s_addr + c * 16, pk);
+        };
+        // O_hf *= alpha (this half's previous P.V must have completed).
+        auto rescale_o = [&](float alpha) {
+            mbar_wait(&bar->pv_done[hf], (it - 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < kHeadDim / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(o_addr + c * 32, v);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
+                tmem_st32(o_addr + c * 32, v);
+            }
+        };
         for (int j = 0; j < nsel; ++j) {
             if (!active(hf, j)) continue;
-            const int64_t key0 = static_cast<int64_t>(sel[j]) * kBlock;
-            // S arrives in two 64-column halves (separate commits): mask and
-            // reduce the first while the tensor pipe computes the second. Row
-            // max with 8 independent chains (ptxas fuses them into FMNMX3);
-            // keys past the query (causal) or past the sequence end are -inf.
+            const int64_t key0 = static_cast<int64_t>(sel_at(j)) * kBlock;
+            const bool need_mask = key0 + kBlock - 1 > lim;  // keys past the query / sequence end
             uint32_t sv[kBlock];
             float* s = reinterpret_cast<float*>(sv);
-            const bool need_mask = key0 + kBlock - 1 > lim;
-            float mx8[8];
-#pragma unroll
-            for (int hc = 0; hc < 2; ++hc) {
-                uint32_t(&ca)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[hc * 64]);
-                uint32_t(&cb)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[hc * 64 + 32]);
-                mbar_wait(&bar->s_full[hf][hc], it & 1);
-                tc_fence_after();
-                if (hc == 0) TRACE(j, 3 * hf + 0, r == 0);
-                tmem_ld32(s_addr + hc * 64, ca);
-                tmem_ld32(s_addr + hc * 64 + 32, cb);
-                tmem_wait_ld();
-                if (need_mask) {
-#pragma unroll
-                    for (int c = hc * 64; c < hc * 64 + 64; ++c)
-                        if (key0 + c > lim) s[c] = -INFINITY;
-                }
-#pragma unroll
-                for (int c = hc * 64; c < hc * 64 + 64; ++c) mx8[c & 7] = c < 8 ? s[c] : fmaxf(mx8[c & 7], s[c]);
-            }
-#ifdef SHPLB_DIAG_SKIP_SOFTMAX  // dev-only diagnostic: MMA/TMA pipeline alone
+            uint32_t(&lo0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[0]);
+            uint32_t(&lo1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[32]);
+            uint32_t(&hi0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[64]);
+            uint32_t(&hi1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&sv[96]);
+            mbar_wait(&bar->s_full[hf], it & 1);
+            tc_fence_after();
+            TRACE(j, 3 * hf + 0, r == 0);
+#ifdef SHPLB_DIAG_SKIP_ALL  // dev-only diagnostic: no TMEM reads either (pure MMA/TMA pipeline)
             tc_fence_before();
-            for (int c = 0; c < kPChunks; ++c) mbar_arrive(&bar->p_full[hf][c]);
+            p_arrive(&bar->p_full[hf]);
             ++it;
             continue;
 #endif
-            const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                                     fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-            const float mx = mraw * sl2;  // scale > 0 commutes with max
-            float alpha = 1.0f;
-            if (mx > m + kRescaleThreshold || (m == -INFINITY && mx > -INFINITY)) {
-                alpha = (m == -INFINITY) ? 0.0f : ex2(m - mx);
-                m = mx;
-            }
-            // Rescale O_hf (needs this half's previous PV complete) when the max moved.
-            if (it >= 1 && __any_sync(0xffffffffu, alpha != 1.0f)) {
-                mbar_wait(&bar->pv_done[hf], (it - 1) & 1);
-                tc_fence_after();
+            tmem_ld32(s_addr + 0, lo0);
+            tmem_ld32(s_addr + 32, lo1);
+            tmem_ld32(s_addr + 64, hi0);
+            tmem_ld32(s_addr + 96, hi1);
+            tmem_wait_ld();
+#ifdef SHPLB_DIAG_SKIP_SOFTMAX  // dev-only diagnostic: MMA/TMA pipeline alone
+            tc_fence_before();
+            p_arrive(&bar->p_full[hf]);
+            ++it;
+            continue;
+#endif
+            float mx8[8];
 #pragma unroll
-                for (int c = 0; c < kHeadDim / 32; ++c) {
-                    uint32_t v[32];
-                    tmem_ld32(o_addr + c * 32, v);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
-                    tmem_st32(o_addr + c * 32, v);
-                }
-            }
-            const float msub = (m == -INFINITY) ? 0.0f : m;
-            // x = s*scale_log2 - m and the row sum run on packed pairs
-            // (FFMA2/FADD2). With kPChunks > 1, P is handed to the MMA warp in
-            // pieces (p_full[hf][c]) so P.V can start while later keys are
-            // still being exponentiated; a piece's tcgen05.st is waited for
-            // only after the next quarter's exponentials are issued.
-            // Blocks with no masked lane in the warp may send kEmuPairs of
-            // every 16 pairs to the FMA-pipe polynomial instead of MUFU.
-            const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-msub, -msub);
+            for (int e = 0; e < 8; ++e) mx8[e] = -INFINITY;
             float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+            float alpha = 1.0f;
             const bool emu_blk = kEmuPairs > 0 && !__any_sync(0xffffffffu, need_mask);
-            TRACE(j, 3 * hf + 1, r == 0);
+            {
+                if (need_mask) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {  // four 32-key quarters -> 16 packed columns each
-                uint32_t pk[16];
+                    for (int c = 0; c < kBlock; ++c)
+                        if (key0 + c > lim) s[c] = -INFINITY;
+                }
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const float2 x = ffma2(make_float2(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]), sc2, nm2);
-                    float2 pe;
-                    if (emu_blk && ((e * kEmuPairs) & 15) < kEmuPairs) {
-                        pe = ex2_poly2(x);
-                    } else {
-                        pe.x = ex2(x.x);
-                        pe.y = ex2(x.y);
-                    }
-                    sum2[e & 1] = fadd2(sum2[e & 1], pe);
-                    pk[e] = pack_bf16x2(pe.x, pe.y);
+                for (int c = 0; c < kBlock; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
+                const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+                const float mx = mraw * sl2;
+                if (mx > m + kRescaleThreshold || (m == -INFINITY && mx > -INFINITY)) {
+                    alpha = (m == -INFINITY) ? 0.0f : ex2(m - mx);
+                    m = mx;
                 }
-                if (kPChunks > 1 && c > 0 && c % (4 / kPChunks) == 0) {
-                    tmem_wait_st();
-                    tc_fence_before();
-                    mbar_arrive(&bar->p_full[hf][c / (4 / kPChunks) - 1]);
-                }
-                tmem_st16(s_addr + c * 16, pk);
+                if (it >= 1 && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o(alpha);
+                const float msub = (m == -INFINITY) ? 0.0f : m;
+                TRACE(j, 3 * hf + 1, r == 0);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) exp_quarter(s, c, msub, emu_blk, sum2, mx8, false);
             }
             const float2 sum = fadd2(sum2[0], sum2[1]);
             l = l * alpha + (sum.x + sum.y);
             tmem_wait_st();
             TRACE(j, 3 * hf + 2, r == 0);
             tc_fence_before();
-            mbar_arrive(&bar->p_full[hf][kPChunks - 1]);
+            p_arrive(&bar->p_full[hf]);
             ++it;
         }
 

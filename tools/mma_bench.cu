@@ -20,11 +20,10 @@ using namespace shplb::ptx;
 __global__ void __launch_bounds__(256, 1) mma_kernel(int mode, int iters, unsigned long long* cycles) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tmem_base;
-    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ __align__(8) uint64_t bar[9];
     const int warp = warp_index_uniform();
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int i = 0; i < 9; ++i) mbar_init(&bar[i], (i == 4 || i == 5) ? 2 : 1);
         fence_mbar_init();
     }
     if (warp == 0) tmem_alloc<512>(&tmem_base);
@@ -41,6 +40,61 @@ __global__ void __launch_bounds__(256, 1) mma_kernel(int mode, int iters, unsign
         const uint64_t bd = umma_desc_sw128(b, 16, 1024);
         const uint64_t vd = umma_desc_sw128(b, 16384, 1024);
         const uint64_t ad0 = umma_desc_sw128(a0, 16, 1024), ad1 = umma_desc_sw128(a1, 16, 1024);
+        if (mode == 9 || mode == 10) {
+            // Kernel 3's skip-softmax chain: S_h done -> helper warps (2 per half)
+            // wait s_full[h], arrive p_full[h] -> issuer waits p_full[h] -> PV_h.
+            // bar[2+h] = s_full[h], bar[4+h] = p_full[h] (count 2). Mode 10: the
+            // issuer polls both halves and issues whichever is ready first.
+            const uint32_t id_ss = idesc_bf16_f32(128, 128, 0, 0), id_ts = idesc_bf16_f32(128, 128, 0, 1);
+            const int nblk = iters >> 5;
+            for (int hf = 0; hf < 2; ++hf) {
+                mma_tile_ss_kmajor(tmem + hf * 128, hf ? ad1 : ad0, bd, id_ss, 0u);
+                mma_commit_warp(&bar[2 + hf]);
+            }
+            for (int blk = 0; blk < nblk; ++blk) {
+                for (int hf = 0; hf < 2; ++hf) {
+                    mbar_wait(&bar[4 + hf], blk & 1);
+                    tc_fence_after();
+                    mma_tile_ts_mnmajor(tmem + 256 + hf * 128, tmem + hf * 128, vd, id_ts, 1u);
+                    if (blk + 1 < nblk) {
+                        mma_tile_ss_kmajor(tmem + hf * 128, hf ? ad1 : ad0, bd, id_ss, 0u);
+                        mma_commit_warp(&bar[2 + hf]);
+                    }
+                }
+            }
+            mma_commit_warp(&bar[0]);
+            mbar_wait(&bar[0], 0);
+            const long long t1 = clock64();
+            if ((threadIdx.x & 31) == 0) cycles[blockIdx.x] = static_cast<unsigned long long>(t1 - t0);
+            stop = 1;
+        } else if (mode >= 5) {
+            // Kernel 3's MMA stream: per key block PV_0 (TS into O_0), S_0 (SS into S_0),
+            // PV_1, S_1; mode 5 adds the kernel's commits (8 per block), mode 6
+            // only one per block, mode 7 = mode 5 with SS-only (S twice), mode 8 TS-only.
+            const uint32_t id_ss = idesc_bf16_f32(128, 128, 0, 0), id_ts = idesc_bf16_f32(128, 128, 0, 1);
+            for (int blk = 0; blk < (iters >> 5); ++blk) {
+                if (blk >= 2) mbar_wait(&bar[blk & 1], ((blk - 2) >> 1) & 1);
+                for (int hf = 0; hf < 2; ++hf) {
+                    if (mode == 7) mma_tile_ss_kmajor(tmem + 256 + hf * 128, hf ? ad1 : ad0, bd, id_ss, 1u);
+                    else mma_tile_ts_mnmajor(tmem + 256 + hf * 128, tmem + hf * 128, vd, id_ts, 1u);
+                    if (mode == 5 || mode == 7 || mode == 8) mma_commit_warp(&bar[2 + hf]);
+                    if (mode == 8) mma_tile_ts_mnmajor(tmem + hf * 128, tmem + 256 + hf * 128, vd, id_ts, 0u);
+                    else mma_tile_ss_kmajor(tmem + hf * 128, hf ? ad1 : ad0, bd, id_ss, 0u);
+                    if (mode == 5 || mode == 7 || mode == 8) {
+                        mma_commit_warp(&bar[4 + hf]);
+                        mma_commit_warp(&bar[6 + hf]);
+                    }
+                }
+                if (mode == 5 || mode == 7 || mode == 8) mma_commit_warp(&bar[8]);
+                mma_commit_warp(&bar[blk & 1]);
+            }
+            const int lastb = (iters >> 5) - 1;
+            mbar_wait(&bar[lastb & 1], (lastb >> 1) & 1);
+            if (lastb >= 1) mbar_wait(&bar[(lastb - 1) & 1], ((lastb - 1) >> 1) & 1);
+            const long long t1 = clock64();
+            if ((threadIdx.x & 31) == 0) cycles[blockIdx.x] = static_cast<unsigned long long>(t1 - t0);
+            stop = 1;
+        } else {
         for (int grp = 0; grp < (iters >> 3); ++grp) {  // 8 MMAs per group, committed to bar[grp & 1]
             if (grp >= 2) mbar_wait(&bar[grp & 1], ((grp - 2) >> 1) & 1);
             if (mode == 1) {
@@ -56,6 +110,17 @@ __global__ void __launch_bounds__(256, 1) mma_kernel(int mode, int iters, unsign
         const long long t1 = clock64();
         if ((threadIdx.x & 31) == 0) cycles[blockIdx.x] = static_cast<unsigned long long>(t1 - t0);
         stop = 1;
+        }
+    } else if ((mode == 9 || mode == 10) && warp >= 2 && warp <= 5) {
+        const int hf = (warp - 2) >> 1;
+        const int nblk = iters >> 5;
+        for (int blk = 0; blk < nblk; ++blk) {
+            mbar_wait(&bar[2 + hf], blk & 1);
+            tc_fence_after();
+            tc_fence_before();
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&bar[4 + hf]);
+        }
     } else if (mode == 4 && warp >= 2) {
         // Background smem writes (stand-in for TMA fills): 6 warps x 16 B stores.
         uint4* dst = reinterpret_cast<uint4*>(smem + 98304);
@@ -72,14 +137,16 @@ int main(int argc, char** argv) {
     unsigned long long* d;
     cudaMalloc(&d, 148 * sizeof(unsigned long long));
     cudaFuncSetAttribute(mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    const char* names[] = {"SS M128N128", "TS M128N128", "SS M128N256", "SS alt-A  ", "SS+stores  "};
+    const char* names[] = {"SS M128N128", "TS M128N128", "SS M128N256", "SS alt-A  ", "SS+stores  ",
+                           "K3 stream+commits", "K3 stream 1 commit", "SS-only+commits", "TS-only+commits",
+                           "K3 chain (skip)", "K3 chain dyn"};
     int clk = 0;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-    for (int mode = 0; mode < 5; ++mode) {
+    for (int mode = 0; mode < 10; ++mode) {
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
-        mma_kernel<<<148, 256, 200 * 1024>>>(mode, 1000, d);  // warm-up
+        mma_kernel<<<148, 256, 200 * 1024>>>(mode, 1024, d);  // warm-up
         cudaEventRecord(e0);
         mma_kernel<<<148, 256, 200 * 1024>>>(mode, iters, d);
         cudaEventRecord(e1);
@@ -96,6 +163,7 @@ int main(int argc, char** argv) {
         printf("%s  %8.1f TFLOP/s  %6.1f cycles/MMA (floor %d)  err=%s\n", names[mode],
                flops / (ms * 1e-3) / 1e12, avg / iters, mode == 2 ? 128 : 64,
                cudaGetErrorString(cudaGetLastError()));
+        fflush(stdout);
     }
     return 0;
 }

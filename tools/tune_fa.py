@@ -32,22 +32,31 @@ for _ in range(3):
     ctx.sparse_attention_layer(q, k, v, budgets, out=out, **kw)
 torch.cuda.synchronize()
 ctx.set_timing(True)
+import subprocess
+smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader,nounits",
+                        "-lms", "100"], stdout=subprocess.PIPE, text=True)
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
 e0.record()
 for _ in range(%(steps)d):
     ctx.sparse_attention_layer(q, k, v, budgets, out=out, **kw)
 e1.record()
 torch.cuda.synchronize()
+smi.terminate()
+vals = [l.split(",") for l in smi.communicate()[0].strip().splitlines() if "," in l]
+clk = sorted(float(a) for a, b in vals) if vals else [0.0]
+pw = sorted(float(b) for a, b in vals) if vals else [0.0]
 st = ctx.read_timing().mean(0)
 tiles, flops = P.layer_work(32, 8, n, budgets)
 print(json.dumps({"ms": e0.elapsed_time(e1) / %(steps)d, "k3_ms": st[2], "k2_ms": st[1],
-                  "k1_ms": st[0], "k3_tflops": flops / st[2] / 1e9}))
+                  "k1_ms": st[0], "k3_tflops": flops / st[2] / 1e9,
+                  "sm_mhz": clk[len(clk) // 2], "power_w": pw[len(pw) // 2],
+                  "k3_mcycles": st[2] * clk[len(clk) // 2] / 1e3}))
 """
 
 
 def main():
     n = int(os.environ.get("TUNE_N", "131072"))
-    steps = int(os.environ.get("TUNE_STEPS", "5"))
+    steps = int(os.environ.get("TUNE_STEPS", "10"))
     for spec in sys.argv[1:]:  # path[:block_q]
         lib, _, bq = spec.partition(":")
         env = dict(os.environ, SHPLB_LIB=os.path.abspath(lib))
