@@ -74,6 +74,9 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="target CPU time of the bounded reference sample")
+    p.add_argument("--gather", choices=["nccl", "p2p"], default="p2p",
+                   help="N>1 output reassembly: NCCL all-gather + reorder on a comm stream, or the "
+                        "fused gather (kernel 3 stores rows into every rank's buffer over NVLink)")
     p.add_argument("--force-gather", action="store_true",
                    help="validation: run the overlapped all-gather pipeline even at N=1 (1-rank NCCL group)")
     p.add_argument("--debug-one-device", action="store_true",
@@ -371,6 +374,58 @@ def time_stack_gathered(ctx, shards, plans, steps, warmup, world, stream):
     return max(allgather_float(e0.elapsed_time(e1) / (steps * n_l), world))
 
 
+def time_stack_p2p(ctx, shards, hq, steps, warmup, world, rank, stream):
+    """The stack with the fused gather: kernel 3 of every rank stores each output
+    row straight into every rank's full [Hq, n, d] buffer (CUDA IPC peer
+    pointers over NVLink), so a layer needs no all-gather or reorder — only a
+    cross-rank barrier (a 1-element NCCL all-reduce on a communication stream)
+    before its buffer set is reused two layers later. ms per layer, max over
+    ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_10353_b200.head_parallel import PeerOutputs
+    ref = next(ls.q for ls in shards if ls.heads)
+    po = PeerOutputs(hq, ref.shape[1], ref.shape[2], world, rank, ref.device, sets=2)
+    comm = torch.cuda.Stream()
+    flag = torch.zeros(1, device=ref.device)
+    done = [torch.cuda.Event() for _ in range(2)]
+    computed = [torch.cuda.Event() for _ in range(2)]
+
+    def one_step():
+        for l, ls in enumerate(shards):
+            b = l % 2
+            stream.wait_event(done[b])
+            if ls.heads:
+                ctx.sparse_attention_layer(ls.q, ls.k, ls.v, ls.budgets, causal=True, kv_map=ls.kv_map,
+                                           stream=stream, q_block_range=ls.ranges,
+                                           gather=(po.ptrs(b), ls.heads, hq))
+            computed[b].record(stream)
+            comm.wait_event(computed[b])
+            with torch.cuda.stream(comm):
+                if world > 1:
+                    dist.all_reduce(flag)
+            done[b].record(comm)
+        stream.wait_stream(comm)
+
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            one_step()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(steps):
+            one_step()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    po.close()
+    return max(allgather_float(e0.elapsed_time(e1) / (steps * len(shards)), world))
+
+
 def time_e2e(ctx, shards, steps, warmup, world, stream):
     """End to end through the reference-facing C-ABI call with HOST buffers
     (shplb_sparse_attention_layer_host): for every layer of `shards`, pinned
@@ -575,8 +630,20 @@ def main():
                    (float(p.loads.max() * world / p.loads.sum()) if name == "split"
                     else P.imbalance(b, p, world).imbalance) for b, p in zip(budgets_l, plans)]))}
         if (world > 1 or args.force_gather) and not DEBUG_GLOO:
-            res["ms_with_gather"] = time_stack_gathered(ctx, shards, plans, max(2, args.steps // 2),
-                                                        1, world, stream)
+            if args.gather == "p2p":
+                try:
+                    res["ms_with_gather"] = time_stack_p2p(ctx, shards, hq, max(2, args.steps // 2), 1, world,
+                                                           rank, stream)
+                    res["gather_kind"] = "p2p"
+                except P.ShplbError as e:  # IPC / peer access unavailable: NCCL all-gather instead
+                    torch.cuda.synchronize()
+                    res["gather_kind"] = f"nccl (fused p2p unavailable: {e})"
+                    res["ms_with_gather"] = time_stack_gathered(ctx, shards, plans, max(2, args.steps // 2),
+                                                                1, world, stream)
+            else:
+                res["gather_kind"] = "nccl"
+                res["ms_with_gather"] = time_stack_gathered(ctx, shards, plans, max(2, args.steps // 2),
+                                                            1, world, stream)
         if name == "greedy" and not args.no_e2e:
             e2e_ms, h2d, d2h = time_e2e(ctx, shards[:max(1, args.e2e_layers)], max(2, args.steps // 2), 1,
                                         world, stream)
@@ -666,7 +733,11 @@ def main():
                                  "plan": "sub-head balancer (shplb_plan_split), an extension "
                                          "beyond the reference's whole-head greedy_assign"}
         line["gather"] = ("every layer's [Hq, n, d] output all-gathered (NCCL) and head-reordered on a "
-                          "communication stream, overlapped with the next layer's compute")
+                          "communication stream, overlapped with the next layer's compute"
+                          if g.get("gather_kind", "nccl").startswith("nccl") else
+                          "fused: kernel 3 stores every output row into every rank's [Hq, n, d] buffer over "
+                          "NVLink (CUDA IPC peer pointers); one NCCL barrier per layer on a comm stream")
+        line["gather_kind"] = g.get("gather_kind")
         line["load_imbalance"] = round(g["load_imbalance"], 4)
     line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)

@@ -198,7 +198,27 @@ typedef struct {
      * are left untouched). NULL = every query block. Used by the sub-head
      * balancer (shplb_plan_split), which splits heavy heads across ranks. */
     const int32_t* q_block_range;
+    /* Optional fused output gather for head parallelism (NULL / 0 = off): device
+     * pointers of FULL outputs bf16 [out_heads_total][seq_len][head_dim] — this
+     * GPU's own and its peers' (mapped with shplb_ipc_open; NVLink P2P) — up to 8.
+     * Kernel 3's epilogue stores every output row of local q head h into each of
+     * them at global head out_head_of_q[h] (host int32 [num_q_heads]); `out` is
+     * not written and may be NULL. Rows outside a head's q_block_range are left
+     * untouched, so sub-head (split) plans reassemble without a reorder pass. The
+     * caller orders the ranks (a barrier after the call) before reading. */
+    void* const* out_peers;
+    int32_t n_out_peers;
+    const int32_t* out_head_of_q;
+    int32_t out_heads_total;
 } shplb_layer_shape;
+
+/* CUDA IPC for the fused gather: export a device allocation of this process as
+ * an opaque 64-byte handle, map a peer's handle into this process (P2P over
+ * NVLink), unmap it. (cudaIpcGetMemHandle / cudaIpcOpenMemHandle /
+ * cudaIpcCloseMemHandle; a handle cannot be opened in the process that made it.) */
+int shplb_ipc_handle(const void* dev_ptr, void* handle_out, size_t handle_bytes);
+int shplb_ipc_open(int device, const void* handle, size_t handle_bytes, void** dev_ptr_out);
+int shplb_ipc_close(int device, void* dev_ptr);
 
 /* Kernel 1 — block-importance estimator. Mean-pools q/k blocks (fp32,
  * fixed summation order) and scores pooled q.k * (1/sqrt(d)).

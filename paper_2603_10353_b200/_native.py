@@ -27,6 +27,7 @@ EXPORTS = (
     "shplb_sparse_attention_layer", "shplb_sparse_attention_layer_host", "shplb_dense_attention_layer",
     "shplb_last_selection", "shplb_copy_last_selection",
     "shplb_layer_work", "shplb_last_selection_work",
+    "shplb_ipc_handle", "shplb_ipc_open", "shplb_ipc_close",
 )
 
 SHPLB_OK = 0
@@ -84,6 +85,10 @@ class LayerShape(C.Structure):
         ("validate", C.c_int32),
         ("kv_head_of_q", C.c_void_p),
         ("q_block_range", C.c_void_p),
+        ("out_peers", C.c_void_p),
+        ("n_out_peers", C.c_int32),
+        ("out_head_of_q", C.c_void_p),
+        ("out_heads_total", C.c_int32),
     ]
 
 
@@ -149,6 +154,9 @@ def lib() -> C.CDLL:
     L.shplb_sparse_attention_layer.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp, vp]
     L.shplb_sparse_attention_layer_host.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp, vp]
     L.shplb_dense_attention_layer.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp]
+    L.shplb_ipc_handle.argtypes = [vp, vp, C.c_size_t]
+    L.shplb_ipc_open.argtypes = [C.c_int, vp, C.c_size_t, P(vp)]
+    L.shplb_ipc_close.argtypes = [C.c_int, vp]
     L.shplb_last_selection.argtypes = [vp, P(vp), P(vp), P(i64)]
     L.shplb_copy_last_selection.argtypes = [vp, vp, i64, vp, i64, vp]
     L.shplb_layer_work.argtypes = [P(LayerShape), vp, P(i64), P(f64)]

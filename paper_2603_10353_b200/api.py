@@ -223,9 +223,18 @@ def barrier(device_latency) -> SimulationResult:
 # ---------------------------------------------------------------------------
 
 def _shape(num_q_heads, num_kv_heads, seq_len, causal, validate=False, kv_map=None,
-           head_dim=HEAD_DIM, block_q=BLOCK_Q, q_block_range=None) -> LayerShape:
+           head_dim=HEAD_DIM, block_q=BLOCK_Q, q_block_range=None, gather=None) -> LayerShape:
     sh = LayerShape(num_q_heads, num_kv_heads, seq_len, head_dim, block_q, BLOCK, int(causal), 0,
-                    int(validate), None, None)
+                    int(validate), None, None, None, 0, None, 0)
+    if gather is not None:  # (output buffer device pointers, global head of each local q head, total heads)
+        ptrs, head_of_q, total = gather
+        arr = (C.c_void_p * len(ptrs))(*[int(x) for x in ptrs])
+        hq_ = _i32(head_of_q)
+        sh._gather_keepalive = (arr, hq_)
+        sh.out_peers = C.cast(arr, C.c_void_p)
+        sh.n_out_peers = len(ptrs)
+        sh.out_head_of_q = hq_.ctypes.data
+        sh.out_heads_total = int(total)
     if kv_map is not None:
         m = _i32(kv_map)
         sh._kv_map_keepalive = m  # the C struct only borrows the pointer
@@ -360,22 +369,29 @@ class Context:
 
     # -- the layer: kernels 1+2 fused, then 3 -----------------------------
     def sparse_attention_layer(self, q, k, v, budgets_tokens, causal=True, stream=None, out=None,
-                               validate=False, kv_map=None, block_q=BLOCK_Q, q_block_range=None):
-        """sparse_attention for every head with its own token budget."""
+                               validate=False, kv_map=None, block_q=BLOCK_Q, q_block_range=None,
+                               gather=None):
+        """sparse_attention for every head with its own token budget. gather =
+        (device pointers of full output buffers, global head index of each local
+        q head, total heads): kernel 3 writes every output row into each buffer
+        (fused head-parallel gather over NVLink peer memory); `out` is unused."""
         import torch
         hq, n, d = q.shape
-        if out is None:
-            out = torch.empty_like(q)
         b = _i64(budgets_tokens)
         if b.size != hq:
             from ._native import InvalidArgument
             raise InvalidArgument(f"need one budget per query head ({hq}), got {b.size}")
-        sh = _shape(hq, k.shape[0], n, causal, validate, kv_map, d, block_q, q_block_range)
+        sh = _shape(hq, k.shape[0], n, causal, validate, kv_map, d, block_q, q_block_range, gather)
         self._last_block_q = block_q
+        if gather is not None:
+            out_ptr = None
+        else:
+            if out is None:
+                out = torch.empty_like(q)
+            out_ptr = _dev_ptr(out, "out", torch.bfloat16)
         check(lib().shplb_sparse_attention_layer(
             self._h, C.byref(sh), _dev_ptr(q, "q", torch.bfloat16), _dev_ptr(k, "k", torch.bfloat16),
-            _dev_ptr(v, "v", torch.bfloat16), _ptr(b), _dev_ptr(out, "out", torch.bfloat16),
-            _stream_ptr(stream)))
+            _dev_ptr(v, "v", torch.bfloat16), _ptr(b), out_ptr, _stream_ptr(stream)))
         return out
 
     def dense_attention_layer(self, q, k, v, causal=True, stream=None, out=None, validate=False,

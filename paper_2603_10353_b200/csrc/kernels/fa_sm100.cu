@@ -50,7 +50,13 @@ namespace {
 
 using namespace shplb::ptx;
 
-constexpr int kThreads = 384;  // 3 warpgroups
+#ifndef SHPLB_THREADS
+#define SHPLB_THREADS 384
+#endif
+// 384: 3 warpgroups, registers rebalanced with setmaxnreg (softmax 216 / control 72).
+// 320: 10 warps (no idle warps), no setmaxnreg; every thread gets the 200-register launch grant.
+constexpr int kThreads = SHPLB_THREADS;
+constexpr bool kRebalance = kThreads == 384;
 // Register split. The CTA is granted 384 x 168 registers at launch (65536/384
 // rounded down to a multiple of 8); setmaxnreg.inc blocks until the pool can
 // cover it, so 2*softmax + control must not exceed 3*168 or the kernel hangs.
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
     const uint32_t tmem = bar->tmem_base;
 
     if (warp >= 8) {
-      setmaxnreg_dec<kRegsControl>();
+      if constexpr (kRebalance) setmaxnreg_dec<kRegsControl>();
       // The control warps run their loops with all 32 lanes (warp-uniform
       // control flow); one elected lane issues each TMA / MMA / commit inside
       // the same asm statement, so ptxas emits plain uniform-datapath issue.
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
         }
       }
     } else {
-        setmaxnreg_inc<kRegsSoftmax>();
+        if constexpr (kRebalance) setmaxnreg_inc<kRegsSoftmax>();
         // ------------------------------------------------ softmax warpgroups
         const int hf = warp >> 2;             // query half
         const int r = threadIdx.x & 127;      // row within the half == TMEM lane
@@ -400,9 +406,22 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
         }
 
         // -------------------------------------------------------- epilogue
-        // Row i of this half: O_hf / l (zero when no kept key was visible).
-        const bool live = hf < halves && qrow < p.n;
-        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) + (static_cast<int64_t>(h) * p.n + qrow) * kHeadDim;
+        // Row i of this half: O_hf / l (zero when no kept key was visible),
+        // stored to `out`, or — fused gather — to every listed output buffer
+        // at the head's global index (peer buffers are written over NVLink).
+        // (The head / row are re-derived from the work list here rather than kept
+        // live across the block loop, which is register-bound.)
+        const int32_t tile_e = p.tiles[blockIdx.x];
+        const int h_e = tile_e >> 20;
+        const int64_t qrow_e = static_cast<int64_t>(tile_e & 0xFFFFF) * p.bq + hf * kBlock + r;
+        const bool live = hf < halves && qrow_e < p.n;
+        const int ndst = p.n_out_peers > 0 ? p.n_out_peers : 1;
+        auto dst_row = [&](int i) -> __nv_bfloat16* {
+            if (p.n_out_peers == 0)
+                return static_cast<__nv_bfloat16*>(p.out) + (static_cast<int64_t>(h_e) * p.n + qrow_e) * kHeadDim;
+            return static_cast<__nv_bfloat16*>(p.out_peers[i]) +
+                   (static_cast<int64_t>(p.heads.k[h_e]) * p.n + qrow_e) * kHeadDim;
+        };
         if (it > 0) {
             mbar_wait(&bar->pv_done[hf], (it - 1) & 1);
             tc_fence_after();
@@ -413,21 +432,33 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
                 tmem_ld32(o_addr + c * 32, v);
                 tmem_wait_ld();
                 if (live) {
+                    uint4 w[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        uint4 w;
-                        w.x = pack_bf16x2(__uint_as_float(v[u * 8 + 0]) * inv, __uint_as_float(v[u * 8 + 1]) * inv);
-                        w.y = pack_bf16x2(__uint_as_float(v[u * 8 + 2]) * inv, __uint_as_float(v[u * 8 + 3]) * inv);
-                        w.z = pack_bf16x2(__uint_as_float(v[u * 8 + 4]) * inv, __uint_as_float(v[u * 8 + 5]) * inv);
-                        w.w = pack_bf16x2(__uint_as_float(v[u * 8 + 6]) * inv, __uint_as_float(v[u * 8 + 7]) * inv);
-                        *reinterpret_cast<uint4*>(out + c * 32 + u * 8) = w;
+                        w[u].x = pack_bf16x2(__uint_as_float(v[u * 8 + 0]) * inv, __uint_as_float(v[u * 8 + 1]) * inv);
+                        w[u].y = pack_bf16x2(__uint_as_float(v[u * 8 + 2]) * inv, __uint_as_float(v[u * 8 + 3]) * inv);
+                        w[u].z = pack_bf16x2(__uint_as_float(v[u * 8 + 4]) * inv, __uint_as_float(v[u * 8 + 5]) * inv);
+                        w[u].w = pack_bf16x2(__uint_as_float(v[u * 8 + 6]) * inv, __uint_as_float(v[u * 8 + 7]) * inv);
+                    }
+#pragma unroll 1
+                    for (int i = 0; i < ndst; ++i) {
+                        __nv_bfloat16* out = dst_row(i);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(out + c * 32 + u * 8) = w[u];
                     }
                 }
             }
         } else if (live) {
+#pragma unroll 1
+            for (int i = 0; i < ndst; ++i) {
+                __nv_bfloat16* out = dst_row(i);
 #pragma unroll
-            for (int u = 0; u < kHeadDim / 8; ++u) *reinterpret_cast<uint4*>(out + u * 8) = make_uint4(0, 0, 0, 0);
+                for (int u = 0; u < kHeadDim / 8; ++u) *reinterpret_cast<uint4*>(out + u * 8) = make_uint4(0, 0, 0, 0);
+            }
         }
+        // Peer stores: make them visible system-wide before the kernel retires
+        // (the caller's cross-rank barrier follows the kernel on its stream).
+        if (p.n_out_peers > 1) __threadfence_system();
     }
 
     tc_fence_before();

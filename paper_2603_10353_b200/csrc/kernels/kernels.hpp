@@ -13,6 +13,7 @@ constexpr int kBlock = 128;     // bq = bk
 constexpr int kPoolSplit = 16;  // interleaved row groups of the pooled sum
 constexpr int kMaxHeads = 256;  // per-launch k-block table lives in the kernel parameters
 constexpr int kMaxSelected = 2048;  // selected key blocks per query tile staged in smem (256K tokens)
+constexpr int kMaxPeers = 8;        // output buffers kernel 3 can write each row to (fused gather)
 
 // Per-q-head table passed in kernel parameters.
 struct HeadTable {
@@ -53,7 +54,12 @@ struct FaParams {
     int32_t bq;  // query block rows: 256 (two 128-row halves share each K/V tile) or 128
     int32_t causal;
     float scale_log2;  // (1/sqrt(d)) * log2(e)
-    HeadTable heads;   // kv head of each q head (k unused)
+    HeadTable heads;   // kv head of each q head; k = global output head index (fused gather)
+    // Fused output gather: with n_out_peers > 0 every output row of local head h
+    // is stored to out_peers[i] + (heads.k[h] * n + row) * 128 for every i (this
+    // GPU's full output and its peers' over NVLink) instead of to `out`.
+    void* out_peers[kMaxPeers];
+    int32_t n_out_peers;
 };
 void launch_fa(const FaParams& p, int num_tiles, cudaStream_t s);
 

@@ -116,7 +116,25 @@ void check_shape(const shplb_layer_shape* s) {
         throw NotSupported("block sizes must be block_q in {128, 256}, block_k = 128");
     if (s->kind != SHPLB_BLOCK_TOPK) throw NotSupported("selection kind not supported");
     if (s->seq_len > (int64_t(1) << 26)) throw NotSupported("seq_len too large");
+    if (s->out_peers && s->n_out_peers > 0) {  // fused output gather
+        if (s->n_out_peers > kern::kMaxPeers)
+            throw NotSupported("at most " + std::to_string(kern::kMaxPeers) + " output buffers per call");
+        if (!s->out_head_of_q) throw InvalidArgument("out_head_of_q is null");
+        for (int i = 0; i < s->n_out_peers; ++i) {
+            if (!s->out_peers[i] || reinterpret_cast<uintptr_t>(s->out_peers[i]) % 16 != 0)
+                throw InvalidArgument("out_peers[" + std::to_string(i) + "] must be a 16-byte aligned device pointer");
+        }
+        for (int h = 0; h < s->num_q_heads; ++h) {
+            const int gh = s->out_head_of_q[h];
+            if (gh < 0 || gh >= s->out_heads_total) {
+                throw InvalidArgument("head " + std::to_string(h) + ": output head " + std::to_string(gh) +
+                                      " out of range [0, " + std::to_string(s->out_heads_total) + ")");
+            }
+        }
+    }
 }
+
+bool fused_gather(const shplb_layer_shape* s) { return s->out_peers != nullptr && s->n_out_peers > 0; }
 
 void check_ptr(const void* p, const char* what) {
     if (!p) throw InvalidArgument(std::string(what) + " is null");
@@ -354,6 +372,11 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     p.bq = s->block_q;
     p.causal = s->causal;
     fill_kv_map(s, p.heads);
+    if (fused_gather(s)) {  // validated by check_shape
+        for (int i = 0; i < s->n_out_peers; ++i) p.out_peers[i] = s->out_peers[i];
+        for (int h = 0; h < s->num_q_heads; ++h) p.heads.k[h] = s->out_head_of_q[h];
+        p.n_out_peers = s->n_out_peers;
+    }
     p.scale_log2 = static_cast<float>((1.0 / std::sqrt(static_cast<double>(s->head_dim))) * 1.4426950408889634);
     if (ctx->current->num_tiles > 0) kern::launch_fa(p, ctx->current->num_tiles, st);
     check_launch(ctx);
@@ -499,7 +522,7 @@ int shplb_block_sparse_attention(shplb_ctx* ctx, const shplb_layer_shape* shape,
         check_ptr(q, "q");
         check_ptr(k, "k");
         check_ptr(v, "v");
-        check_ptr(out, "out");
+        if (!fused_gather(shape)) check_ptr(out, "out");
         require(idx && cnt && kmax >= 1, "null selection or kmax < 1");
         DeviceGuard g(ctx->device);
         auto st = static_cast<cudaStream_t>(stream);
@@ -520,7 +543,7 @@ int shplb_sparse_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape,
         check_ptr(q, "q");
         check_ptr(k, "k");
         check_ptr(v, "v");
-        check_ptr(out, "out");
+        if (!fused_gather(shape)) check_ptr(out, "out");
         std::vector<int32_t> kbl;
         const kern::HeadTable kb = budgets_to_blocks(shape, budgets_tokens, kbl);
         const int64_t kmax = *std::max_element(kbl.begin(), kbl.end());
@@ -551,7 +574,7 @@ int shplb_dense_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, 
         check_ptr(q, "q");
         check_ptr(k, "k");
         check_ptr(v, "v");
-        check_ptr(out, "out");
+        if (!fused_gather(shape)) check_ptr(out, "out");
         kern::HeadTable ht{};
         fill_kv_map(shape, ht);
         DeviceGuard g(ctx->device);
@@ -586,6 +609,7 @@ int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* s
         require(ctx != nullptr, "ctx is null");
         check_shape(shape);
         require(q_host && k_host && v_host && out_host, "null host buffer");
+        if (fused_gather(shape)) throw NotSupported("the host-buffer entry does not take a fused output gather");
         const size_t qb = sizeof(uint16_t) * shape->num_q_heads * shape->seq_len * shape->head_dim;
         const size_t kb = sizeof(uint16_t) * shape->num_kv_heads * shape->seq_len * shape->head_dim;
         const size_t al = 256;
@@ -805,6 +829,34 @@ int shplb_profile_curves(shplb_ctx* ctx, const void* q_rows, const void* k, int3
         SHPLB_CUDA(cudaMemcpyAsync(recovery_out, recovery_dev, sizeof(double) * num_q_heads * n_grid,
                                    cudaMemcpyDeviceToHost, st));
         SHPLB_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int shplb_ipc_handle(const void* dev_ptr, void* handle_out, size_t handle_bytes) {
+    return guarded([&] {
+        require(dev_ptr && handle_out, "null pointer");
+        require(handle_bytes >= sizeof(cudaIpcMemHandle_t), "handle buffer must hold 64 bytes");
+        cudaIpcMemHandle_t hnd;
+        SHPLB_CUDA(cudaIpcGetMemHandle(&hnd, const_cast<void*>(dev_ptr)));
+        std::memcpy(handle_out, &hnd, sizeof hnd);
+    });
+}
+
+int shplb_ipc_open(int device, const void* handle, size_t handle_bytes, void** dev_ptr_out) {
+    return guarded([&] {
+        require(handle && dev_ptr_out, "null pointer");
+        require(handle_bytes >= sizeof(cudaIpcMemHandle_t), "handle must be 64 bytes");
+        DeviceGuard g(device);
+        cudaIpcMemHandle_t hnd;
+        std::memcpy(&hnd, handle, sizeof hnd);
+        SHPLB_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, hnd, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int shplb_ipc_close(int device, void* dev_ptr) {
+    return guarded([&] {
+        DeviceGuard g(device);
+        SHPLB_CUDA(cudaIpcCloseMemHandle(dev_ptr));
     });
 }
 

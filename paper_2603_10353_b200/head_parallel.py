@@ -140,3 +140,57 @@ def gather_heads(local_out, device_of_head, world: int, group=None):
     RankShard.heads). Returns the full tensor on every rank.
     """
     return _gather(local_out, gather_map(np.asarray(device_of_head), world, local_out.shape[1]), world, group)
+
+
+class PeerOutputs:
+    """Full-layer output buffers [Hq, n, d] on every rank, mapped into every
+    other rank (CUDA IPC over NVLink) for the fused gather: kernel 3 stores each
+    output row straight into every rank's buffer (shplb_layer_shape.out_peers),
+    so reassembly needs no all-gather and no reorder, only a barrier.
+
+    `sets` buffers per rank alternate between layers. ptrs(b) lists the device
+    pointers of set b as seen from this rank, own buffer first.
+    """
+
+    def __init__(self, num_heads: int, seq_len: int, head_dim: int, world: int, rank: int, device,
+                 sets: int = 2, group=None):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from ._native import check, lib
+        self.world, self.rank, self.device = world, rank, torch.device(device)
+        self.local = [torch.empty((num_heads, seq_len, head_dim), dtype=torch.bfloat16, device=self.device)
+                      for _ in range(sets)]
+        self._opened = []
+        self._ptrs = []
+        for t in self.local:
+            hnd = (C.c_char * 64)()
+            check(lib().shplb_ipc_handle(C.c_void_p(t.data_ptr()), hnd, 64))
+            handles = [None] * world
+            if world > 1:
+                dist.all_gather_object(handles, bytes(hnd), group=group)
+            else:
+                handles = [bytes(hnd)]
+            ptrs = [t.data_ptr()]
+            for r in range(world):
+                if r == rank:
+                    continue
+                out = C.c_void_p()
+                buf = (C.c_char * 64).from_buffer_copy(handles[r])
+                check(lib().shplb_ipc_open(self.device.index or 0, buf, 64, C.byref(out)))
+                self._opened.append(out.value)
+                ptrs.append(out.value)
+            self._ptrs.append(ptrs)
+
+    def ptrs(self, b: int) -> list:
+        return self._ptrs[b % len(self._ptrs)]
+
+    def close(self) -> None:
+        import ctypes as C
+
+        from ._native import lib
+        for p in self._opened:
+            lib().shplb_ipc_close(self.device.index or 0, C.c_void_p(p))
+        self._opened = []
