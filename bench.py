@@ -70,6 +70,9 @@ def parse_args():
                    help="budget table from an allocation.json (reference format) instead of profiling")
     p.add_argument("--assignment-json", default=None,
                    help="S-HPLB head plan from an assignment.json (reference format) instead of greedy_assign")
+    p.add_argument("--project-degrees", type=int, nargs="*", default=[2, 4, 8],
+                   help="N=1 only: time every rank's shard of layer 0 under the naive / greedy / split "
+                        "plans for these GPU counts on this GPU (per-rank compute of a D-GPU run)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0,
@@ -653,6 +656,15 @@ def main():
         torch.cuda.empty_cache()
 
     q, k, v = layers[0]
+    projection = None
+    if world == 1 and args.project_degrees:
+        from paper_2603_10353_b200 import experiments as X
+        rows = X.measured_sweep(ctx, {n: (q, k, v, budgets)}, args.project_degrees, steps=2)
+        projection = {}
+        for r in rows:
+            projection.setdefault(str(r.degree), {})[r.assigner] = {
+                "barrier_ms": round(r.barrier_latency, 3), "bubble": round(r.bubble_fraction, 4),
+                "speedup_vs_naive": round(r.speedup_vs_naive, 4)}
     g = results["greedy"]
     flops_total = g["flops_total"]
     cpu = None
@@ -739,6 +751,13 @@ def main():
                           "NVLink (CUDA IPC peer pointers); one NCCL barrier per layer on a comm stream")
         line["gather_kind"] = g.get("gather_kind")
         line["load_imbalance"] = round(g["load_imbalance"], 4)
+    if projection:
+        line["per_rank_projection"] = {
+            "what": ("layer 0: every rank's shard timed in turn on this GPU (CUDA events, median of 3); "
+                     "barrier = max over ranks, bubble = 1 - mean/max (simulator.cpp:40-44); "
+                     "naive = even head parallelism, greedy = S-HPLB greedy_assign, split = sub-head "
+                     "balancer; gathers excluded"),
+            "degrees": projection}
     line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
 
