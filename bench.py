@@ -64,7 +64,7 @@ def parse_args():
     p.add_argument("--layers", type=int, default=32,
                    help="distinct attention layers per step (C3: the 32-layer stack); each has its "
                         "own inputs, budget table and head plan")
-    p.add_argument("--e2e-layers", type=int, default=2,
+    p.add_argument("--e2e-layers", type=int, default=4,
                    help="layers timed through the host-buffer entry for e2e (ms/layer)")
     p.add_argument("--allocation-json", default=None,
                    help="budget table from an allocation.json (reference format) instead of profiling")
@@ -439,10 +439,13 @@ def time_e2e(ctx, shards, steps, warmup, world, stream):
     host = [tuple(t.cpu().pin_memory() for t in (ls.q, ls.k, ls.v)) for ls in shards]
     host_out = torch.empty(shards[0].q.shape, dtype=shards[0].q.dtype, pin_memory=True)
 
-    def step():
-        for ls, (hq_, hk_, hv_) in zip(shards, host):
-            ctx.sparse_attention_layer_host(hq_, hk_, hv_, ls.budgets, causal=True, out=host_out,
-                                            stream=stream, kv_map=ls.kv_map)
+    outs = [host_out] + [torch.empty_like(host_out, pin_memory=True) for _ in shards[1:]]
+
+    def step():  # layer l+1's H2D overlaps layer l's kernels and D2H (async host entry)
+        for ls, (hq_, hk_, hv_), o in zip(shards, host, outs):
+            ctx.sparse_attention_layer_host(hq_, hk_, hv_, ls.budgets, causal=True, out=o,
+                                            stream=stream, kv_map=ls.kv_map, asynchronous=True)
+        stream.synchronize()
 
     for _ in range(warmup):
         step()

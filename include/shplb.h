@@ -274,6 +274,17 @@ int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* s
                                       const uint16_t* v_host, const int64_t* budgets_tokens,
                                       uint16_t* out_host, void* stream);
 
+/* The same host-buffer layer call without the final synchronisation: returns
+ * once the copies and kernels are queued; `stream` completes when the output is
+ * back in out_host. Consecutive async calls alternate between two device
+ * staging slots, so layer l+1's host->device copies overlap layer l's kernels
+ * and device->host copy (a multi-layer prefill hides the PCIe time). Host
+ * buffers must stay valid (pinned for async DMA) until the stream completes. */
+int shplb_sparse_attention_layer_host_async(shplb_ctx* ctx, const shplb_layer_shape* shape,
+                                            const uint16_t* q_host, const uint16_t* k_host,
+                                            const uint16_t* v_host, const int64_t* budgets_tokens,
+                                            uint16_t* out_host, void* stream);
+
 /* Device pointers of the selection made by the last shplb_sparse_attention_layer
  * call on this context (valid until the next call): idx [Hq][nqb][kmax],
  * cnt [Hq][nqb]. */

@@ -25,6 +25,7 @@ EXPORTS = (
     "shplb_ctx_set_timing", "shplb_ctx_read_timing",
     "shplb_block_scores", "shplb_select_blocks", "shplb_block_sparse_attention",
     "shplb_sparse_attention_layer", "shplb_sparse_attention_layer_host", "shplb_dense_attention_layer",
+    "shplb_sparse_attention_layer_host_async",
     "shplb_last_selection", "shplb_copy_last_selection",
     "shplb_layer_work", "shplb_last_selection_work",
     "shplb_ipc_handle", "shplb_ipc_open", "shplb_ipc_close",
@@ -154,6 +155,7 @@ def lib() -> C.CDLL:
     L.shplb_sparse_attention_layer.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp, vp]
     L.shplb_sparse_attention_layer_host.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp, vp]
     L.shplb_dense_attention_layer.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp]
+    L.shplb_sparse_attention_layer_host_async.argtypes = [vp, P(LayerShape), vp, vp, vp, vp, vp, vp]
     L.shplb_ipc_handle.argtypes = [vp, vp, C.c_size_t]
     L.shplb_ipc_open.argtypes = [C.c_int, vp, C.c_size_t, P(vp)]
     L.shplb_ipc_close.argtypes = [C.c_int, vp]

@@ -409,9 +409,13 @@ class Context:
         return out
 
     def sparse_attention_layer_host(self, q, k, v, budgets_tokens, causal=True, out=None,
-                                    stream=None, kv_map=None, block_q=BLOCK_Q, q_block_range=None):
+                                    stream=None, kv_map=None, block_q=BLOCK_Q, q_block_range=None,
+                                    asynchronous=False):
         """The layer call on HOST bf16 tensors (pinned for async DMA): copy in,
-        kernels 1-3, copy out, synchronise (shplb_sparse_attention_layer_host)."""
+        kernels 1-3, copy out, synchronise (shplb_sparse_attention_layer_host). With
+        asynchronous=True nothing is synchronised (shplb_sparse_attention_layer_host_async):
+        consecutive calls overlap one layer's copies with the previous layer's work;
+        `out` is valid once `stream` completes."""
         import torch
         for t, nm in ((q, "q"), (k, "k"), (v, "v")):
             if t.is_cuda or t.dtype != torch.bfloat16 or not t.is_contiguous():
@@ -423,7 +427,9 @@ class Context:
         b = _i64(budgets_tokens)
         sh = _shape(hq, k.shape[0], n, causal, False, kv_map, d, block_q, q_block_range)
         self._last_block_q = block_q
-        check(lib().shplb_sparse_attention_layer_host(
+        fn = (lib().shplb_sparse_attention_layer_host_async if asynchronous
+              else lib().shplb_sparse_attention_layer_host)
+        check(fn(
             self._h, C.byref(sh), C.c_void_p(q.data_ptr()), C.c_void_p(k.data_ptr()),
             C.c_void_p(v.data_ptr()), _ptr(b), C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
         return out

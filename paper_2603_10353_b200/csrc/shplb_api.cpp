@@ -195,6 +195,8 @@ struct shplb_ctx {
     void* host_io = nullptr;  // device staging for shplb_sparse_attention_layer_host
     cudaStream_t copy_in = nullptr, copy_out = nullptr;  // its H2D / D2H copy streams
     std::vector<cudaEvent_t> chunk_events;
+    int host_slot = 1;                          // staging slot of the last async host call
+    cudaEvent_t slot_done[2] = {nullptr, nullptr};  // slot's last user finished (kernels + D2H)
     size_t host_io_bytes = 0;
     // Dense comparator selection (shplb_dense_attention_layer), cached per key.
     int32_t* dense_idx = nullptr;
@@ -470,6 +472,8 @@ int shplb_ctx_destroy(shplb_ctx* ctx) {
         if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
         if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
         for (cudaEvent_t e : ctx->chunk_events) cudaEventDestroy(e);
+        for (cudaEvent_t e : ctx->slot_done)
+            if (e) cudaEventDestroy(e);
         delete ctx;
     });
 }
@@ -636,10 +640,14 @@ int shplb_dense_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, 
     });
 }
 
-int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* shape,
-                                      const uint16_t* q_host, const uint16_t* k_host,
-                                      const uint16_t* v_host, const int64_t* budgets_tokens,
-                                      uint16_t* out_host, void* stream) {
+namespace {
+// Host-buffer layer call. Synchronous: one staging slot, waits for earlier
+// work on `stream`, synchronises at the end. Asynchronous: staging alternates
+// between two slots, a call's copies wait only for the call two back (which
+// used the same slot), so layer l+1's H2D overlaps layer l's compute and D2H.
+int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q_host,
+               const uint16_t* k_host, const uint16_t* v_host, const int64_t* budgets_tokens,
+               uint16_t* out_host, void* stream, bool async_call) {
     int rc = SHPLB_OK;
     const int err = guarded([&] {
         require(ctx != nullptr, "ctx is null");
@@ -652,13 +660,19 @@ int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* s
         const size_t q_off = 0, k_off = (qb + al - 1) / al * al, v_off = k_off + (kb + al - 1) / al * al,
                      o_off = v_off + (kb + al - 1) / al * al, total = o_off + qb;
         DeviceGuard g(ctx->device);
-        if (total > ctx->host_io_bytes) {
-            if (ctx->host_io) SHPLB_CUDA(cudaFree(ctx->host_io));
+        const size_t slot_bytes = (total + al - 1) / al * al;
+        const size_t need = async_call ? 2 * slot_bytes : slot_bytes;
+        if (need > ctx->host_io_bytes) {
+            if (ctx->host_io) {
+                SHPLB_CUDA(cudaDeviceSynchronize());  // in-flight async calls may still use it
+                SHPLB_CUDA(cudaFree(ctx->host_io));
+            }
             ctx->host_io = nullptr;
-            SHPLB_CUDA(cudaMalloc(&ctx->host_io, total));
-            ctx->host_io_bytes = total;
+            SHPLB_CUDA(cudaMalloc(&ctx->host_io, need));
+            ctx->host_io_bytes = need;
         }
-        auto* base = static_cast<uint8_t*>(ctx->host_io);
+        const int slot = async_call ? (ctx->host_slot ^= 1) : 0;
+        auto* base = static_cast<uint8_t*>(ctx->host_io) + slot * slot_bytes;
         auto st = static_cast<cudaStream_t>(stream);
         // Pipeline by KV-head chunks (standard GQA grouping only): chunk c's
         // H2D copies on a copy stream overlap chunk c-1's kernels on the
@@ -688,10 +702,20 @@ int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* s
             SHPLB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
             ctx->chunk_events.push_back(e);
         }
-        cudaEvent_t start = ctx->chunk_events[0];
-        SHPLB_CUDA(cudaEventRecord(start, st));  // copies may not overtake earlier work on `st`
-        SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_in, start, 0));
-        SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_out, start, 0));
+        for (cudaEvent_t& e : ctx->slot_done) {
+            if (!e) SHPLB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        if (async_call) {
+            // The slot's previous user (two calls back) must have finished its
+            // kernels and its D2H before this call's H2D overwrites the slot.
+            SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_in, ctx->slot_done[slot], 0));
+            SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_out, ctx->slot_done[slot], 0));
+        } else {
+            cudaEvent_t start = ctx->chunk_events[0];
+            SHPLB_CUDA(cudaEventRecord(start, st));  // copies may not overtake earlier work on `st`
+            SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_in, start, 0));
+            SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_out, start, 0));
+        }
         const size_t row_bytes = sizeof(uint16_t) * shape->seq_len * shape->head_dim;  // one head
         for (int32_t c = 0; c < chunks; ++c) {
             const int32_t g0 = monotone ? hkv * c / chunks : 0, g1 = monotone ? hkv * (c + 1) / chunks : hkv;
@@ -729,9 +753,25 @@ int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* s
         cudaEvent_t out_done = ctx->chunk_events[3];
         SHPLB_CUDA(cudaEventRecord(out_done, ctx->copy_out));
         SHPLB_CUDA(cudaStreamWaitEvent(st, out_done, 0));  // `stream` completes after the last D2H
-        SHPLB_CUDA(cudaStreamSynchronize(st));
+        SHPLB_CUDA(cudaEventRecord(ctx->slot_done[slot], st));
+        if (!async_call) SHPLB_CUDA(cudaStreamSynchronize(st));
     });
     return rc != SHPLB_OK ? rc : err;
+}
+}  // namespace
+
+int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* shape,
+                                      const uint16_t* q_host, const uint16_t* k_host,
+                                      const uint16_t* v_host, const int64_t* budgets_tokens,
+                                      uint16_t* out_host, void* stream) {
+    return host_layer(ctx, shape, q_host, k_host, v_host, budgets_tokens, out_host, stream, false);
+}
+
+int shplb_sparse_attention_layer_host_async(shplb_ctx* ctx, const shplb_layer_shape* shape,
+                                            const uint16_t* q_host, const uint16_t* k_host,
+                                            const uint16_t* v_host, const int64_t* budgets_tokens,
+                                            uint16_t* out_host, void* stream) {
+    return host_layer(ctx, shape, q_host, k_host, v_host, budgets_tokens, out_host, stream, true);
 }
 
 int shplb_last_selection(const shplb_ctx* ctx, const int32_t** idx, const int32_t** cnt,

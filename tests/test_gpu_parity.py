@@ -277,3 +277,23 @@ def test_split_plan_shards_reassemble_the_layer(cuda_ctx, bq):
             got[h, r0:r1] = part[i, r0:r1]
     torch.cuda.synchronize()
     assert torch.equal(got, full)
+
+
+def test_async_host_entry_matches_sync_over_layers(cuda_ctx):
+    """shplb_sparse_attention_layer_host_async over several layers (two staging
+    slots alternate) gives the synchronous call's outputs."""
+    outs_sync, outs_async, inputs = [], [], []
+    for li in range(3):
+        q, k, v = make_layer(LayerSpec(num_q_heads=4, num_kv_heads=2, seq_len=777 + 256 * li, seed=40 + li), "cpu")
+        b = np.array([128, 384, 777, 256], np.int64)
+        hq_, hk_, hv_ = (t.contiguous().pin_memory() for t in (q, k, v))
+        inputs.append((hq_, hk_, hv_, b))
+        outs_sync.append(cuda_ctx.sparse_attention_layer_host(hq_, hk_, hv_, b).clone())
+    stream = torch.cuda.Stream()
+    for hq_, hk_, hv_, b in inputs:
+        o = torch.empty(hq_.shape, dtype=hq_.dtype, pin_memory=True)
+        outs_async.append(cuda_ctx.sparse_attention_layer_host(hq_, hk_, hv_, b, stream=stream, out=o,
+                                                               asynchronous=True))
+    stream.synchronize()
+    for a, s_ in zip(outs_async, outs_sync):
+        assert torch.equal(a, s_)
