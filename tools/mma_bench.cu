@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256, 1) mma_kernel(int mode, int iters, unsign
     tc_fence_after();
     const uint32_t tmem = tmem_base;
     const uint32_t a0 = smem_u32(smem), a1 = smem_u32(smem + 32768), b = smem_u32(smem + 65536);
-    const uint32_t n = (mode == 2) ? 256 : 128;
+    const uint32_t n = (mode == 2) ? 256 : (mode == 11 ? 64 : 128);
     const uint32_t idesc = idesc_bf16_f32(128, n, 0, mode == 1 ? 1 : 0);
     volatile int stop = 0;
     if (warp == 1) {  // whole warp, elected lane issues (warp-uniform control flow)
@@ -40,7 +40,19 @@ __global__ void __launch_bounds__(256, 1) mma_kernel(int mode, int iters, unsign
         const uint64_t bd = umma_desc_sw128(b, 16, 1024);
         const uint64_t vd = umma_desc_sw128(b, 16384, 1024);
         const uint64_t ad0 = umma_desc_sw128(a0, 16, 1024), ad1 = umma_desc_sw128(a1, 16, 1024);
-        if (mode == 9 || mode == 10) {
+        if (mode == 11) {
+            for (int grp = 0; grp < (iters >> 3); ++grp) {
+                if (grp >= 2) mbar_wait(&bar[grp & 1], ((grp - 2) >> 1) & 1);
+                mma_tile_ss_kmajor(tmem, ad0, bd, idesc, 1u);
+                mma_commit_warp(&bar[grp & 1]);
+            }
+            const int last = (iters >> 3) - 1;
+            mbar_wait(&bar[last & 1], (last >> 1) & 1);
+            if (last >= 1) mbar_wait(&bar[(last - 1) & 1], ((last - 1) >> 1) & 1);
+            const long long t1 = clock64();
+            if ((threadIdx.x & 31) == 0) cycles[blockIdx.x] = static_cast<unsigned long long>(t1 - t0);
+            stop = 1;
+        } else if (mode == 9 || mode == 10) {
             // Kernel 3's skip-softmax chain: S_h done -> helper warps (2 per half)
             // wait s_full[h], arrive p_full[h] -> issuer waits p_full[h] -> PV_h.
             // bar[2+h] = s_full[h], bar[4+h] = p_full[h] (count 2). Mode 10: the
@@ -139,10 +151,11 @@ int main(int argc, char** argv) {
     cudaFuncSetAttribute(mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const char* names[] = {"SS M128N128", "TS M128N128", "SS M128N256", "SS alt-A  ", "SS+stores  ",
                            "K3 stream+commits", "K3 stream 1 commit", "SS-only+commits", "TS-only+commits",
-                           "K3 chain (skip)", "K3 chain dyn"};
+                           "K3 chain (skip)", "K3 chain dyn", "SS M128N64"};
     int clk = 0;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-    for (int mode = 0; mode < 10; ++mode) {
+    for (int mode = 0; mode < 12; ++mode) {
+        if (mode == 10) continue;
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
@@ -158,7 +171,7 @@ int main(int argc, char** argv) {
         double avg = 0;
         for (int i = 0; i < 148; ++i) avg += h[i];
         avg /= 148;
-        const double n = mode == 2 ? 256 : 128;
+        const double n = mode == 2 ? 256 : (mode == 11 ? 64 : 128);
         const double flops = 2.0 * 128 * n * 16 * iters * 148;
         printf("%s  %8.1f TFLOP/s  %6.1f cycles/MMA (floor %d)  err=%s\n", names[mode],
                flops / (ms * 1e-3) / 1e12, avg / iters, mode == 2 ? 128 : 64,
