@@ -297,3 +297,15 @@ def test_async_host_entry_matches_sync_over_layers(cuda_ctx):
     stream.synchronize()
     for a, s_ in zip(outs_async, outs_sync):
         assert torch.equal(a, s_)
+
+
+def test_max_heads_per_call(cuda_ctx):
+    """256 q heads (kMaxHeads: the per-launch head table) in one call, against the
+    oracle; 257 is refused with NotSupported."""
+    spec = LayerSpec(num_q_heads=256, num_kv_heads=32, seq_len=384, seed=99)
+    kb = (np.arange(256) % 3) + 1
+    run_case(cuda_ctx, spec, kb, causal=True, bq=256)
+    q = torch.zeros((257, 128, 128), dtype=torch.bfloat16, device="cuda")
+    k = torch.zeros((1, 128, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(P.NotSupported, match="at most 256 query heads per call"):
+        cuda_ctx.sparse_attention_layer(q, k, k, np.full(257, 128, np.int64))
