@@ -212,10 +212,13 @@ typedef struct {
     int32_t out_heads_total;
 } shplb_layer_shape;
 
-/* CUDA IPC for the fused gather: export a device allocation of this process as
- * an opaque 64-byte handle, map a peer's handle into this process (P2P over
- * NVLink), unmap it. (cudaIpcGetMemHandle / cudaIpcOpenMemHandle /
- * cudaIpcCloseMemHandle; a handle cannot be opened in the process that made it.) */
+/* CUDA IPC for the fused gather: export a device pointer of this process as an
+ * opaque SHPLB_IPC_HANDLE_BYTES handle (the allocation's cudaIpcMemHandle_t plus
+ * the pointer's offset inside that allocation), map a peer's handle into this
+ * process (P2P over NVLink; returns the peer's pointer, offset applied), unmap
+ * it. A handle cannot be opened in the process that made it, and an allocation
+ * is opened at most once per process (export one buffer per rank). */
+#define SHPLB_IPC_HANDLE_BYTES 72
 int shplb_ipc_handle(const void* dev_ptr, void* handle_out, size_t handle_bytes);
 int shplb_ipc_open(int device, const void* handle, size_t handle_bytes, void** dev_ptr_out);
 int shplb_ipc_close(int device, void* dev_ptr);

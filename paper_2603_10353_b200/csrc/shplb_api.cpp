@@ -62,6 +62,27 @@ EncodeTiledFn encode_tiled() {
     return fn;
 }
 
+// cuMemGetAddressRange (driver API, resolved at run time like the tensor-map
+// encoder): base address of the allocation holding a device pointer.
+using AddressRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+uintptr_t allocation_base(const void* p) {
+    static AddressRangeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<AddressRangeFn>(f);
+    });
+    if (!fn) throw CudaError("cuMemGetAddressRange unavailable from the driver");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS)
+        throw CudaError("cuMemGetAddressRange failed");
+    return static_cast<uintptr_t>(base);
+}
+
 // [heads][n][128] bf16 as a 3-D tensor map with a {64, 128, 1} box and 128-byte
 // swizzle: one box is one 128-row x 128-byte UMMA K-major chunk. Rows past n
 // are zero-filled on load and clipped on store.
@@ -908,31 +929,41 @@ int shplb_profile_curves(shplb_ctx* ctx, const void* q_rows, const void* k, int3
     });
 }
 
+// IPC handle layout (SHPLB_IPC_HANDLE_BYTES = 72): the CUDA IPC handle of the
+// allocation holding dev_ptr, then dev_ptr's byte offset inside it (caching
+// allocators hand out pointers inside larger allocations).
 int shplb_ipc_handle(const void* dev_ptr, void* handle_out, size_t handle_bytes) {
     return guarded([&] {
         require(dev_ptr && handle_out, "null pointer");
-        require(handle_bytes >= sizeof(cudaIpcMemHandle_t), "handle buffer must hold 64 bytes");
+        require(handle_bytes >= SHPLB_IPC_HANDLE_BYTES, "handle buffer must hold 72 bytes");
         cudaIpcMemHandle_t hnd;
         SHPLB_CUDA(cudaIpcGetMemHandle(&hnd, const_cast<void*>(dev_ptr)));
-        std::memcpy(handle_out, &hnd, sizeof hnd);
+        const uint64_t off = reinterpret_cast<uintptr_t>(dev_ptr) - allocation_base(dev_ptr);
+        auto* out = static_cast<uint8_t*>(handle_out);
+        std::memcpy(out, &hnd, sizeof hnd);
+        std::memcpy(out + sizeof hnd, &off, sizeof off);
     });
 }
 
 int shplb_ipc_open(int device, const void* handle, size_t handle_bytes, void** dev_ptr_out) {
     return guarded([&] {
         require(handle && dev_ptr_out, "null pointer");
-        require(handle_bytes >= sizeof(cudaIpcMemHandle_t), "handle must be 64 bytes");
+        require(handle_bytes >= SHPLB_IPC_HANDLE_BYTES, "handle must be 72 bytes");
         DeviceGuard g(device);
         cudaIpcMemHandle_t hnd;
+        uint64_t off = 0;
         std::memcpy(&hnd, handle, sizeof hnd);
-        SHPLB_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, hnd, cudaIpcMemLazyEnablePeerAccess));
+        std::memcpy(&off, static_cast<const uint8_t*>(handle) + sizeof hnd, sizeof off);
+        void* base = nullptr;
+        SHPLB_CUDA(cudaIpcOpenMemHandle(&base, hnd, cudaIpcMemLazyEnablePeerAccess));
+        *dev_ptr_out = static_cast<uint8_t*>(base) + off;
     });
 }
 
 int shplb_ipc_close(int device, void* dev_ptr) {
     return guarded([&] {
         DeviceGuard g(device);
-        SHPLB_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+        SHPLB_CUDA(cudaIpcCloseMemHandle(reinterpret_cast<void*>(allocation_base(dev_ptr))));
     });
 }
 

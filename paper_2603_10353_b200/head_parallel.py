@@ -148,9 +148,12 @@ class PeerOutputs:
     output row straight into every rank's buffer (shplb_layer_shape.out_peers),
     so reassembly needs no all-gather and no reorder, only a barrier.
 
-    `sets` buffers per rank alternate between layers. ptrs(b) lists the device
-    pointers of set b as seen from this rank, own buffer first.
+    All `sets` buffers of a rank are one allocation (one IPC handle, opened
+    once per peer); ptrs(b) lists set b's device pointers as seen from this
+    rank, own buffer first, then the other ranks in rank order.
     """
+
+    HANDLE_BYTES = 72  # SHPLB_IPC_HANDLE_BYTES
 
     def __init__(self, num_heads: int, seq_len: int, head_dim: int, world: int, rank: int, device,
                  sets: int = 2, group=None):
@@ -161,28 +164,26 @@ class PeerOutputs:
 
         from ._native import check, lib
         self.world, self.rank, self.device = world, rank, torch.device(device)
-        self.local = [torch.empty((num_heads, seq_len, head_dim), dtype=torch.bfloat16, device=self.device)
-                      for _ in range(sets)]
-        self._opened = []
-        self._ptrs = []
-        for t in self.local:
-            hnd = (C.c_char * 64)()
-            check(lib().shplb_ipc_handle(C.c_void_p(t.data_ptr()), hnd, 64))
+        self.buffer = torch.empty((sets, num_heads, seq_len, head_dim), dtype=torch.bfloat16, device=self.device)
+        self.local = [self.buffer[b] for b in range(sets)]
+        set_bytes = num_heads * seq_len * head_dim * 2
+        hnd = (C.c_char * self.HANDLE_BYTES)()
+        check(lib().shplb_ipc_handle(C.c_void_p(self.buffer.data_ptr()), hnd, self.HANDLE_BYTES))
+        handles = [bytes(hnd)]
+        if world > 1:
             handles = [None] * world
-            if world > 1:
-                dist.all_gather_object(handles, bytes(hnd), group=group)
-            else:
-                handles = [bytes(hnd)]
-            ptrs = [t.data_ptr()]
-            for r in range(world):
-                if r == rank:
-                    continue
-                out = C.c_void_p()
-                buf = (C.c_char * 64).from_buffer_copy(handles[r])
-                check(lib().shplb_ipc_open(self.device.index or 0, buf, 64, C.byref(out)))
-                self._opened.append(out.value)
-                ptrs.append(out.value)
-            self._ptrs.append(ptrs)
+            dist.all_gather_object(handles, bytes(hnd), group=group)
+        bases = [self.buffer.data_ptr()]
+        self._opened = []
+        for r in range(world):
+            if r == rank:
+                continue
+            out = C.c_void_p()
+            buf = (C.c_char * self.HANDLE_BYTES).from_buffer_copy(handles[r])
+            check(lib().shplb_ipc_open(self.device.index or 0, buf, self.HANDLE_BYTES, C.byref(out)))
+            self._opened.append(out.value)
+            bases.append(out.value)
+        self._ptrs = [[base + b * set_bytes for base in bases] for b in range(sets)]
 
     def ptrs(self, b: int) -> list:
         return self._ptrs[b % len(self._ptrs)]

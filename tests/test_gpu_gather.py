@@ -73,3 +73,75 @@ def test_peer_outputs_single_rank(cuda_ctx):
     po = PeerOutputs(4, 512, 128, world=1, rank=0, device="cuda:0", sets=2)
     assert po.ptrs(0) == [po.local[0].data_ptr()] and po.ptrs(3) == [po.local[1].data_ptr()]
     po.close()
+
+
+def test_ipc_handle_carries_offset_inside_allocation(cuda_ctx):
+    import ctypes as C
+
+    from paper_2603_10353_b200._native import check, lib
+    big = torch.empty(1 << 20, dtype=torch.bfloat16, device="cuda")
+    sub = big[4096:]
+    offs = []
+    for t in (big, sub):
+        h = (C.c_char * 72)()
+        check(lib().shplb_ipc_handle(C.c_void_p(t.data_ptr()), h, 72))
+        offs.append(int.from_bytes(bytes(h)[64:72], "little"))
+    assert offs[1] - offs[0] == 4096 * 2
+
+
+def _two_rank_worker(rank, port, result):
+    import os
+
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        torch.cuda.set_device(0)
+        ctx = P.Context(0)
+        q, k, v, budgets = _layer(n=1500)
+        hq = q.shape[0]
+        ref = ctx.sparse_attention_layer(q, k, v, budgets)
+        po = PeerOutputs(hq, q.shape[1], q.shape[2], world=2, rank=rank, device="cuda:0", sets=2)
+        for b, plan in enumerate((P.greedy_assign(budgets, 2), P.split_assign(budgets, 2, q.shape[1]))):
+            group = hq // k.shape[0]
+            if b == 0:
+                sh = rank_shard(plan, rank, group, budgets)
+                rng = None
+            else:
+                sh = rank_segments(plan, rank, group, budgets)
+                rng = sh.q_block_range
+            if sh.heads:
+                ctx.sparse_attention_layer(q[sh.heads].contiguous(), k[sh.kv_heads].contiguous(),
+                                           v[sh.kv_heads].contiguous(), sh.budgets, kv_map=sh.kv_map,
+                                           q_block_range=rng, gather=(po.ptrs(b), sh.heads, hq))
+            torch.cuda.synchronize()
+            dist.barrier()
+            result[2 * rank + b] = int(torch.equal(po.local[b], ref))
+        dist.barrier()
+        po.close()
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_outputs_two_processes_one_gpu():
+    """Two ranks (processes) on one GPU: each maps the other's output buffers by
+    CUDA IPC and its kernel 3 writes its heads (greedy plan) / head segments
+    (split plan) into both; afterwards both ranks hold the full layer."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx_mp = mp.get_context("spawn")
+    result = ctx_mp.Array("i", [0, 0, 0, 0])
+    procs = [ctx_mp.Process(target=_two_rank_worker, args=(r, port, result)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    for p_ in procs:
+        p_.join(timeout=300)
+    assert all(p_.exitcode == 0 for p_ in procs)
+    assert list(result) == [1, 1, 1, 1]
