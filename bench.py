@@ -403,6 +403,10 @@ def time_stack_p2p(ctx, shards, hq, steps, warmup, world, rank, stream):
                 ctx.sparse_attention_layer(ls.q, ls.k, ls.v, ls.budgets, causal=True, kv_map=ls.kv_map,
                                            stream=stream, q_block_range=ls.ranges,
                                            gather=(po.ptrs(b), ls.heads, hq))
+            if DEBUG_GLOO:  # exercising the path with every rank on one GPU: host barrier
+                torch.cuda.synchronize()
+                dist.barrier()
+                continue
             computed[b].record(stream)
             comm.wait_event(computed[b])
             with torch.cuda.stream(comm):
@@ -437,9 +441,8 @@ def time_e2e(ctx, shards, steps, warmup, world, stream):
     import torch
     shards = [ls for ls in shards if ls.heads]
     host = [tuple(t.cpu().pin_memory() for t in (ls.q, ls.k, ls.v)) for ls in shards]
-    host_out = torch.empty(shards[0].q.shape, dtype=shards[0].q.dtype, pin_memory=True)
 
-    outs = [host_out] + [torch.empty_like(host_out, pin_memory=True) for _ in shards[1:]]
+    outs = [torch.empty(ls.q.shape, dtype=ls.q.dtype, pin_memory=True) for ls in shards]  # per layer
 
     def step():  # layer l+1's H2D overlaps layer l's kernels and D2H (async host entry)
         for ls, (hq_, hk_, hv_), o in zip(shards, host, outs):
@@ -458,8 +461,9 @@ def time_e2e(ctx, shards, steps, warmup, world, stream):
     e1.record(stream)
     torch.cuda.synchronize()
     barrier(world)
-    h2d = sum(t.numel() * t.element_size() for t in host[0])
-    d2h = host_out.numel() * host_out.element_size()
+    # bytes per layer (the e2e value is ms per layer), averaged over the timed layers
+    h2d = sum(t.numel() * t.element_size() for hs in host for t in hs) // len(host)
+    d2h = sum(o.numel() * o.element_size() for o in outs) // len(outs)
     return e0.elapsed_time(e1) / (steps * len(shards)), h2d, d2h
 
 
@@ -635,7 +639,7 @@ def main():
                "load_imbalance": float(np.mean([
                    (float(p.loads.max() * world / p.loads.sum()) if name == "split"
                     else P.imbalance(b, p, world).imbalance) for b, p in zip(budgets_l, plans)]))}
-        if (world > 1 or args.force_gather) and not DEBUG_GLOO:
+        if (world > 1 or args.force_gather) and (not DEBUG_GLOO or args.gather == "p2p"):
             if args.gather == "p2p":
                 try:
                     res["ms_with_gather"] = time_stack_p2p(ctx, shards, hq, max(2, args.steps // 2), 1, world,
