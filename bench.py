@@ -510,6 +510,25 @@ def cpu_reference_sample(q, k, v, budgets, group, target_s, rng_seed=0):
     return ms_layer, threads, sample
 
 
+def cpu_reference_serial_head(q, k, v, budgets, group, rows=8):
+    """The bench_attention pattern (bench_attention.cpp:71-80): the serial
+    reference::sparse_attention on one head, timed on `rows` query rows and
+    extrapolated to the head's n rows (ms)."""
+    import time as _t
+
+    from oracle import oracle as O
+    from paper_2603_10353_b200.workload import bf16_bits
+    hq, n, d = q.shape
+    h = int(np.argmax(budgets))
+    kk = (bf16_bits(k[h // group]).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    vv = (bf16_bits(v[h // group]).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    sel = np.linspace(0, n - 1, rows).astype(np.int64)
+    qq = (bf16_bits(q[h][sel]).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    t0 = _t.time()
+    O.ref.sparse_attention(qq, kk, vv, int(budgets[h]), causal=False, serial=True)
+    return (_t.time() - t0) / rows * n * 1e3
+
+
 def run_reference(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -679,7 +698,10 @@ def main():
         try:
             ms_cpu, cores, sample = cpu_reference_sample(q, k, v, budgets, group, args.cpu_seconds)
             cpu = {"value": round(ms_cpu, 1), "unit": "ms", "cores": cores, "kind": "reference",
-                   "sample": sample}
+                   "sample": sample,
+                   "serial_one_head_ms": round(cpu_reference_serial_head(q, k, v, budgets, group), 1),
+                   "serial_one_head_note": ("reference::sparse_attention (serial) on the largest-budget "
+                                            "head, 8 rows timed, extrapolated to n rows")}
         except Exception as e:  # reference library missing: report, do not fail the bench
             cpu = {"value": None, "unit": "ms", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
