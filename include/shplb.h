@@ -158,7 +158,10 @@ int shplb_barrier(const double* device_latency, int32_t devices, double* barrier
  * Block-sparse attention on sm_100a  (reference: proj/include/headbal/attention.hpp)
  * ====================================================================== */
 
-/* One context per CUDA device (rank). Owns the device workspace. */
+/* One context per CUDA device (rank). Owns the device workspace. The budget-
+ * table, plan and metric functions are pure and reentrant like the reference's
+ * (SPEC: no shared mutable state); a context is not: calls on one context must
+ * not overlap across host threads (use one context per thread or stream). */
 int shplb_ctx_create(int device, shplb_ctx** ctx_out);
 int shplb_ctx_destroy(shplb_ctx* ctx);
 /* Number of kernel launches the context issued since creation (all kinds). */

@@ -484,12 +484,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
 }  // namespace
 
 void launch_fa(const FaParams& p, int num_tiles, cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(fa_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kSmemTotal));
-        configured = true;
-    }
+    // Per launch (not cached in a static): the attribute belongs to the current
+    // device's context, and the call costs microseconds against a long kernel.
+    cudaFuncSetAttribute(fa_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemTotal));
     fa_sparse_kernel<<<num_tiles, kThreads, kSmemTotal, s>>>(p);
 }
 

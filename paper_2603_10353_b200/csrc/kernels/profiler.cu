@@ -149,12 +149,9 @@ __global__ void segment_offsets_kernel(int64_t* off, int64_t units, int64_t n_k)
 void launch_profile_scores(const void* q_rows, const void* k, int hq, int hkv, int64_t n_rows,
                            int64_t n_k, double scale, double* scores, cudaStream_t s) {
     constexpr size_t smem = sizeof(double) * (kHeadDim * (kProfKeys + 1) + kProfRows * kHeadDim);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(profile_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        configured = true;
-    }
+    // Per launch (not cached in a static): the attribute belongs to the current
+    // device's context, and the call costs microseconds against a long kernel.
+    cudaFuncSetAttribute(profile_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>((n_k + kProfKeys - 1) / kProfKeys), static_cast<unsigned>(hkv));
     profile_scores_kernel<<<grid, kProfThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(q_rows),
                                                         static_cast<const __nv_bfloat16*>(k), hq, hkv, n_rows,
