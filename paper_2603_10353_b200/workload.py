@@ -15,6 +15,12 @@ can see:
   dense. So different heads need different budgets, which is what the max-min
   allocator and the balancer act on.
 
+``targets="per_head"`` (the accuracy study, not the bench default): each head
+h has its own set of m_h "hot" key blocks, m_h log-uniform in [1, hot_max];
+a query targets a random visible hot block of its head (its own block if none
+is visible yet). Heads then differ in how many *blocks* they need — the
+block-level heterogeneity the head-adaptive budget is meant to exploit.
+
 Generation runs with torch on the target device (plumbing, not the product);
 the same seed gives the same tensors on CPU and GPU generators separately, so
 tests generate on CPU and copy, and the bench generates on the GPU.
@@ -41,6 +47,8 @@ class LayerSpec:
     local_weight: float = 0.5
     target_weight: float = 1.0
     layer: int = 0
+    targets: str = "per_query"  # or "per_head" (hot key blocks per head, see module doc)
+    hot_max: int = 256
 
 
 def head_temperatures(spec: LayerSpec) -> torch.Tensor:
@@ -64,11 +72,22 @@ def make_layer(spec: LayerSpec, device="cpu"):
     tau = head_temperatures(spec).to(dev)
     group = hq // hkv
     q = torch.empty(hq, n, d, device=dev)
+    if spec.targets == "per_head":
+        gh_ = torch.Generator().manual_seed(spec.seed * 1000003 + spec.layer * 7919 + 23)
+        lo, hi = 0.0, math.log(max(1, min(spec.hot_max, nb)))
+        m = torch.exp(lo + (hi - lo) * torch.rand(hq, generator=gh_, dtype=torch.float64)).round().long().clamp(min=1)
     for h in range(hq):
         gh = h // group
-        # one random earlier (or same) block per query: uniform in [0, own block]
         u = torch.rand(n, generator=g, device=dev)
-        tgt = torch.floor(u * (blk + 1).to(u.dtype)).to(torch.int64)
+        if spec.targets == "per_head":
+            # m_h hot blocks per head; a query picks a random visible one (else its own block)
+            hot = torch.sort(torch.randperm(nb, generator=g, device=dev)[: int(m[h])]).values
+            nvis = torch.searchsorted(hot, blk, right=True)  # hot blocks <= own block
+            pick = torch.floor(u * nvis.clamp(min=1).to(u.dtype)).to(torch.int64)
+            tgt = torch.where(nvis > 0, hot[pick.clamp(max=hot.numel() - 1)], blk)
+        else:
+            # one random earlier (or same) block per query: uniform in [0, own block]
+            tgt = torch.floor(u * (blk + 1).to(u.dtype)).to(torch.int64)
         qh = (spec.local_weight * cent[gh, blk, :] + spec.target_weight * cent[gh, tgt, :]
               + torch.randn(n, d, generator=g, device=dev))
         q[h] = tau[h] * qh
