@@ -38,6 +38,7 @@
 //                     O half 0 [256,384), O half 1 [384,512).
 #include <cstdint>
 #include <cstdio>
+#include <type_traits>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -301,21 +302,21 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
         // blocks, the FMA-pipe polynomial) / FADD2 row sum, bf16 pairs stored
         // back over S's first columns (tcgen05.st). With track, the raw row
         // max of the quarter is folded into mx8 on the ALU pipe meanwhile.
-        auto exp_quarter = [&](const float* s, int c, float msub, bool emu_blk, float2 (&sum2)[2],
-                               float (&mx8)[8], bool track) {
+        auto exp_quarter = [&](const float* s, int c, float msub, float2 (&sum2)[2], auto emu_tag) {
+            constexpr bool kEmu = decltype(emu_tag)::value;
             const float2 nm2 = make_float2(-msub, -msub);
             uint32_t pk[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-                const float a0 = s[c * 32 + 2 * e], a1 = s[c * 32 + 2 * e + 1];
-                if (track) {
-                    mx8[(2 * e) & 7] = fmaxf(mx8[(2 * e) & 7], a0);
-                    mx8[(2 * e + 1) & 7] = fmaxf(mx8[(2 * e + 1) & 7], a1);
-                }
-                const float2 x = ffma2(make_float2(a0, a1), sc2, nm2);
+                const float2 x = ffma2(make_float2(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]), sc2, nm2);
                 float2 pe;
-                if (emu_blk && ((e * kEmuPairs) & 15) < kEmuPairs) {
-                    pe = ex2_poly2(x);
+                if constexpr (kEmu) {
+                    if (((e * kEmuPairs) & 15) < kEmuPairs) {
+                        pe = ex2_poly2(x);
+                    } else {
+                        pe.x = ex2(x.x);
+                        pe.y = ex2(x.y);
+                    }
                 } else {
                     pe.x = ex2(x.x);
                     pe.y = ex2(x.y);
@@ -393,8 +394,13 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
                 if (it >= 1 && __any_sync(0xffffffffu, alpha != 1.0f)) rescale_o(alpha);
                 const float msub = (m == -INFINITY) ? 0.0f : m;
                 TRACE(j, 3 * hf + 1, r == 0);
+                if (kEmuPairs > 0 && emu_blk) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c) exp_quarter(s, c, msub, emu_blk, sum2, mx8, false);
+                    for (int c = 0; c < 4; ++c) exp_quarter(s, c, msub, sum2, std::true_type{});
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) exp_quarter(s, c, msub, sum2, std::false_type{});
+                }
             }
             const float2 sum = fadd2(sum2[0], sum2[1]);
             l = l * alpha + (sum.x + sum.y);
