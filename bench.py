@@ -682,6 +682,10 @@ def main():
         torch.cuda.empty_cache()
 
     q, k, v = layers[0]
+    dense_ms = None
+    if world == 1:  # the paper's "vs full attention" axis: dense causal layer 0 on the same kernel 3
+        from paper_2603_10353_b200 import experiments as X
+        dense_ms = X._time(lambda: ctx.dense_attention_layer(q, k, v, causal=True, stream=stream), 2)
     projection = None
     if world == 1 and args.project_degrees:
         from paper_2603_10353_b200 import experiments as X
@@ -780,6 +784,9 @@ def main():
                           "NVLink (CUDA IPC peer pointers); one NCCL barrier per layer on a comm stream")
         line["gather_kind"] = g.get("gather_kind")
         line["load_imbalance"] = round(g["load_imbalance"], 4)
+    if dense_ms is not None:
+        line["dense_comparator"] = {"ms": round(dense_ms, 3), "speedup_sparse_vs_dense": round(dense_ms / value, 3),
+                                    "what": "layer 0, every causally visible key block (shplb_dense_attention_layer)"}
     if projection:
         line["per_rank_projection"] = {
             "what": ("layer 0: every rank's shard timed in turn on this GPU (CUDA events, median of 3); "
