@@ -685,7 +685,7 @@ def main():
     dense_ms = None
     if world == 1:  # the paper's "vs full attention" axis: dense causal layer 0 on the same kernel 3
         from paper_2603_10353_b200 import experiments as X
-        dense_ms = X._time(lambda: ctx.dense_attention_layer(q, k, v, causal=True, stream=stream), 2)
+        dense_ms = X._time(lambda: ctx.dense_attention_layer(q, k, v, causal=True), 2)  # current stream
     projection = None
     if world == 1 and args.project_degrees:
         from paper_2603_10353_b200 import experiments as X
