@@ -137,7 +137,10 @@ void check_shape(const shplb_layer_shape* s) {
     if ((s->block_q != 128 && s->block_q != 256) || s->block_k != kern::kBlock)
         throw NotSupported("block sizes must be block_q in {128, 256}, block_k = 128");
     if (s->kind != SHPLB_BLOCK_TOPK) throw NotSupported("selection kind not supported");
-    if (s->seq_len > (int64_t(1) << 26)) throw NotSupported("seq_len too large");
+    if (s->seq_len > int64_t(kern::kMaxKeyBlocks) * kern::kBlock) {
+        throw NotSupported("seq_len " + std::to_string(s->seq_len) + " exceeds the selector's limit of " +
+                           std::to_string(int64_t(kern::kMaxKeyBlocks) * kern::kBlock) + " tokens");
+    }
     if (s->out_peers && s->n_out_peers > 0) {  // fused output gather
         if (s->n_out_peers > kern::kMaxPeers)
             throw NotSupported("at most " + std::to_string(kern::kMaxPeers) + " output buffers per call");

@@ -309,3 +309,11 @@ def test_max_heads_per_call(cuda_ctx):
     k = torch.zeros((1, 128, 128), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(P.NotSupported, match="at most 256 query heads per call"):
         cuda_ctx.sparse_attention_layer(q, k, k, np.full(257, 128, np.int64))
+
+
+def test_sequence_length_limit_is_reported(cuda_ctx):
+    """Kernel 2's shared-memory score rows bound n (382,976 tokens); longer
+    sequences are refused up front with NotSupported, not a launch failure."""
+    q = torch.zeros((1, 383104, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(P.NotSupported, match="exceeds the selector's limit of 382976 tokens"):
+        cuda_ctx.sparse_attention_layer(q, q, q, [128])
