@@ -317,3 +317,22 @@ def test_sequence_length_limit_is_reported(cuda_ctx):
     q = torch.zeros((1, 383104, 128), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(P.NotSupported, match="exceeds the selector's limit of 382976 tokens"):
         cuda_ctx.sparse_attention_layer(q, q, q, [128])
+
+
+def test_zero_q_gives_uniform_weights_over_kept_keys(cuda_ctx):
+    """test_attention.cpp:44-61 at block granularity: Q = 0 makes every score 0,
+    all blocks tie and the lowest k block indices are kept; each output row is
+    the plain mean of V over its kept, causally visible keys."""
+    n, kblk = 512, 2
+    spec = LayerSpec(num_q_heads=1, num_kv_heads=1, seq_len=n, seed=17)
+    _, k, v = make_layer(spec, "cpu")
+    q = torch.zeros((1, n, 128), dtype=torch.bfloat16)
+    out = cuda_ctx.sparse_attention_layer(q.cuda(), k.cuda(), v.cuda(), [kblk * 128], causal=True)
+    torch.cuda.synchronize()
+    vf = v[0].double().numpy()
+    ref = np.empty((n, 128))
+    for i in range(n):
+        last = min(i, kblk * 128 - 1)  # kept blocks 0..kblk-1, causal
+        ref[i] = vf[: last + 1].mean(0)
+    mx, rel = _errors(out[0], ref)
+    assert mx <= MAX_ABS and rel <= MEAN_REL, (mx, rel)
