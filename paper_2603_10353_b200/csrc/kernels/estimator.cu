@@ -90,23 +90,24 @@ __device__ __forceinline__ uint32_t order_key(float s) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// Warp-level top-k over row[0..vis) held in shared memory: bisection on the
-// key bits finds T, the kk-th largest key; keys > T are kept, plus the first
-// (kk - #keys>T) keys == T in index order (index-ascending tie rule). Output
-// is compacted in ascending index order with ballots.
-__device__ void warp_select_row(const float* row, int vis, int kk, int64_t kmax,
-                                int32_t* __restrict__ idx_row) {
+// Warp-level top-k over keys[0..vis) (order_key images, shared or global
+// memory): bisection on the key bits finds T, the kk-th largest key; keys > T
+// are kept, plus the first (kk - #keys>T) keys == T in index order
+// (index-ascending tie rule). Output is compacted in ascending index order
+// with ballots.
+template <typename KeyAt>
+__device__ void warp_select_row(KeyAt key_at, int vis, int kk, int64_t kmax, int32_t* __restrict__ idx_row) {
     const int lane = threadIdx.x & 31;
     uint32_t T = 0;
     for (int bit = 31; bit >= 0; --bit) {
         const uint32_t trial = T | (1u << bit);
         int c = 0;
-        for (int j = lane; j < vis; j += 32) c += order_key(row[j]) >= trial;
+        for (int j = lane; j < vis; j += 32) c += key_at(j) >= trial;
         c = __reduce_add_sync(0xffffffffu, c);
         if (c >= kk) T = trial;
     }
     int gt = 0;
-    for (int j = lane; j < vis; j += 32) gt += order_key(row[j]) > T;
+    for (int j = lane; j < vis; j += 32) gt += key_at(j) > T;
     gt = __reduce_add_sync(0xffffffffu, gt);
     const int need = kk - gt;
     const uint32_t lt_mask = (1u << lane) - 1u;
@@ -114,7 +115,7 @@ __device__ void warp_select_row(const float* row, int vis, int kk, int64_t kmax,
     for (int base = 0; base < vis; base += 32) {
         const int j = base + lane;
         const bool valid = j < vis;
-        const uint32_t key = valid ? order_key(row[j]) : 0u;
+        const uint32_t key = valid ? key_at(j) : 0u;
         const bool eq = valid && key == T;
         const uint32_t eq_mask = __ballot_sync(0xffffffffu, eq);
         const int tie_rank = ties + __popc(eq_mask & lt_mask);
@@ -130,20 +131,22 @@ __device__ void warp_select_row(const float* row, int vis, int kk, int64_t kmax,
 constexpr int kSelThreads = 256;  // 8 warps
 constexpr int kRowsPerCta = 16;   // query blocks per CTA
 constexpr int kChunk = 64;        // key blocks per shared-memory chunk
+constexpr int kPad = kHeadDim + 4;  // row stride (floats) of the Q / K tiles: 16-byte rows, no bank conflicts
 
 // One CTA: head h, query blocks [qb0, qb0+16). Scores for all visible key
 // blocks are built in shared memory with an FFMA micro-tile (2 rows x 2 key
-// blocks per thread, fmaf chain over c = 0..127 in order), then each warp
-// selects two rows.
+// blocks per thread; per 4 columns two float4 loads of Q, two of K, 16
+// FFMAs; every dot product is one fmaf chain over c = 0..127 in order), then
+// converted once to order keys, then each warp selects two rows.
 __global__ void __launch_bounds__(kSelThreads)
     score_select_kernel(const float* __restrict__ qp, const float* __restrict__ kp, int hq,
                         int hkv, int64_t n, int64_t nqb, int64_t nkb, int bq, int causal, float scale,
                         HeadTable ht, int64_t kmax, float* __restrict__ scores_out, int select,
                         int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
     extern __shared__ __align__(16) float smem[];
-    float* Qs = smem;                          // [128 c][16 rows]
-    float* Ks = Qs + kHeadDim * kRowsPerCta;   // [128 c][64 key blocks]
-    float* S = Ks + kHeadDim * kChunk;         // [16 rows][nkb_pad]
+    float* Qs = smem;                     // [16 rows][kPad]
+    float* Ks = Qs + kRowsPerCta * kPad;  // [64 key blocks][kPad]
+    float* S = Ks + kChunk * kPad;        // [16 rows][nkb_pad]
     const int64_t nkb_pad = (nkb + 3) & ~int64_t(3);
 
     const int h = blockIdx.y;
@@ -152,10 +155,12 @@ __global__ void __launch_bounds__(kSelThreads)
     const int rows = static_cast<int>(min(static_cast<int64_t>(kRowsPerCta), nqb - qb0));
     const int tid = threadIdx.x;
 
-    // Q tile, transposed to [c][row].
-    for (int f = tid; f < kRowsPerCta * kHeadDim; f += kSelThreads) {
-        const int r = f / kHeadDim, c = f % kHeadDim;
-        Qs[c * kRowsPerCta + r] = r < rows ? qp[((int64_t)h * nqb + qb0 + r) * kHeadDim + c] : 0.0f;
+    // Q tile (row-major, float4).
+    for (int f = tid; f < kRowsPerCta * (kHeadDim / 4); f += kSelThreads) {
+        const int r = f / (kHeadDim / 4), c4 = f % (kHeadDim / 4);
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < rows) v = *reinterpret_cast<const float4*>(qp + ((int64_t)h * nqb + qb0 + r) * kHeadDim + c4 * 4);
+        *reinterpret_cast<float4*>(Qs + r * kPad + c4 * 4) = v;
     }
     const int64_t vis_max = visible_blocks(qb0 + rows - 1, n, nkb, bq, causal != 0);
 
@@ -163,27 +168,30 @@ __global__ void __launch_bounds__(kSelThreads)
     const int kq = tid >> 3;  // key blocks 2kq, 2kq+1 of the chunk
     for (int64_t kc = 0; kc < vis_max; kc += kChunk) {
         __syncthreads();  // previous chunk fully consumed (and Q tile visible)
-        // K chunk transposed to [c][kb]: a warp covers 32 consecutive key
-        // blocks at one column quad (conflict-free shared stores).
         for (int f = tid; f < kChunk * (kHeadDim / 4); f += kSelThreads) {
-            const int kb = f % kChunk, c4 = f / kChunk;
+            const int kb = f / (kHeadDim / 4), c4 = f % (kHeadDim / 4);
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
             if (kc + kb < nkb) v = *reinterpret_cast<const float4*>(kp + ((int64_t)g * nkb + kc + kb) * kHeadDim + c4 * 4);
-            Ks[(c4 * 4 + 0) * kChunk + kb] = v.x;
-            Ks[(c4 * 4 + 1) * kChunk + kb] = v.y;
-            Ks[(c4 * 4 + 2) * kChunk + kb] = v.z;
-            Ks[(c4 * 4 + 3) * kChunk + kb] = v.w;
+            *reinterpret_cast<float4*>(Ks + kb * kPad + c4 * 4) = v;
         }
         __syncthreads();
         float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
-#pragma unroll 8
-        for (int c = 0; c < kHeadDim; ++c) {
-            const float2 q2 = *reinterpret_cast<const float2*>(Qs + c * kRowsPerCta + 2 * rp);
-            const float2 k2 = *reinterpret_cast<const float2*>(Ks + c * kChunk + 2 * kq);
-            a00 = __fmaf_rn(q2.x, k2.x, a00);
-            a01 = __fmaf_rn(q2.x, k2.y, a01);
-            a10 = __fmaf_rn(q2.y, k2.x, a10);
-            a11 = __fmaf_rn(q2.y, k2.y, a11);
+        const float* q0p = Qs + (2 * rp) * kPad;
+        const float* k0p = Ks + (2 * kq) * kPad;
+#pragma unroll 4
+        for (int c4 = 0; c4 < kHeadDim / 4; ++c4) {
+            const float4 q0 = *reinterpret_cast<const float4*>(q0p + c4 * 4);
+            const float4 q1 = *reinterpret_cast<const float4*>(q0p + kPad + c4 * 4);
+            const float4 k0 = *reinterpret_cast<const float4*>(k0p + c4 * 4);
+            const float4 k1 = *reinterpret_cast<const float4*>(k0p + kPad + c4 * 4);
+            a00 = __fmaf_rn(q0.x, k0.x, a00); a01 = __fmaf_rn(q0.x, k1.x, a01);
+            a10 = __fmaf_rn(q1.x, k0.x, a10); a11 = __fmaf_rn(q1.x, k1.x, a11);
+            a00 = __fmaf_rn(q0.y, k0.y, a00); a01 = __fmaf_rn(q0.y, k1.y, a01);
+            a10 = __fmaf_rn(q1.y, k0.y, a10); a11 = __fmaf_rn(q1.y, k1.y, a11);
+            a00 = __fmaf_rn(q0.z, k0.z, a00); a01 = __fmaf_rn(q0.z, k1.z, a01);
+            a10 = __fmaf_rn(q1.z, k0.z, a10); a11 = __fmaf_rn(q1.z, k1.z, a11);
+            a00 = __fmaf_rn(q0.w, k0.w, a00); a01 = __fmaf_rn(q0.w, k1.w, a01);
+            a10 = __fmaf_rn(q1.w, k0.w, a10); a11 = __fmaf_rn(q1.w, k1.w, a11);
         }
         const float a[2][2] = {{a00, a01}, {a10, a11}};
 #pragma unroll
@@ -207,12 +215,18 @@ __global__ void __launch_bounds__(kSelThreads)
         }
     }
     if (!select) return;
+    // Scores -> order keys in place, once (the bisection reads each key 33 times).
+    uint32_t* Kk = reinterpret_cast<uint32_t*>(S);
+    for (int r = 0; r < rows; ++r)
+        for (int64_t kb = tid; kb < vis_max; kb += kSelThreads) Kk[r * nkb_pad + kb] = order_key(S[r * nkb_pad + kb]);
+    __syncthreads();
     const int warp = tid >> 5;
     for (int r = warp; r < rows; r += kSelThreads / 32) {
         const int64_t qb = qb0 + r;
         const int vis = static_cast<int>(visible_blocks(qb, n, nkb, bq, causal != 0));
         const int kk = min(ht.k[h], vis);
-        warp_select_row(S + r * nkb_pad, vis, kk, kmax, idx + ((int64_t)h * nqb + qb) * kmax);
+        const uint32_t* keys = Kk + r * nkb_pad;
+        warp_select_row([keys](int j) { return keys[j]; }, vis, kk, kmax, idx + ((int64_t)h * nqb + qb) * kmax);
         if ((tid & 31) == 0) cnt[(int64_t)h * nqb + qb] = kk;
     }
 }
@@ -228,7 +242,8 @@ __global__ void __launch_bounds__(kSelThreads)
     const int64_t qb = row % nqb;
     const int vis = static_cast<int>(visible_blocks(qb, n, nkb, bq, causal != 0));
     const int kk = min(ht.k[h], vis);
-    warp_select_row(scores + row * nkb, vis, kk, kmax, idx + row * kmax);
+    const float* srow = scores + row * nkb;
+    warp_select_row([srow](int j) { return order_key(srow[j]); }, vis, kk, kmax, idx + row * kmax);
     if ((threadIdx.x & 31) == 0) cnt[row] = kk;
 }
 
@@ -254,7 +269,7 @@ void launch_pool(const void* x, int heads, int64_t n, int rows, float* out, cuda
 
 static size_t score_select_smem(int64_t nkb) {
     const int64_t nkb_pad = (nkb + 3) & ~int64_t(3);
-    return sizeof(float) * (kHeadDim * kRowsPerCta + kHeadDim * kChunk + kRowsPerCta * nkb_pad);
+    return sizeof(float) * (kPad * kRowsPerCta + kPad * kChunk + kRowsPerCta * nkb_pad);
 }
 
 void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n, int bq,

@@ -15,8 +15,8 @@ constexpr int kMaxHeads = 256;  // per-launch k-block table lives in the kernel 
 constexpr int kMaxSelected = 2048;  // selected key blocks per query tile staged in smem (256K tokens)
 constexpr int kMaxPeers = 8;        // output buffers kernel 3 can write each row to (fused gather)
 // Kernel 2 keeps 16 rows of scores for all key blocks in shared memory:
-// 40 KB + 64 B per key block within the 227 KB opt-in limit.
-constexpr int kMaxKeyBlocks = (227 * 1024 - 40960) / 64;  // 2992 -> 382,976 tokens
+// 41.25 KB of Q / K tiles + 64 B per key block within the 227 KB opt-in limit.
+constexpr int kMaxKeyBlocks = (227 * 1024 - 42240) / 64;  // 2972 -> 380,416 tokens
 
 // Per-q-head table passed in kernel parameters.
 struct HeadTable {

@@ -312,10 +312,10 @@ def test_max_heads_per_call(cuda_ctx):
 
 
 def test_sequence_length_limit_is_reported(cuda_ctx):
-    """Kernel 2's shared-memory score rows bound n (382,976 tokens); longer
+    """Kernel 2's shared-memory score rows bound n (380,416 tokens); longer
     sequences are refused up front with NotSupported, not a launch failure."""
     q = torch.zeros((1, 383104, 128), dtype=torch.bfloat16, device="cuda")
-    with pytest.raises(P.NotSupported, match="exceeds the selector's limit of 382976 tokens"):
+    with pytest.raises(P.NotSupported, match="exceeds the selector's limit of 380416 tokens"):
         cuda_ctx.sparse_attention_layer(q, q, q, [128])
 
 
