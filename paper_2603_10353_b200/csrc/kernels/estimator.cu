@@ -90,32 +90,46 @@ __device__ __forceinline__ uint32_t order_key(float s) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// Warp-level top-k over keys[0..vis) (order_key images, shared or global
-// memory): bisection on the key bits finds T, the kk-th largest key; keys > T
-// are kept, plus the first (kk - #keys>T) keys == T in index order
-// (index-ascending tie rule). Output is compacted in ascending index order
-// with ballots.
+// Warp-level top-k over keys[0..vis) (order_key images): bisection on the key
+// bits finds T, the kk-th largest key; keys > T are kept, plus the first
+// (kk - #keys>T) keys == T in index order (index-ascending tie rule). Output
+// is compacted in ascending index order with ballots. Rows of up to 1024
+// candidates are held in registers (32 per lane) for the 33 counting passes.
 template <typename KeyAt>
 __device__ void warp_select_row(KeyAt key_at, int vis, int kk, int64_t kmax, int32_t* __restrict__ idx_row) {
     const int lane = threadIdx.x & 31;
+    constexpr int kRegKeys = 32;  // rows of up to 1024 candidates (128K tokens) run from registers
+    uint32_t kr[kRegKeys];
+    const bool in_regs = vis <= 32 * kRegKeys;
+    if (in_regs) {
+#pragma unroll
+        for (int t = 0; t < kRegKeys; ++t) {
+            const int j = lane + 32 * t;
+            kr[t] = j < vis ? key_at(j) : 0u;  // 0 is below every real key (order_key(-inf) > 0)
+        }
+    }
+    auto count_ge = [&](uint32_t trial) {
+        int c = 0;
+        if (in_regs) {
+#pragma unroll
+            for (int t = 0; t < kRegKeys; ++t) c += kr[t] >= trial;
+        } else {
+            for (int j = lane; j < vis; j += 32) c += key_at(j) >= trial;
+        }
+        return __reduce_add_sync(0xffffffffu, c);
+    };
     uint32_t T = 0;
     for (int bit = 31; bit >= 0; --bit) {
         const uint32_t trial = T | (1u << bit);
-        int c = 0;
-        for (int j = lane; j < vis; j += 32) c += key_at(j) >= trial;
-        c = __reduce_add_sync(0xffffffffu, c);
-        if (c >= kk) T = trial;
+        if (count_ge(trial) >= kk) T = trial;
     }
-    int gt = 0;
-    for (int j = lane; j < vis; j += 32) gt += key_at(j) > T;
-    gt = __reduce_add_sync(0xffffffffu, gt);
+    const int gt = T == 0xFFFFFFFFu ? 0 : count_ge(T + 1);  // keys > T
     const int need = kk - gt;
     const uint32_t lt_mask = (1u << lane) - 1u;
     int written = 0, ties = 0;
-    for (int base = 0; base < vis; base += 32) {
-        const int j = base + lane;
+    // Ascending compaction of the kept indices, 32 candidates per step.
+    auto emit = [&](int j, uint32_t key) {
         const bool valid = j < vis;
-        const uint32_t key = valid ? key_at(j) : 0u;
         const bool eq = valid && key == T;
         const uint32_t eq_mask = __ballot_sync(0xffffffffu, eq);
         const int tie_rank = ties + __popc(eq_mask & lt_mask);
@@ -124,6 +138,18 @@ __device__ void warp_select_row(KeyAt key_at, int vis, int kk, int64_t kmax, int
         if (sel) idx_row[written + __popc(sel_mask & lt_mask)] = j;
         written += __popc(sel_mask);
         ties += __popc(eq_mask);
+    };
+    if (in_regs) {
+#pragma unroll
+        for (int t = 0; t < kRegKeys; ++t) {
+            if (32 * t >= vis) break;  // warp-uniform
+            emit(lane + 32 * t, kr[t]);
+        }
+    } else {
+        for (int base = 0; base < vis; base += 32) {
+            const int j = base + lane;
+            emit(j, j < vis ? key_at(j) : 0u);
+        }
     }
     for (int64_t p = kk + lane; p < kmax; p += 32) idx_row[p] = -1;
 }
