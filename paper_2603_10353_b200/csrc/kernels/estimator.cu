@@ -161,8 +161,9 @@ constexpr int kPad = kHeadDim + 4;  // row stride (floats) of the Q / K tiles: 1
 
 // One CTA: head h, query blocks [qb0, qb0+16). Scores for all visible key
 // blocks are built in shared memory with an FFMA micro-tile (2 rows x 2 key
-// blocks per thread; per 4 columns two float4 loads of Q, two of K, 16
-// FFMAs; every dot product is one fmaf chain over c = 0..127 in order), then
+// blocks per thread, strided 8 rows / 32 blocks apart; per 4 columns two
+// float4 loads of Q, two of K, 16 FFMAs; every dot product is one fmaf chain
+// over c = 0..127 in order), then
 // converted once to order keys, then each warp selects two rows.
 __global__ void __launch_bounds__(kSelThreads)
     score_select_kernel(const float* __restrict__ qp, const float* __restrict__ kp, int hq,
@@ -190,8 +191,11 @@ __global__ void __launch_bounds__(kSelThreads)
     }
     const int64_t vis_max = visible_blocks(qb0 + rows - 1, n, nkb, bq, causal != 0);
 
-    const int rp = tid & 7;   // rows 2rp, 2rp+1
-    const int kq = tid >> 3;  // key blocks 2kq, 2kq+1 of the chunk
+    // Thread (rp, kq) computes rows {rp, rp+8} x key blocks {kq, kq+32} of the
+    // chunk: a warp's 8 row / 4 key-block float4 loads then hit distinct bank
+    // quads (row stride 132 floats = 4 banks).
+    const int rp = tid & 7;
+    const int kq = tid >> 3;
     for (int64_t kc = 0; kc < vis_max; kc += kChunk) {
         __syncthreads();  // previous chunk fully consumed (and Q tile visible)
         for (int f = tid; f < kChunk * (kHeadDim / 4); f += kSelThreads) {
@@ -202,14 +206,14 @@ __global__ void __launch_bounds__(kSelThreads)
         }
         __syncthreads();
         float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
-        const float* q0p = Qs + (2 * rp) * kPad;
-        const float* k0p = Ks + (2 * kq) * kPad;
+        const float* q0p = Qs + rp * kPad;
+        const float* k0p = Ks + kq * kPad;
 #pragma unroll 4
         for (int c4 = 0; c4 < kHeadDim / 4; ++c4) {
             const float4 q0 = *reinterpret_cast<const float4*>(q0p + c4 * 4);
-            const float4 q1 = *reinterpret_cast<const float4*>(q0p + kPad + c4 * 4);
+            const float4 q1 = *reinterpret_cast<const float4*>(q0p + 8 * kPad + c4 * 4);
             const float4 k0 = *reinterpret_cast<const float4*>(k0p + c4 * 4);
-            const float4 k1 = *reinterpret_cast<const float4*>(k0p + kPad + c4 * 4);
+            const float4 k1 = *reinterpret_cast<const float4*>(k0p + 32 * kPad + c4 * 4);
             a00 = __fmaf_rn(q0.x, k0.x, a00); a01 = __fmaf_rn(q0.x, k1.x, a01);
             a10 = __fmaf_rn(q1.x, k0.x, a10); a11 = __fmaf_rn(q1.x, k1.x, a11);
             a00 = __fmaf_rn(q0.y, k0.y, a00); a01 = __fmaf_rn(q0.y, k1.y, a01);
@@ -222,11 +226,11 @@ __global__ void __launch_bounds__(kSelThreads)
         const float a[2][2] = {{a00, a01}, {a10, a11}};
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            const int r = 2 * rp + i;
+            const int r = rp + 8 * i;
             const int64_t vis = visible_blocks(qb0 + r, n, nkb, bq, causal != 0);
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                const int64_t kb = kc + 2 * kq + j;
+                const int64_t kb = kc + kq + 32 * j;
                 if (kb < nkb) S[r * nkb_pad + kb] = kb < vis ? __fmul_rn(a[i][j], scale) : -INFINITY;
             }
         }
