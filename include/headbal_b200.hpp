@@ -23,6 +23,8 @@
 #include "headbal/partitioner.hpp"
 #include "headbal/profiler.hpp"
 #include "headbal/workload.hpp"
+#include <cuda_runtime.h>
+
 #include "shplb.h"
 
 namespace headbal::b200 {
@@ -155,6 +157,60 @@ inline BudgetAllocation maxmin_allocate(const std::vector<RecoveryCurve>& curves
     a.hit_iteration_cap = diag.hit_iteration_cap != 0;
     a.off_grid_evaluations = diag.off_grid_evaluations;
     return a;
+}
+
+// ----- recovery curves (profiler.hpp:86-89): build_profiles for PerQueryTopK on the
+// workload's query rows (all n_k keys, no causal mask as the reference's
+// profile command), through the GPU profiler when a context is given, else the
+// host C++ one. Heads with equal K share a kv head. Curves agree with the
+// reference to rounding (1e-12).
+inline std::vector<RecoveryCurve> build_profiles(const AttentionWorkload& w, const std::vector<long>& grid,
+                                                 Context* ctx = nullptr) {
+    w.validate();
+    const auto H = static_cast<int32_t>(w.num_heads());
+    const auto rows = static_cast<int64_t>(w.num_queries());
+    const auto n_k = static_cast<int64_t>(w.context_length());
+    const auto d = static_cast<int32_t>(w.head_dim());
+    // The C ABI takes the standard GQA grouping: every q head of a group
+    // contiguous with the same K. Group consecutive heads with equal K.
+    int32_t group = 1;
+    while (group < H && w.heads[group].K == w.heads[0].K) ++group;
+    if (H % group != 0) group = 1;
+    for (int32_t h = 0; h < H; ++h)
+        if (!(w.heads[h].K == w.heads[(h / group) * group].K)) group = 1;
+    const int32_t hkv = H / group;
+    std::vector<uint16_t> q(static_cast<size_t>(H) * rows * d), k(static_cast<size_t>(hkv) * n_k * d);
+    for (int32_t h = 0; h < H; ++h)
+        for (size_t i = 0; i < static_cast<size_t>(rows) * d; ++i) q[h * rows * d + i] = to_bf16(w.heads[h].Q.data[i]);
+    for (int32_t g = 0; g < hkv; ++g)
+        for (size_t i = 0; i < static_cast<size_t>(n_k) * d; ++i)
+            k[g * n_k * d + i] = to_bf16(w.heads[g * group].K.data[i]);
+    const std::vector<int64_t> gr(grid.begin(), grid.end());
+    std::vector<double> rec(static_cast<size_t>(H) * gr.size());
+    if (ctx) {
+        // device copies for the GPU profiler
+        void* dq = nullptr;
+        void* dk = nullptr;
+        check(cudaMalloc(&dq, q.size() * 2) == cudaSuccess ? SHPLB_OK : SHPLB_CUDA_ERROR);
+        check(cudaMalloc(&dk, k.size() * 2) == cudaSuccess ? SHPLB_OK : SHPLB_CUDA_ERROR);
+        cudaMemcpy(dq, q.data(), q.size() * 2, cudaMemcpyHostToDevice);
+        cudaMemcpy(dk, k.data(), k.size() * 2, cudaMemcpyHostToDevice);
+        const int rc = shplb_profile_curves(ctx->get(), dq, dk, H, hkv, rows, n_k, d, gr.data(),
+                                            static_cast<int64_t>(gr.size()), rec.data(), nullptr);
+        cudaFree(dq);
+        cudaFree(dk);
+        check(rc);
+    } else {
+        check(shplb_profile_curves_host(q.data(), k.data(), H, hkv, rows, n_k, d, gr.data(),
+                                        static_cast<int64_t>(gr.size()), rec.data()));
+    }
+    std::vector<RecoveryCurve> curves(static_cast<size_t>(H));
+    for (int32_t h = 0; h < H; ++h) {
+        curves[h].id = HeadId{0, h};
+        curves[h].context_length = n_k;
+        for (size_t i = 0; i < gr.size(); ++i) curves[h].points.push_back({grid[i], rec[h * gr.size() + i]});
+    }
+    return curves;
 }
 
 // ----- head plan (partitioner.hpp:36-51): same signatures, bit-exact results

@@ -86,6 +86,29 @@ static int run_cpu() {
     try { naive_assign({1, 2}, 3); } catch (const std::invalid_argument& e) { ref_msg = e.what(); }
     try { b200::naive_assign({1, 2}, 3); } catch (const std::invalid_argument& e) { got_msg = e.what(); }
     EXPECT(!ref_msg.empty() && ref_msg == got_msg, "devices > heads: invalid_argument with the reference text");
+    // build_profiles (host path) vs the reference's on a bf16-exact workload.
+    {
+        std::mt19937_64 r2(11);
+        std::normal_distribution<double> N01(0.0, 1.0);
+        auto bf = [](double x) { return b200::from_bf16(b200::to_bf16(x)); };
+        AttentionWorkload w;
+        Matrix K(300, 128), V(300, 128);
+        for (auto& x : K.data) x = bf(N01(r2));
+        for (auto& x : V.data) x = bf(N01(r2));
+        for (int h = 0; h < 4; ++h) {
+            HeadData hd{Matrix(6, 128), K, V};
+            for (auto& x : hd.Q.data) x = bf(0.2 * N01(r2));
+            w.heads.push_back(hd);
+        }
+        const auto grid = default_budget_grid(300, 32);
+        const auto ref = build_profiles(w, grid, SelectionKind::PerQueryTopK, Provenance{"r", "t"});
+        const auto got = b200::build_profiles(w, grid);
+        double worst = 0.0;
+        for (int h = 0; h < 4; ++h)
+            for (size_t i = 0; i < grid.size(); ++i)
+                worst = std::max(worst, std::fabs(ref[h].curve.points[i].recovery - got[h].points[i].recovery));
+        EXPECT(worst < 1e-12, "build_profiles (host) vs reference");
+    }
     std::printf("cpu checks: %d failures\n", failures);
     return failures == 0 ? 0 : 1;
 }
@@ -123,6 +146,17 @@ static int run_gpu() {
         msg = e.what();
     }
     EXPECT(msg == "head 0: budget k = 0 out of range [1, 640]", "budget range message");
+    // build_profiles through the GPU profiler vs the host one (to rounding).
+    {
+        const auto grid = default_budget_grid(640, 64);
+        const auto host = b200::build_profiles(w, grid);
+        const auto gpu = b200::build_profiles(w, grid, &ctx);
+        double worst_p = 0.0;
+        for (size_t h = 0; h < host.size(); ++h)
+            for (size_t i = 0; i < grid.size(); ++i)
+                worst_p = std::max(worst_p, std::fabs(host[h].points[i].recovery - gpu[h].points[i].recovery));
+        EXPECT(worst_p < 1e-12, "build_profiles GPU vs host");
+    }
     std::printf("gpu checks: max abs %.3e, %d failures\n", worst, failures);
     return failures == 0 ? 0 : 1;
 }
