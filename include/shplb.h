@@ -175,7 +175,16 @@ int64_t shplb_ctx_launch_count(const shplb_ctx* ctx);
 int shplb_ctx_set_timing(shplb_ctx* ctx, int enable);
 int shplb_ctx_read_timing(shplb_ctx* ctx, double* stage_ms, int max_calls, int* n_calls_out);
 
-enum { SHPLB_BLOCK_TOPK = 0 }; /* selection kind: per (head, query block) top-k key blocks */
+/* Selection kind (SelectionKind, workload.cpp:14; attention.cpp:125-148), at
+ * block granularity:
+ *  SHPLB_BLOCK_TOPK            — PerQueryTopK: each (head, query block) keeps its
+ *                                own top-k visible key blocks by pooled score;
+ *  SHPLB_COLUMN_AGGREGATE_TOPK — ColumnAggregateTopK: each head keeps ONE set of k
+ *                                key blocks, those with the largest column sums of
+ *                                the block-softmax weights over all query blocks;
+ *                                each query block attends to the part it can see
+ *                                (possibly none: a zero output row). */
+enum { SHPLB_BLOCK_TOPK = 0, SHPLB_COLUMN_AGGREGATE_TOPK = 1 };
 
 /* One attention layer. q: bf16 [num_q_heads][seq_len][head_dim],
  * k/v: bf16 [num_kv_heads][seq_len][head_dim], out: bf16 like q; all dense,
@@ -189,7 +198,7 @@ typedef struct {
     int32_t block_q;   /* query block (pooling and FA tile rows): 128 */
     int32_t block_k;   /* key block (pooling and FA tile cols): 128 */
     int32_t causal;    /* top-left causal mask (attention.cpp:28-30) */
-    int32_t kind;      /* SHPLB_BLOCK_TOPK */
+    int32_t kind;      /* SHPLB_BLOCK_TOPK or SHPLB_COLUMN_AGGREGATE_TOPK */
     int32_t validate;  /* 1: scan q/k/v for NaN/Inf first (workload.cpp:56-58); synchronises */
     /* Optional host int32 [num_q_heads]: kv head read by each q head. NULL =
      * standard GQA grouping h / (num_q_heads/num_kv_heads). A rank under

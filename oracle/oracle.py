@@ -59,6 +59,11 @@ def _load_oracle():
         L.orc_topk_row.argtypes = [_f64p, i64, i64, _i64p]
         L.orc_block_sparse_attention.argtypes = [_u16p, _u16p, _u16p, i64, i64, i32, i32, i32,
                                                  C.c_int, _i32p, _i32p, i64, _f64p]
+        L.orc_det_ex2.argtypes = [C.c_float]
+        L.orc_det_ex2.restype = C.c_float
+        L.orc_colagg_select.argtypes = [_f32p, i64, i64, i32, i32, C.c_int, i64, i64, _i32p, _i32p]
+        L.orc_layer_kind.argtypes = [_u16p, _u16p, _u16p, i32, i32, i64, i64, i32, i32, i32, C.c_int,
+                                     C.c_int, _i64p, i64, _f32p, _i32p, _i32p, C.c_void_p]
         L.orc_layer.argtypes = [_u16p, _u16p, _u16p, i32, i32, i64, i64, i32, i32, i32, C.c_int,
                                 _i64p, i64, _f32p, _i32p, _i32p, C.c_void_p]
         L.orc_recovery_at.argtypes = [_i64p, _f64p, C.c_int64, C.c_int64]
@@ -205,6 +210,22 @@ def select_topk(scores: np.ndarray, n: int, bq: int, bk: int, causal: bool, k_bl
     return idx, cnt
 
 
+def colagg_select(scores: np.ndarray, n: int, bq: int, bk: int, causal: bool, k_blocks: int,
+                  kmax: int, n_k: int = None):
+    """Block-level ColumnAggregateTopK for one head (see orc_colagg_select)."""
+    nqb = nblocks(n, bq)
+    idx = np.empty((nqb, kmax), np.int32)
+    cnt = np.empty(nqb, np.int32)
+    _load_oracle().orc_colagg_select(np.ascontiguousarray(scores, np.float32), n,
+                                     n if n_k is None else n_k, bq, bk, int(causal), k_blocks,
+                                     kmax, idx, cnt)
+    return idx, cnt
+
+
+def det_ex2(x: float) -> float:
+    return float(_load_oracle().orc_det_ex2(x))
+
+
 def topk_row(values: np.ndarray, k: int) -> np.ndarray:
     values = np.ascontiguousarray(values, np.float64)
     out = np.empty(k, np.int64)
@@ -213,7 +234,7 @@ def topk_row(values: np.ndarray, k: int) -> np.ndarray:
 
 
 def layer(q_bits, k_bits, v_bits, k_blocks, *, bq=128, bk=128, causal=True, kmax=None,
-          with_output=True):
+          with_output=True, kind=0):
     """Whole layer: pooled scores, selections and fp64 outputs for every q head.
 
     q_bits [Hq, n_q, d], k_bits/v_bits [Hkv, n_k, d] (bf16 bit patterns);
@@ -232,9 +253,9 @@ def layer(q_bits, k_bits, v_bits, k_blocks, *, bq=128, bk=128, causal=True, kmax
     idx = np.empty((hq, nqb, kmax), np.int32)
     cnt = np.empty((hq, nqb), np.int32)
     out = np.empty((hq, n, d), np.float64) if with_output else None
-    _load_oracle().orc_layer(q_bits, k_bits, v_bits, hq, hkv, n, n_k, d, bq, bk, int(causal),
-                             k_blocks, kmax, scores, idx, cnt,
-                             out.ctypes.data if with_output else None)
+    _load_oracle().orc_layer_kind(q_bits, k_bits, v_bits, hq, hkv, n, n_k, d, bq, bk, int(causal),
+                                  int(kind), k_blocks, kmax, scores, idx, cnt,
+                                  out.ctypes.data if with_output else None)
     return scores, idx, cnt, out
 
 

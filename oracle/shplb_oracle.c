@@ -162,6 +162,87 @@ void orc_select_topk(const float* scores, int64_t n_q, int64_t n_k, int32_t bq, 
     free(buf);
 }
 
+/* --- ColumnAggregateTopK at block granularity (attention.cpp:66-73,136-148) --
+ * One key-block set per head, ranked by the column sums of the block-level
+ * attention weights: for every query block qb the softmax of its visible
+ * pooled scores, W[qb][kb] = e / Z with e = det_ex2((S - m) * log2 e) and Z the
+ * sum of e over kb ascending; c[kb] = sum of W over qb ascending; keep the
+ * k_h blocks with the largest c (value desc, index asc). Query block qb then
+ * attends to the kept blocks it can see (kept ∩ [0, vis(qb)), ascending); the
+ * reference keeps invisible keys too, with zero weight, so this is
+ * output-identical. det_ex2 is a fixed fp32 polynomial evaluated with the same
+ * IEEE operations here and on the GPU, so the sums — and the decisions — are
+ * bit-identical. */
+float orc_det_ex2(float x) {
+    if (!(x > -126.0f)) return 0.0f;
+    const float t = x + 12582912.0f;
+    const float j = t - 12582912.0f;
+    const float f = x - j;
+    float p = fmaf(1.3333558e-3f, f, 9.6181291e-3f);
+    p = fmaf(p, f, 5.5504109e-2f);
+    p = fmaf(p, f, 2.4022651e-1f);
+    p = fmaf(p, f, 6.9314718e-1f);
+    p = fmaf(p, f, 1.0f);
+    int32_t pb, tb;
+    memcpy(&pb, &p, 4);
+    memcpy(&tb, &t, 4);
+    pb += (int32_t)((uint32_t)tb << 23);
+    float r;
+    memcpy(&r, &pb, 4);
+    return r;
+}
+
+void orc_colagg_select(const float* scores, int64_t n_q, int64_t n_k, int32_t bq, int32_t bk,
+                       int causal, int64_t k_blocks, int64_t kmax, int32_t* idx, int32_t* cnt) {
+    const int64_t nqb = (n_q + bq - 1) / bq, nkb = (n_k + bk - 1) / bk;
+    const float log2e = 1.44269504088896340736f;
+    float* m = (float*)malloc(sizeof(float) * (size_t)nqb);
+    float* z = (float*)malloc(sizeof(float) * (size_t)nqb);
+    float* c = (float*)calloc((size_t)nkb, sizeof(float));
+    for (int64_t qb = 0; qb < nqb; ++qb) {
+        const int64_t vis = orc_visible_blocks(qb, n_q, n_k, bq, bk, causal);
+        const float* row = scores + qb * nkb;
+        float mx = -INFINITY;
+        for (int64_t j = 0; j < vis; ++j) mx = row[j] > mx ? row[j] : mx;
+        float sum = 0.0f;
+        for (int64_t j = 0; j < vis; ++j) sum = sum + orc_det_ex2((row[j] - mx) * log2e);
+        m[qb] = mx;
+        z[qb] = sum;
+    }
+    for (int64_t kb = 0; kb < nkb; ++kb) {
+        float acc = 0.0f;
+        for (int64_t qb = 0; qb < nqb; ++qb) {
+            if (kb >= orc_visible_blocks(qb, n_q, n_k, bq, bk, causal)) continue;
+            acc = acc + orc_det_ex2((scores[qb * nkb + kb] - m[qb]) * log2e) / z[qb];
+        }
+        c[kb] = acc;
+    }
+    const int64_t kk = k_blocks < nkb ? k_blocks : nkb;
+    scored* buf = (scored*)malloc(sizeof(scored) * (size_t)nkb);
+    for (int64_t j = 0; j < nkb; ++j) {
+        buf[j].v = c[j] + 0.0f;  /* -0.0 -> +0.0, as the GPU's order key */
+        buf[j].i = (int32_t)j;
+    }
+    qsort(buf, (size_t)nkb, sizeof(scored), cmp_desc);
+    int32_t* kept = (int32_t*)malloc(sizeof(int32_t) * (size_t)(kk > 0 ? kk : 1));
+    for (int64_t j = 0; j < kk; ++j) kept[j] = buf[j].i;
+    qsort(kept, (size_t)kk, sizeof(int32_t), cmp_i32);
+    for (int64_t qb = 0; qb < nqb; ++qb) {
+        const int64_t vis = orc_visible_blocks(qb, n_q, n_k, bq, bk, causal);
+        int32_t* r = idx + qb * kmax;
+        int64_t w = 0;
+        for (int64_t j = 0; j < kk; ++j)
+            if (kept[j] < vis) r[w++] = kept[j];
+        for (int64_t j = w; j < kmax; ++j) r[j] = -1;
+        cnt[qb] = (int32_t)w;
+    }
+    free(kept);
+    free(buf);
+    free(c);
+    free(z);
+    free(m);
+}
+
 /* Token-granular top-k on an arbitrary score row (value desc, index asc),
  * returned ascending: the reference's top_k_indices (attention.cpp:53-64). */
 void orc_topk_row(const double* values, int64_t n, int64_t k, int64_t* out) {
@@ -249,10 +330,10 @@ void orc_block_sparse_attention(const uint16_t* q, const uint16_t* k, const uint
  * attention.cpp:214-223). q: [hq][n_q][d], k/v: [hkv][n_k][d]; out
  * [hq][n_q][d]. The GPU path is prefill (n_q == n_k); the reference (and so
  * this restatement) also allows n_q != n_k. */
-void orc_layer(const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t hq, int32_t hkv,
-               int64_t n_q, int64_t n_k, int32_t d, int32_t bq, int32_t bk, int causal,
-               const int64_t* k_blocks, int64_t kmax, float* scores_out, int32_t* idx_out,
-               int32_t* cnt_out, double* out) {
+void orc_layer_kind(const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t hq, int32_t hkv,
+                    int64_t n_q, int64_t n_k, int32_t d, int32_t bq, int32_t bk, int causal, int kind,
+                    const int64_t* k_blocks, int64_t kmax, float* scores_out, int32_t* idx_out,
+                    int32_t* cnt_out, double* out) {
     const int64_t nqb = (n_q + bq - 1) / bq, nkb = (n_k + bk - 1) / bk;
     const int32_t group = hq / hkv;
 #pragma omp parallel for schedule(dynamic)
@@ -266,7 +347,10 @@ void orc_layer(const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t 
         orc_block_scores(qp, kp, n_q, n_k, d, bq, bk, causal, sc);
         int32_t* ix = idx_out + (int64_t)h * nqb * kmax;
         int32_t* ct = cnt_out + (int64_t)h * nqb;
-        orc_select_topk(sc, n_q, n_k, bq, bk, causal, k_blocks[h], kmax, ix, ct);
+        if (kind == 1)
+            orc_colagg_select(sc, n_q, n_k, bq, bk, causal, k_blocks[h], kmax, ix, ct);
+        else
+            orc_select_topk(sc, n_q, n_k, bq, bk, causal, k_blocks[h], kmax, ix, ct);
         if (out) {
             orc_block_sparse_attention(q + (int64_t)h * n_q * d, k + (int64_t)g * n_k * d,
                                        v + (int64_t)g * n_k * d, n_q, n_k, d, bq, bk, causal, ix,
@@ -275,6 +359,14 @@ void orc_layer(const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t 
         free(qp);
         free(kp);
     }
+}
+
+void orc_layer(const uint16_t* q, const uint16_t* k, const uint16_t* v, int32_t hq, int32_t hkv,
+               int64_t n_q, int64_t n_k, int32_t d, int32_t bq, int32_t bk, int causal,
+               const int64_t* k_blocks, int64_t kmax, float* scores_out, int32_t* idx_out,
+               int32_t* cnt_out, double* out) {
+    orc_layer_kind(q, k, v, hq, hkv, n_q, n_k, d, bq, bk, causal, 0, k_blocks, kmax, scores_out, idx_out,
+                   cnt_out, out);
 }
 
 /* --- budget table (allocator.cpp) ------------------------------------------ */

@@ -4,10 +4,10 @@ Host API over libshplb.so (C ABI: include/shplb.h). See DESIGN.md.
 """
 from ._native import (CudaError, InvalidArgument, LogicError, NotSupported, ShplbError,
                       ShplbRuntimeError, build, lib)
-from .api import (BLOCK, BLOCK_Q, HEAD_DIM, BudgetAllocation, Context, LoadReport, RecoveryCurve,
+from .api import (BLOCK, BLOCK_Q, BLOCK_TOPK, COLUMN_AGGREGATE_TOPK, HEAD_DIM, BudgetAllocation, Context, LoadReport, RecoveryCurve,
                   SimulationResult, barrier, default_budget_grid, greedy_assign, imbalance,
                   layer_work, maxmin_allocate, naive_assign, profile_curves, simulate,
-                  split_assign, uniform_allocate)
+                  selection_kind, split_assign, uniform_allocate)
 from . import formats  # noqa: E402  (allocation / assignment / profiles JSON, reference layout)
 from . import experiments  # noqa: E402  (sweep / skyline on measured latency)
 

@@ -222,10 +222,28 @@ def barrier(device_latency) -> SimulationResult:
 # Sparse attention on the GPU (attention.hpp)
 # ---------------------------------------------------------------------------
 
+BLOCK_TOPK = 0               # SHPLB_BLOCK_TOPK: PerQueryTopK at block granularity
+COLUMN_AGGREGATE_TOPK = 1    # SHPLB_COLUMN_AGGREGATE_TOPK: one kept key-block set per head
+_KINDS = {"per_query_topk": BLOCK_TOPK, "column_aggregate_topk": COLUMN_AGGREGATE_TOPK}
+
+
+def selection_kind(kind) -> int:
+    """SHPLB_* selection kind from an int or the reference's policy name
+    (selection_kind_from_string, workload.cpp:12-17, same error text)."""
+    if isinstance(kind, str):
+        if kind not in _KINDS:
+            from ._native import InvalidArgument
+            raise InvalidArgument(f'unknown selection policy "{kind}" '
+                                  "(expected per_query_topk or column_aggregate_topk)")
+        return _KINDS[kind]
+    return int(kind)
+
+
 def _shape(num_q_heads, num_kv_heads, seq_len, causal, validate=False, kv_map=None,
-           head_dim=HEAD_DIM, block_q=BLOCK_Q, q_block_range=None, gather=None) -> LayerShape:
-    sh = LayerShape(num_q_heads, num_kv_heads, seq_len, head_dim, block_q, BLOCK, int(causal), 0,
-                    int(validate), None, None, None, 0, None, 0)
+           head_dim=HEAD_DIM, block_q=BLOCK_Q, q_block_range=None, gather=None,
+           kind=BLOCK_TOPK) -> LayerShape:
+    sh = LayerShape(num_q_heads, num_kv_heads, seq_len, head_dim, block_q, BLOCK, int(causal),
+                    selection_kind(kind), int(validate), None, None, None, 0, None, 0)
     if gather is not None:  # (output buffer device pointers, global head of each local q head, total heads)
         ptrs, head_of_q, total = gather
         arr = (C.c_void_p * len(ptrs))(*[int(x) for x in ptrs])
@@ -338,14 +356,14 @@ class Context:
 
     # -- kernel 2 ---------------------------------------------------------
     def select_blocks(self, scores, k_blocks, n, causal=True, kmax=None, stream=None,
-                      block_q=BLOCK_Q):
+                      block_q=BLOCK_Q, kind=BLOCK_TOPK):
         import torch
         hq, nqb, _ = scores.shape
         kb = _i64(k_blocks)
         kmax = int(kb.max()) if kmax is None else int(kmax)
         idx = torch.empty((hq, nqb, kmax), dtype=torch.int32, device=scores.device)
         cnt = torch.empty((hq, nqb), dtype=torch.int32, device=scores.device)
-        sh = _shape(hq, 1, n, causal, block_q=block_q)
+        sh = _shape(hq, 1, n, causal, block_q=block_q, kind=kind)
         sh.num_kv_heads = 1
         check(lib().shplb_select_blocks(self._h, C.byref(sh), _dev_ptr(scores, "scores", torch.float32),
                                         _ptr(kb), kmax, _dev_ptr(idx, "idx"), _dev_ptr(cnt, "cnt"),
@@ -370,8 +388,9 @@ class Context:
     # -- the layer: kernels 1+2 fused, then 3 -----------------------------
     def sparse_attention_layer(self, q, k, v, budgets_tokens, causal=True, stream=None, out=None,
                                validate=False, kv_map=None, block_q=BLOCK_Q, q_block_range=None,
-                               gather=None):
-        """sparse_attention for every head with its own token budget. gather =
+                               gather=None, kind=BLOCK_TOPK):
+        """sparse_attention for every head with its own token budget under selection
+        `kind` (BLOCK_TOPK / COLUMN_AGGREGATE_TOPK or the policy name). gather =
         (device pointers of full output buffers, global head index of each local
         q head, total heads): kernel 3 writes every output row into each buffer
         (fused head-parallel gather over NVLink peer memory); `out` is unused."""
@@ -381,7 +400,7 @@ class Context:
         if b.size != hq:
             from ._native import InvalidArgument
             raise InvalidArgument(f"need one budget per query head ({hq}), got {b.size}")
-        sh = _shape(hq, k.shape[0], n, causal, validate, kv_map, d, block_q, q_block_range, gather)
+        sh = _shape(hq, k.shape[0], n, causal, validate, kv_map, d, block_q, q_block_range, gather, kind)
         self._last_block_q = block_q
         if gather is not None:
             out_ptr = None
@@ -410,7 +429,7 @@ class Context:
 
     def sparse_attention_layer_host(self, q, k, v, budgets_tokens, causal=True, out=None,
                                     stream=None, kv_map=None, block_q=BLOCK_Q, q_block_range=None,
-                                    asynchronous=False):
+                                    asynchronous=False, kind=BLOCK_TOPK):
         """The layer call on HOST bf16 tensors (pinned for async DMA): copy in,
         kernels 1-3, copy out, synchronise (shplb_sparse_attention_layer_host). With
         asynchronous=True nothing is synchronised (shplb_sparse_attention_layer_host_async):
@@ -425,7 +444,7 @@ class Context:
         if out is None:
             out = torch.empty_like(q)
         b = _i64(budgets_tokens)
-        sh = _shape(hq, k.shape[0], n, causal, False, kv_map, d, block_q, q_block_range)
+        sh = _shape(hq, k.shape[0], n, causal, False, kv_map, d, block_q, q_block_range, kind=kind)
         self._last_block_q = block_q
         fn = (lib().shplb_sparse_attention_layer_host_async if asynchronous
               else lib().shplb_sparse_attention_layer_host)

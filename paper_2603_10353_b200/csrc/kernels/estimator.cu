@@ -327,6 +327,113 @@ void launch_select_from_scores(const float* scores, int hq, int64_t n, int bq, b
 }
 
 namespace {
+// ---- ColumnAggregateTopK at block granularity (attention.cpp:136-148;
+// restated in oracle/shplb_oracle.c orc_colagg_select with the same IEEE ops).
+
+// 2^x, x <= 0, by a fixed fp32 polynomial (no MUFU: its result would differ
+// from the CPU's), 0 below -126.
+__device__ __forceinline__ float det_ex2(float x) {
+    if (!(x > -126.0f)) return 0.0f;
+    const float t = __fadd_rn(x, 12582912.0f);
+    const float j = __fsub_rn(t, 12582912.0f);
+    const float f = __fsub_rn(x, j);
+    float p = __fmaf_rn(1.3333558e-3f, f, 9.6181291e-3f);
+    p = __fmaf_rn(p, f, 5.5504109e-2f);
+    p = __fmaf_rn(p, f, 2.4022651e-1f);
+    p = __fmaf_rn(p, f, 6.9314718e-1f);
+    p = __fmaf_rn(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + static_cast<int>(static_cast<uint32_t>(__float_as_int(t)) << 23));
+}
+
+constexpr float kLog2e = 1.44269504088896340736f;
+
+// Per (head, query block): m = max visible score, z = sum of det_ex2((s - m) log2 e).
+__global__ void colagg_rowstats_kernel(const float* __restrict__ scores, int hq, int64_t nqb, int64_t nkb,
+                                       int64_t n, int bq, int causal, float* __restrict__ m_out,
+                                       float* __restrict__ z_out) {
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (row >= hq * nqb) return;
+    const int64_t vis = visible_blocks(row % nqb, n, nkb, bq, causal != 0);
+    const float* s = scores + row * nkb;
+    float mx = -INFINITY;
+    for (int64_t j = 0; j < vis; ++j) mx = s[j] > mx ? s[j] : mx;
+    float sum = 0.0f;
+    for (int64_t j = 0; j < vis; ++j) sum = __fadd_rn(sum, det_ex2(__fmul_rn(__fsub_rn(s[j], mx), kLog2e)));
+    m_out[row] = mx;
+    z_out[row] = sum;
+}
+
+// Per (head, key block): column sum of the block weights over query blocks, ascending.
+__global__ void colagg_colsum_kernel(const float* __restrict__ scores, const float* __restrict__ m,
+                                     const float* __restrict__ z, int hq, int64_t nqb, int64_t nkb, int64_t n,
+                                     int bq, int causal, float* __restrict__ c_out) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= hq * nkb) return;
+    const int64_t h = t / nkb, kb = t % nkb;
+    float acc = 0.0f;
+    for (int64_t qb = 0; qb < nqb; ++qb) {
+        if (kb >= visible_blocks(qb, n, nkb, bq, causal != 0)) continue;
+        const int64_t row = h * nqb + qb;
+        const float w = det_ex2(__fmul_rn(__fsub_rn(scores[row * nkb + kb], m[row]), kLog2e));
+        acc = __fadd_rn(acc, __fdiv_rn(w, z[row]));
+    }
+    c_out[t] = acc;
+}
+
+// One warp per head: the k_h key blocks with the largest column sums, ascending.
+__global__ void colagg_select_kernel(const float* __restrict__ c, int hq, int64_t nkb, HeadTable ht,
+                                     int64_t kmax, int32_t* __restrict__ kept, int32_t* __restrict__ kk_out) {
+    const int h = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+    if (h >= hq) return;
+    const int kk = static_cast<int>(min(static_cast<int64_t>(ht.k[h]), nkb));
+    const float* row = c + static_cast<int64_t>(h) * nkb;
+    warp_select_row([row](int j) { return order_key(row[j]); }, static_cast<int>(nkb), kk, kmax,
+                    kept + static_cast<int64_t>(h) * kmax);
+    if ((threadIdx.x & 31) == 0) kk_out[h] = kk;
+}
+
+// Per (head, query block): the head's kept blocks the query block can see.
+__global__ void colagg_fill_kernel(const int32_t* __restrict__ kept, const int32_t* __restrict__ kk, int hq,
+                                   int64_t nqb, int64_t nkb, int64_t kmax, int64_t n, int bq, int causal,
+                                   int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (row >= hq * nqb) return;
+    const int64_t h = row / nqb;
+    const int64_t vis = visible_blocks(row % nqb, n, nkb, bq, causal != 0);
+    const int32_t* kr = kept + h * kmax;
+    int32_t* out = idx + row * kmax;
+    int64_t w = 0;
+    for (int64_t j = 0; j < kk[h]; ++j)
+        if (kr[j] < vis) out[w++] = kr[j];
+    for (int64_t j = w; j < kmax; ++j) out[j] = -1;
+    cnt[row] = static_cast<int32_t>(w);
+}
+}  // namespace
+
+void launch_colagg_select(const float* scores, int hq, int64_t n, int bq, bool causal, const HeadTable& ht,
+                          int64_t kmax, float* work, int32_t* kept, int32_t* idx, int32_t* cnt, cudaStream_t s) {
+    const int64_t nqb = (n + bq - 1) / bq, nkb = (n + kBlock - 1) / kBlock;
+    float* m = work;
+    float* z = m + hq * nqb;
+    float* c = z + hq * nqb;
+    int32_t* kk = kept + hq * kmax;
+    const int cz = causal ? 1 : 0;
+    colagg_rowstats_kernel<<<static_cast<unsigned>((hq * nqb + 127) / 128), 128, 0, s>>>(scores, hq, nqb, nkb, n,
+                                                                                         bq, cz, m, z);
+    colagg_colsum_kernel<<<static_cast<unsigned>((hq * nkb + 127) / 128), 128, 0, s>>>(scores, m, z, hq, nqb,
+                                                                                       nkb, n, bq, cz, c);
+    colagg_select_kernel<<<static_cast<unsigned>((hq * 32 + 127) / 128), 128, 0, s>>>(c, hq, nkb, ht, kmax, kept,
+                                                                                       kk);
+    colagg_fill_kernel<<<static_cast<unsigned>((hq * nqb + 127) / 128), 128, 0, s>>>(kept, kk, hq, nqb, nkb, kmax,
+                                                                                     n, bq, cz, idx, cnt);
+}
+
+size_t colagg_work_floats(int hq, int64_t n, int bq) {
+    const int64_t nqb = (n + bq - 1) / bq, nkb = (n + kBlock - 1) / kBlock;
+    return static_cast<size_t>(hq) * (2 * nqb + nkb);
+}
+
+namespace {
 // Dense comparator selection: every causally visible key block, ascending.
 __global__ void dense_selection_kernel(int32_t* idx, int32_t* cnt, int64_t rows, int64_t nqb, int64_t nkb,
                                        int bq, int64_t n, int causal) {

@@ -78,6 +78,13 @@ void launch_profile_prefix(const double* sorted, int64_t units, int64_t n_k, con
 void launch_profile_rows(const double* mass, int hq, int64_t n_rows, const int64_t* grid, int64_t n_grid,
                          double* recovery, cudaStream_t s);
 
+// Block-level ColumnAggregateTopK from a score matrix [hq][nqb][nkb]: one kept
+// key-block set per head (largest block-weight column sums), each query block
+// gets its visible part. work: colagg_work_floats(...) floats; kept: hq*(kmax+1) int32.
+void launch_colagg_select(const float* scores, int hq, int64_t n, int bq, bool causal, const HeadTable& ht,
+                          int64_t kmax, float* work, int32_t* kept, int32_t* idx, int32_t* cnt, cudaStream_t s);
+size_t colagg_work_floats(int hq, int64_t n, int bq);
+
 // Dense comparator: idx [hq][nqb][nkb] = every visible key block ascending
 // (tail -1), cnt [hq][nqb] = visible count.
 void launch_dense_selection(int32_t* idx, int32_t* cnt, int hq, int64_t n, int bq, bool causal, cudaStream_t s);

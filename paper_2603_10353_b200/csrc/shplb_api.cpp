@@ -136,7 +136,8 @@ void check_shape(const shplb_layer_shape* s) {
         throw NotSupported("head_dim " + std::to_string(s->head_dim) + " not supported (kernels are built for 128)");
     if ((s->block_q != 128 && s->block_q != 256) || s->block_k != kern::kBlock)
         throw NotSupported("block sizes must be block_q in {128, 256}, block_k = 128");
-    if (s->kind != SHPLB_BLOCK_TOPK) throw NotSupported("selection kind not supported");
+    if (s->kind != SHPLB_BLOCK_TOPK && s->kind != SHPLB_COLUMN_AGGREGATE_TOPK)
+        throw NotSupported("selection kind " + std::to_string(s->kind) + " not supported");
     if (s->seq_len > int64_t(kern::kMaxKeyBlocks) * kern::kBlock) {
         throw NotSupported("seq_len " + std::to_string(s->seq_len) + " exceeds the selector's limit of " +
                            std::to_string(int64_t(kern::kMaxKeyBlocks) * kern::kBlock) + " tokens");
@@ -239,6 +240,11 @@ struct shplb_ctx {
     size_t prof_aux_bytes = 0;
     void* prof_temp = nullptr;
     size_t prof_temp_bytes = 0;
+    // ColumnAggregateTopK workspace: score matrix + row/column statistics, kept sets.
+    float* ca_ws = nullptr;
+    size_t ca_ws_bytes = 0;
+    int32_t* ca_kept = nullptr;
+    size_t ca_kept_bytes = 0;
     int64_t last_kmax = 0;
     int64_t last_rows = 0;  // Hq * nqb of the last layer call
     int64_t last_n = 0, last_nqb = 0;
@@ -318,6 +324,16 @@ void mark(shplb_ctx* ctx, int slot, cudaStream_t st) {
     if (slot == 3) ++ctx->timed_calls;
 }
 
+// Grows the ColumnAggregateTopK workspace; returns [scores | colagg work] floats.
+float* colagg_workspace(shplb_ctx* ctx, const shplb_layer_shape* s, int64_t kmax) {
+    const int64_t nqb = cdiv(s->seq_len, s->block_q), nkb = cdiv(s->seq_len, kern::kBlock);
+    const size_t floats = static_cast<size_t>(s->num_q_heads) * nqb * nkb +
+                          kern::colagg_work_floats(s->num_q_heads, s->seq_len, s->block_q);
+    grow(ctx->ca_ws, ctx->ca_ws_bytes, sizeof(float) * floats);
+    grow(ctx->ca_kept, ctx->ca_kept_bytes, sizeof(int32_t) * s->num_q_heads * (kmax + 1));
+    return ctx->ca_ws;
+}
+
 void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const void* k,
                     const kern::HeadTable& kb, int64_t kmax, float* scores_out, bool select,
                     int32_t* idx, int32_t* cnt, cudaStream_t st) {
@@ -329,9 +345,20 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
     kern::launch_pool(k, s->num_kv_heads, s->seq_len, kern::kBlock, ctx->kp, st);
     if (select) mark(ctx, 1, st);
     const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(s->head_dim)));
-    kern::launch_score_select(ctx->qp, ctx->kp, s->num_q_heads, s->num_kv_heads, s->seq_len, s->block_q,
-                              s->causal != 0, scale, kb, kmax, scores_out, select, idx, cnt, st);
-    check_launch(ctx, 3);
+    if (select && s->kind == SHPLB_COLUMN_AGGREGATE_TOPK) {
+        // One kept set per head from the full score matrix (attention.cpp:136-148).
+        const size_t n_scores = static_cast<size_t>(s->num_q_heads) * nqb * nkb;
+        float* ws = colagg_workspace(ctx, s, kmax);
+        kern::launch_score_select(ctx->qp, ctx->kp, s->num_q_heads, s->num_kv_heads, s->seq_len, s->block_q,
+                                  s->causal != 0, scale, kb, kmax, ws, false, nullptr, nullptr, st);
+        kern::launch_colagg_select(ws, s->num_q_heads, s->seq_len, s->block_q, s->causal != 0, kb, kmax,
+                                   ws + n_scores, ctx->ca_kept, idx, cnt, st);
+        check_launch(ctx, 3 + 4);
+    } else {
+        kern::launch_score_select(ctx->qp, ctx->kp, s->num_q_heads, s->num_kv_heads, s->seq_len, s->block_q,
+                                  s->causal != 0, scale, kb, kmax, scores_out, select, idx, cnt, st);
+        check_launch(ctx, 3);
+    }
     if (select) mark(ctx, 2, st);
 }
 
@@ -489,6 +516,8 @@ int shplb_ctx_destroy(shplb_ctx* ctx) {
         cudaFree(ctx->dense_idx);
         cudaFree(ctx->dense_cnt);
         cudaFree(ctx->prof_scores);
+        cudaFree(ctx->ca_ws);
+        cudaFree(ctx->ca_kept);
         cudaFree(ctx->prof_sorted);
         cudaFree(ctx->prof_mass);
         cudaFree(ctx->prof_aux);
@@ -570,10 +599,17 @@ int shplb_select_blocks(shplb_ctx* ctx, const shplb_layer_shape* shape, const fl
         }
         if (kmax < need) throw InvalidArgument("kmax " + std::to_string(kmax) + " < largest k " + std::to_string(need));
         DeviceGuard g(ctx->device);
-        kern::launch_select_from_scores(scores, shape->num_q_heads, shape->seq_len, shape->block_q,
-                                        shape->causal != 0,
-                                        kb, kmax, idx_out, cnt_out, static_cast<cudaStream_t>(stream));
-        check_launch(ctx);
+        auto st = static_cast<cudaStream_t>(stream);
+        if (shape->kind == SHPLB_COLUMN_AGGREGATE_TOPK) {
+            float* ws = colagg_workspace(ctx, shape, kmax);
+            kern::launch_colagg_select(scores, shape->num_q_heads, shape->seq_len, shape->block_q,
+                                       shape->causal != 0, kb, kmax, ws, ctx->ca_kept, idx_out, cnt_out, st);
+            check_launch(ctx, 4);
+        } else {
+            kern::launch_select_from_scores(scores, shape->num_q_heads, shape->seq_len, shape->block_q,
+                                            shape->causal != 0, kb, kmax, idx_out, cnt_out, st);
+            check_launch(ctx);
+        }
     });
 }
 
