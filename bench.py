@@ -64,7 +64,7 @@ def parse_args():
     p.add_argument("--layers", type=int, default=32,
                    help="distinct attention layers per step (C3: the 32-layer stack); each has its "
                         "own inputs, budget table and head plan")
-    p.add_argument("--e2e-layers", type=int, default=4,
+    p.add_argument("--e2e-layers", type=int, default=8,
                    help="layers timed through the host-buffer entry for e2e (ms/layer)")
     p.add_argument("--allocation-json", default=None,
                    help="budget table from an allocation.json (reference format) instead of profiling")

@@ -72,8 +72,11 @@ private:
 // the device (GQA). Inputs go through the host-buffer entry (copies in and out
 // are part of the call); selection is per (head, query block) over 128-key
 // blocks, b_h tokens keeping ceil(b_h / 128) blocks.
+// kind: PerQueryTopK -> SHPLB_BLOCK_TOPK, ColumnAggregateTopK -> SHPLB_COLUMN_AGGREGATE_TOPK
+// (one kept key-block set per head from block-softmax column sums).
 inline std::vector<Matrix> sparse_attention_all(Context& ctx, const AttentionWorkload& w,
-                                                const std::vector<long>& budgets, bool causal = true) {
+                                                const std::vector<long>& budgets, bool causal = true,
+                                                SelectionKind kind = SelectionKind::PerQueryTopK) {
     w.validate();  // the reference's shape / finiteness checks and messages
     if (budgets.size() != w.num_heads())
         throw std::invalid_argument("need one budget per head");
@@ -107,7 +110,7 @@ inline std::vector<Matrix> sparse_attention_all(Context& ctx, const AttentionWor
     s.block_q = 256;
     s.block_k = 128;
     s.causal = causal ? 1 : 0;
-    s.kind = SHPLB_BLOCK_TOPK;
+    s.kind = kind == SelectionKind::PerQueryTopK ? SHPLB_BLOCK_TOPK : SHPLB_COLUMN_AGGREGATE_TOPK;
     s.kv_head_of_q = kv_of_q.data();
     const std::vector<int64_t> b(budgets.begin(), budgets.end());
     check(shplb_sparse_attention_layer_host(ctx.get(), &s, q.data(), k.data(), v.data(), b.data(), o.data(),

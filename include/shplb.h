@@ -292,8 +292,13 @@ int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* s
 /* The same host-buffer layer call without the final synchronisation: returns
  * once the copies and kernels are queued; `stream` completes when the output is
  * back in out_host. Consecutive async calls alternate between two device
- * staging slots, so layer l+1's host->device copies overlap layer l's kernels
- * and device->host copy (a multi-layer prefill hides the PCIe time). Host
+ * staging slots and run their kernels on a context-owned stream that does not
+ * wait on `stream`, so layer l+1's host->device copies overlap layer l's
+ * kernels and layer l's device->host copy overlaps layer l+1's kernels (a
+ * multi-layer prefill hides the PCIe time). The first async call after any
+ * other call on the context orders itself after all work queued on `stream`;
+ * a chained call does not wait for work the caller queued on `stream` in
+ * between, so its host inputs must be complete when the call is made. Host
  * buffers must stay valid (pinned for async DMA) until the stream completes. */
 int shplb_sparse_attention_layer_host_async(shplb_ctx* ctx, const shplb_layer_shape* shape,
                                             const uint16_t* q_host, const uint16_t* k_host,

@@ -219,6 +219,8 @@ struct shplb_ctx {
     int32_t* flag = nullptr;
     void* host_io = nullptr;  // device staging for shplb_sparse_attention_layer_host
     cudaStream_t copy_in = nullptr, copy_out = nullptr;  // its H2D / D2H copy streams
+    cudaStream_t compute = nullptr;  // kernels of async host calls (see host_layer)
+    int64_t launches_after_async = -1;  // launch count right after the last async host call
     std::vector<cudaEvent_t> chunk_events;
     int host_slot = 1;                          // staging slot of the last async host call
     cudaEvent_t slot_done[2] = {nullptr, nullptr};  // slot's last user finished (kernels + D2H)
@@ -524,6 +526,7 @@ int shplb_ctx_destroy(shplb_ctx* ctx) {
         cudaFree(ctx->prof_temp);
         if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
         if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
+        if (ctx->compute) cudaStreamDestroy(ctx->compute);
         for (cudaEvent_t e : ctx->chunk_events) cudaEventDestroy(e);
         for (cudaEvent_t e : ctx->slot_done)
             if (e) cudaEventDestroy(e);
@@ -701,10 +704,15 @@ int shplb_dense_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, 
 }
 
 namespace {
-// Host-buffer layer call. Synchronous: one staging slot, waits for earlier
-// work on `stream`, synchronises at the end. Asynchronous: staging alternates
-// between two slots, a call's copies wait only for the call two back (which
-// used the same slot), so layer l+1's H2D overlaps layer l's compute and D2H.
+// Host-buffer layer call. Synchronous: one staging slot, copies and kernels
+// ordered after earlier work on `stream`, synchronised at the end.
+// Asynchronous: staging alternates between two slots; the kernels run on the
+// context's compute stream and `stream` only waits for the call's last D2H.
+// Consecutive async calls therefore never wait on `stream` (it carries the
+// D2H waits): layer l+1's H2D overlaps layer l's kernels, and layer l+1's
+// kernels overlap layer l's D2H. A call's copies wait only for the call two
+// back (same slot); when other work used the context since the last async
+// call, the call first orders itself after everything queued on `stream`.
 int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q_host,
                const uint16_t* k_host, const uint16_t* v_host, const int64_t* budgets_tokens,
                uint16_t* out_host, void* stream, bool async_call) {
@@ -747,7 +755,11 @@ int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q
         fill_kv_map(shape, map);
         bool monotone = true;
         for (int32_t h = 1; h < hq; ++h) monotone &= map.kv[h] >= map.kv[h - 1];
-        const int32_t chunks = monotone ? std::min<int32_t>(hkv, 8) : 1;
+        static const int32_t max_chunks = [] {  // SHPLB_HOST_CHUNKS: pipeline depth (default 8)
+            const char* e = std::getenv("SHPLB_HOST_CHUNKS");
+            return e ? std::max(1, std::atoi(e)) : 8;
+        }();
+        const int32_t chunks = monotone ? std::min<int32_t>(hkv, max_chunks) : 1;
         auto q_begin = [&](int32_t g) {  // first q head whose kv head is >= g
             int32_t h = 0;
             while (h < hq && map.kv[h] < g) ++h;
@@ -756,7 +768,11 @@ int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q
         if (!ctx->copy_in) {
             SHPLB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking));
             SHPLB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking));
+            SHPLB_CUDA(cudaStreamCreateWithFlags(&ctx->compute, cudaStreamNonBlocking));
         }
+        // Kernels: the caller's stream (sync) or the context's compute stream (async).
+        cudaStream_t ks = async_call ? ctx->compute : st;
+        const bool chained = async_call && ctx->launches_after_async == ctx->launches.load();
         while (ctx->chunk_events.size() < 3 * static_cast<size_t>(chunks) + 1) {
             cudaEvent_t e;
             SHPLB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -765,16 +781,17 @@ int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q
         for (cudaEvent_t& e : ctx->slot_done) {
             if (!e) SHPLB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
-        if (async_call) {
+        if (chained) {
             // The slot's previous user (two calls back) must have finished its
             // kernels and its D2H before this call's H2D overwrites the slot.
             SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_in, ctx->slot_done[slot], 0));
             SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_out, ctx->slot_done[slot], 0));
         } else {
             cudaEvent_t start = ctx->chunk_events[0];
-            SHPLB_CUDA(cudaEventRecord(start, st));  // copies may not overtake earlier work on `st`
+            SHPLB_CUDA(cudaEventRecord(start, st));  // nothing may overtake earlier work on `st`
             SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_in, start, 0));
             SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_out, start, 0));
+            if (async_call) SHPLB_CUDA(cudaStreamWaitEvent(ks, start, 0));
         }
         const size_t row_bytes = sizeof(uint16_t) * shape->seq_len * shape->head_dim;  // one head
         for (int32_t c = 0; c < chunks; ++c) {
@@ -791,7 +808,7 @@ int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q
             SHPLB_CUDA(cudaMemcpyAsync(base + v_off + g0 * row_bytes, v_host + g0 * row_bytes / 2,
                                        (g1 - g0) * row_bytes, cudaMemcpyHostToDevice, ctx->copy_in));
             SHPLB_CUDA(cudaEventRecord(in_done, ctx->copy_in));
-            SHPLB_CUDA(cudaStreamWaitEvent(st, in_done, 0));
+            SHPLB_CUDA(cudaStreamWaitEvent(ks, in_done, 0));
             shplb_layer_shape cs = *shape;
             cs.num_q_heads = h1 - h0;
             cs.num_kv_heads = g1 - g0;
@@ -799,22 +816,28 @@ int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q
             if (shape->q_block_range) cs.q_block_range = shape->q_block_range + 2 * h0;
             rc = shplb_sparse_attention_layer(ctx, &cs, base + q_off + h0 * row_bytes,
                                               base + k_off + g0 * row_bytes, base + v_off + g0 * row_bytes,
-                                              budgets_tokens + h0, base + o_off + h0 * row_bytes, stream);
+                                              budgets_tokens + h0, base + o_off + h0 * row_bytes, ks);
             if (rc != SHPLB_OK) {  // message already recorded; drain before returning
                 cudaStreamSynchronize(ctx->copy_in);
-                cudaStreamSynchronize(st);
+                cudaStreamSynchronize(ks);
+                ctx->launches_after_async = -1;
                 return;
             }
-            SHPLB_CUDA(cudaEventRecord(comp_done, st));
+            SHPLB_CUDA(cudaEventRecord(comp_done, ks));
             SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_out, comp_done, 0));
             SHPLB_CUDA(cudaMemcpyAsync(out_host + h0 * row_bytes / 2, base + o_off + h0 * row_bytes,
                                        (h1 - h0) * row_bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
         }
-        cudaEvent_t out_done = ctx->chunk_events[3];
-        SHPLB_CUDA(cudaEventRecord(out_done, ctx->copy_out));
-        SHPLB_CUDA(cudaStreamWaitEvent(st, out_done, 0));  // `stream` completes after the last D2H
-        SHPLB_CUDA(cudaEventRecord(ctx->slot_done[slot], st));
-        if (!async_call) SHPLB_CUDA(cudaStreamSynchronize(st));
+        // The last D2H follows every chunk's kernels, so its completion means the
+        // slot is free and the output is back.
+        SHPLB_CUDA(cudaEventRecord(ctx->slot_done[slot], ctx->copy_out));
+        SHPLB_CUDA(cudaStreamWaitEvent(st, ctx->slot_done[slot], 0));  // `stream` completes after it
+        if (async_call) {
+            ctx->launches_after_async = ctx->launches.load();
+        } else {
+            SHPLB_CUDA(cudaStreamSynchronize(st));
+            ctx->launches_after_async = -1;
+        }
     });
     return rc != SHPLB_OK ? rc : err;
 }

@@ -139,6 +139,13 @@ static int run_gpu() {
         for (size_t i = 0; i < ref.data.size(); ++i) worst = std::max(worst, std::fabs(ref.data[i] - out[h].data[i]));
     }
     EXPECT(worst <= 2e-2, "GPU layer at full budget vs reference dense_attention (max abs 2e-2)");
+    {  // ColumnAggregateTopK at full budget keeps every visible block too
+        const auto ca = b200::sparse_attention_all(ctx, w, std::vector<long>(4, static_cast<long>(n)), true,
+                                                   SelectionKind::ColumnAggregateTopK);
+        bool same = true;
+        for (int h = 0; h < 4; ++h) same = same && ca[h].data == out[h].data;
+        EXPECT(same, "ColumnAggregateTopK at full budget == PerQueryTopK");
+    }
     std::string msg;
     try {
         b200::sparse_attention_all(ctx, w, {0, 1, 1, 1}, true);

@@ -299,6 +299,39 @@ def test_async_host_entry_matches_sync_over_layers(cuda_ctx):
         assert torch.equal(a, s_)
 
 
+def test_async_host_entry_interleaved_with_device_calls(cuda_ctx):
+    """Async host calls run their kernels on the context's own stream; device
+    calls on the caller's stream in between (sharing the context workspace)
+    must stay ordered with them. Six layers, chains of 1-3 async calls broken by device
+    calls, every output checked against the synchronous device call."""
+    stream = torch.cuda.Stream()
+    layers = []
+    for li in range(6):
+        q, k, v = make_layer(LayerSpec(num_q_heads=4, num_kv_heads=2, seq_len=1024 + 128 * li, seed=60 + li), "cpu")
+        b = np.array([128, 384, 1024, 256], np.int64)
+        layers.append((q, k, v, b))
+    want = []
+    for q, k, v, b in layers:
+        want.append(cuda_ctx.sparse_attention_layer(q.cuda(), k.cuda(), v.cuda(), b).cpu())
+    torch.cuda.synchronize()
+    got, dev_got = {}, {}
+    plan = ["a", "a", "d", "a", "a", "a", "d", "a"]  # async host / device call, cycling the layers
+    with torch.cuda.stream(stream):
+        for i, kind in enumerate(plan):
+            q, k, v, b = layers[i % 6]
+            if kind == "a":
+                o = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+                got[i] = cuda_ctx.sparse_attention_layer_host(q.pin_memory(), k.pin_memory(), v.pin_memory(), b,
+                                                              stream=stream, out=o, asynchronous=True)
+            else:
+                dev_got[i] = cuda_ctx.sparse_attention_layer(q.cuda(), k.cuda(), v.cuda(), b, stream=stream)
+    stream.synchronize()
+    for i, o in got.items():
+        assert torch.equal(o, want[i % 6]), f"async call {i}"
+    for i, o in dev_got.items():
+        assert torch.equal(o.cpu(), want[i % 6]), f"device call {i}"
+
+
 def test_max_heads_per_call(cuda_ctx):
     """256 q heads (kMaxHeads: the per-launch head table) in one call, against the
     oracle; 257 is refused with NotSupported."""
