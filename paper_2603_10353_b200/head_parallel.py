@@ -142,6 +142,19 @@ def gather_heads(local_out, device_of_head, world: int, group=None):
     return _gather(local_out, gather_map(np.asarray(device_of_head), world, local_out.shape[1]), world, group)
 
 
+def agree_outcomes(ok: bool, payload, world: int, group=None) -> list:
+    """[(ok, payload)] of every rank (all_gather_object): a setup step that can
+    fail on one rank only (IPC export / open) is judged collectively, so a
+    failure anywhere makes ALL ranks raise and fall back together instead of
+    one rank entering a collective the others never reach."""
+    if world == 1:
+        return [(ok, payload)]
+    import torch.distributed as dist
+    res = [None] * world
+    dist.all_gather_object(res, (ok, payload), group=group)
+    return res
+
+
 class PeerOutputs:
     """Full-layer output buffers [Hq, n, d] on every rank, mapped into every
     other rank (CUDA IPC over NVLink) for the fused gather: kernel 3 stores each
@@ -162,27 +175,44 @@ class PeerOutputs:
         import torch
         import torch.distributed as dist
 
-        from ._native import check, lib
+        from ._native import ShplbError, check, lib
         self.world, self.rank, self.device = world, rank, torch.device(device)
         self.buffer = torch.empty((sets, num_heads, seq_len, head_dim), dtype=torch.bfloat16, device=self.device)
         self.local = [self.buffer[b] for b in range(sets)]
         set_bytes = num_heads * seq_len * head_dim * 2
-        hnd = (C.c_char * self.HANDLE_BYTES)()
-        check(lib().shplb_ipc_handle(C.c_void_p(self.buffer.data_ptr()), hnd, self.HANDLE_BYTES))
-        handles = [bytes(hnd)]
-        if world > 1:
-            handles = [None] * world
-            dist.all_gather_object(handles, bytes(hnd), group=group)
-        bases = [self.buffer.data_ptr()]
         self._opened = []
+
+        def agree(ok: bool, payload):
+            return agree_outcomes(ok, payload, world, group)
+
+        hnd = (C.c_char * self.HANDLE_BYTES)()
+        try:
+            check(lib().shplb_ipc_handle(C.c_void_p(self.buffer.data_ptr()), hnd, self.HANDLE_BYTES))
+            mine = (True, bytes(hnd))
+        except ShplbError as e:
+            mine = (False, f"rank {rank}: {e}")
+        handles = agree(*mine)
+        bad = [m for ok, m in handles if not ok]
+        if bad:
+            raise ShplbError("; ".join(bad))
+        bases = [self.buffer.data_ptr()]
+        err = None
         for r in range(world):
             if r == rank:
                 continue
             out = C.c_void_p()
-            buf = (C.c_char * self.HANDLE_BYTES).from_buffer_copy(handles[r])
-            check(lib().shplb_ipc_open(self.device.index or 0, buf, self.HANDLE_BYTES, C.byref(out)))
+            buf = (C.c_char * self.HANDLE_BYTES).from_buffer_copy(handles[r][1])
+            try:
+                check(lib().shplb_ipc_open(self.device.index or 0, buf, self.HANDLE_BYTES, C.byref(out)))
+            except ShplbError as e:
+                err = f"rank {rank} opening rank {r}'s buffer: {e}"
+                break
             self._opened.append(out.value)
             bases.append(out.value)
+        bad = [m for ok, m in agree(err is None, err) if not ok]
+        if bad:
+            self.close()
+            raise ShplbError("; ".join(bad))
         self._ptrs = [[base + b * set_bytes for base in bases] for b in range(sets)]
 
     def ptrs(self, b: int) -> list:

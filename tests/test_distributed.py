@@ -12,8 +12,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import paper_2603_10353_b200 as P
-from paper_2603_10353_b200.head_parallel import (gather_heads, gather_segments, head_counts,
-                                                  rank_segments, rank_shard)
+from paper_2603_10353_b200.head_parallel import (agree_outcomes, gather_heads, gather_segments,
+                                                  head_counts, rank_segments, rank_shard)
 
 
 def _free_port():
@@ -85,3 +85,30 @@ def test_head_parallel_world2_gloo():
     assert g_T <= n_T and g_bub <= n_bub  # the balancer never does worse here
     assert g_T == max(P.imbalance(budgets, P.greedy_assign(budgets, 2), 2).loads)
     assert results["split_heads"] <= 1  # at most D-1 heads are split
+
+
+def _agree_worker(rank, world, port, results):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # rank 1 fails its (IPC) setup step, rank 0 succeeds: both must see it
+        out = agree_outcomes(rank != 1, "h0" if rank != 1 else "rank 1: open failed", world)
+        results[rank] = [ok for ok, _ in out], [m for ok, m in out if not ok]
+        # and the ranks stay in lock-step afterwards (the NCCL fallback's collectives)
+        t = torch.tensor([rank + 1.0])
+        dist.all_reduce(t)
+        results[("sum", rank)] = float(t)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_gather_setup_failure_is_collective():
+    """PeerOutputs judges IPC setup collectively (agree_outcomes): a failure on
+    one rank makes every rank fall back to the NCCL gather together."""
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_agree_worker, args=(2, _free_port(), results), nprocs=2, join=True)
+    for r in range(2):
+        assert results[r] == ([True, False], ["rank 1: open failed"])
+        assert results[("sum", r)] == 3.0
