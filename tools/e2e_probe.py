@@ -96,7 +96,17 @@ def main():
         for o in outs:
             o.copy_(out, non_blocking=True)
 
-    res = {"layers": L, "host_chunks": os.environ.get("SHPLB_HOST_CHUNKS", "8"),
+    stage = {}
+    for name, fn in (("full", dev), ("chunked", dev_chunked)):
+        fn()
+        torch.cuda.synchronize()
+        ctx.set_timing(True)
+        fn()
+        torch.cuda.synchronize()
+        t = ctx.read_timing()
+        ctx.set_timing(False)
+        stage[name] = [round(float(x) / L, 3) for x in t.sum(0)]  # k1, k2, k3 ms per layer
+    res = {"layers": L, "stages_ms_per_layer": stage, "host_chunks": os.environ.get("SHPLB_HOST_CHUNKS", "8"),
            "dev_ms_per_layer": timed(dev) / L, "dev_chunked_ms_per_layer": timed(dev_chunked) / L,
            "dev_chunked_2streams_ms_per_layer": timed(dev_chunked_2ctx) / L,
            "e2e_ms_per_layer": timed(e2e) / L,
