@@ -80,6 +80,10 @@ def parse_args():
     p.add_argument("--gather", choices=["nccl", "p2p"], default="p2p",
                    help="N>1 output reassembly: NCCL all-gather + reorder on a comm stream, or the "
                         "fused gather (kernel 3 stores rows into every rank's buffer over NVLink)")
+    p.add_argument("--placement", choices=["greedy", "split"], default="split",
+                   help="N>1 headline plan: 'greedy' = the reference's whole-head greedy_assign (LPT on "
+                        "budgets, bit-exact); 'split' = the sub-head balancer (shplb_plan_split). "
+                        "All plans are timed and reported either way")
     p.add_argument("--force-gather", action="store_true",
                    help="validation: run the overlapped all-gather pipeline even at N=1 (1-rank NCCL group)")
     p.add_argument("--debug-one-device", action="store_true",
@@ -447,7 +451,8 @@ def time_e2e(ctx, shards, steps, warmup, world, stream):
     def step():  # layer l+1's H2D overlaps layer l's kernels and D2H (async host entry)
         for ls, (hq_, hk_, hv_), o in zip(shards, host, outs):
             ctx.sparse_attention_layer_host(hq_, hk_, hv_, ls.budgets, causal=True, out=o,
-                                            stream=stream, kv_map=ls.kv_map, asynchronous=True)
+                                            stream=stream, kv_map=ls.kv_map, q_block_range=ls.ranges,
+                                            asynchronous=True)
         stream.synchronize()
 
     for _ in range(warmup):
@@ -572,7 +577,15 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(args, budgets_desc):
+PLACEMENTS = {
+    "greedy": "greedy (LPT) whole-head plan (greedy_assign, bit-exact with the reference)",
+    "split": ("sub-head balancer (shplb_plan_split): heads in index order with exact tile costs, cut "
+              "McNaughton-style at query-block boundaries, at most D-1 heads split; the reference's "
+              "whole-head greedy plan is timed alongside (greedy_whole_head)"),
+}
+
+
+def config_dict(args, budgets_desc, headline="greedy"):
     return {
         "workload": (f"C3: Llama-3-8B-shaped {args.layers}-layer attention stack ({args.q_heads} Q / "
                      f"{args.kv_heads} KV heads, d=128), {args.seq_len}-token causal prefill, "
@@ -581,7 +594,7 @@ def config_dict(args, budgets_desc):
         "layers": args.layers,
         "seq_len": args.seq_len, "q_heads": args.q_heads, "kv_heads": args.kv_heads,
         "head_dim": 128, "budget_fraction": args.budget_fraction, "budgets": budgets_desc,
-        "placement": "greedy (LPT) head plan",
+        "placement": PLACEMENTS[headline],
         "l2": "each layer's inputs (1.5 GiB at 128K) exceed the 126 MB L2; layers run back to back",
     }
 
@@ -632,6 +645,7 @@ def main():
     if world > 1:
         plans_l["naive"] = [P.naive_assign(b, world) for b in budgets_l]
         plans_l["split"] = [P.split_assign(b, world, n) for b in budgets_l]
+    headline = args.placement if world > 1 else "greedy"  # at N = 1 every plan is the whole layer
     results = {}
     for name, plans in plans_l.items():
         shards = []
@@ -642,7 +656,7 @@ def main():
             else:
                 sh = rank_shard(plan, rank, group, b)
                 shards.append(LayerShard(q, k, v, sh, None, len(sh.heads) == hq))
-        sampler = ClockSampler(local) if (name == "greedy") else None
+        sampler = ClockSampler(local) if (name == headline) else None
         if sampler:
             sampler.start()
         ms, stages, launches, _ = time_stack(ctx, shards, args.steps, args.warmup, world, stream)
@@ -673,7 +687,7 @@ def main():
                 res["gather_kind"] = "nccl"
                 res["ms_with_gather"] = time_stack_gathered(ctx, shards, plans, max(2, args.steps // 2),
                                                             1, world, stream)
-        if name == "greedy" and not args.no_e2e:
+        if name == headline and not args.no_e2e:
             e2e_ms, h2d, d2h = time_e2e(ctx, shards[:max(1, args.e2e_layers)], max(2, args.steps // 2), 1,
                                         world, stream)
             res["e2e"] = (max(allgather_float(e2e_ms, world)), h2d, d2h)
@@ -695,7 +709,7 @@ def main():
             projection.setdefault(str(r.degree), {})[r.assigner] = {
                 "barrier_ms": round(r.barrier_latency, 3), "bubble": round(r.bubble_fraction, 4),
                 "speedup_vs_naive": round(r.speedup_vs_naive, 4)}
-    g = results["greedy"]
+    g = results[headline]
     flops_total = g["flops_total"]
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -730,7 +744,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(value * args.layers, 3), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded bf16 Q/K/V with per-head temperature, block-local structure)",
-        "config": config_dict(args, "max-min (calibration-profiled curves), quantum 128, floor 128"),
+        "config": config_dict(args, "max-min (calibration-profiled curves), quantum 128, floor 128", headline),
         "tflops": round(flops_total / (value * 1e-3) / 1e12, 1),
         "layers_per_step": args.layers,
         "compute_only_ms": round(g["ms"], 3),
@@ -770,6 +784,13 @@ def main():
                                  "load_imbalance": round(nv["load_imbalance"], 4)}
         line["speedup_vs_even_hp"] = round(_vg(nv) / value, 4)
         line["speedup_vs_even_hp_compute_only"] = round(nv["ms"] / g["ms"], 4)
+        gr = results["greedy"]
+        line["greedy_whole_head"] = {"ms": round(_vg(gr), 3), "compute_only_ms": round(gr["ms"], 3),
+                                     "bubble": round(gr["bubble"], 4),
+                                     "per_rank_ms": [round(x, 3) for x in gr["per_rank_ms"]],
+                                     "speedup_vs_even_hp": round(_vg(nv) / _vg(gr), 4),
+                                     "load_imbalance": round(gr["load_imbalance"], 4),
+                                     "plan": "the reference's greedy_assign (LPT on budgets), bit-exact"}
         spl = results["split"]
         line["split_subhead"] = {"ms": round(_vg(spl), 3), "compute_only_ms": round(spl["ms"], 3),
                                  "bubble": round(spl["bubble"], 4),

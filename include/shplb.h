@@ -122,11 +122,12 @@ int shplb_plan_greedy(const int64_t* budgets, int32_t num_heads, int32_t devices
  * heads over 8 GPUs under max-min budgets; this plan lets a head's query
  * blocks be split across devices. Cost of query block qb of head h =
  * min(ceil(b_h/128), visible key blocks(qb)) x (query halves holding rows),
- * the 128x128 tiles kernel 3 computes for it. Heads are laid out in LPT order
- * (cost desc, index asc) and cut McNaughton-style at the running target
- * ceil(total/D): device d receives a contiguous run of (head, [qb_begin,
- * qb_end)) segments, at most D-1 heads are split, and every load is within
- * one query block's cost of total/D. Outputs up to max_segments segments
+ * the 128x128 tiles kernel 3 computes for it. Heads are walked in index order
+ * (GQA groups stay contiguous, so a rank needs few kv heads) and cut
+ * McNaughton-style: device d takes the units whose cost midpoint falls in
+ * [d*total/D, (d+1)*total/D) of the running prefix, so device d receives a
+ * contiguous run of (head, [qb_begin, qb_end)) segments, at most D-1 heads are
+ * split, and every load is within half a query block's cost of total/D. Outputs up to max_segments segments
  * (seg_device/head/qb_begin/qb_end), *n_segments, and per-device costs
  * loads_out[devices] in tiles. */
 int shplb_plan_split(const int64_t* budgets, int32_t num_heads, int64_t seq_len, int32_t block_q,
