@@ -159,7 +159,9 @@ int shplb_barrier(const double* device_latency, int32_t devices, double* barrier
  * Block-sparse attention on sm_100a  (reference: proj/include/headbal/attention.hpp)
  * ====================================================================== */
 
-/* One context per CUDA device (rank). Owns the device workspace. The budget-
+/* One context per CUDA device (rank). Owns the device workspace. (No reference
+ * counterpart: the reference is pure value semantics with no handles, SURVEY
+ * §8 b2; the context is where its per-call allocations went.) The budget-
  * table, plan and metric functions are pure and reentrant like the reference's
  * (SPEC: no shared mutable state); a context is not: calls on one context must
  * not overlap across host threads (use one context per thread or stream). */
@@ -230,14 +232,18 @@ typedef struct {
  * the pointer's offset inside that allocation), map a peer's handle into this
  * process (P2P over NVLink; returns the peer's pointer, offset applied), unmap
  * it. A handle cannot be opened in the process that made it, and an allocation
- * is opened at most once per process (export one buffer per rank). */
+ * is opened at most once per process (export one buffer per rank). No
+ * reference counterpart (the reference has no distributed code); together with
+ * shplb_layer_shape.out_peers this replaces the paper's NCCL all-gather of
+ * per-head outputs. */
 #define SHPLB_IPC_HANDLE_BYTES 72
 int shplb_ipc_handle(const void* dev_ptr, void* handle_out, size_t handle_bytes);
 int shplb_ipc_open(int device, const void* handle, size_t handle_bytes, void** dev_ptr_out);
 int shplb_ipc_close(int device, void* dev_ptr);
 
 /* Kernel 1 — block-importance estimator. Mean-pools q/k blocks (fp32,
- * fixed summation order) and scores pooled q.k * (1/sqrt(d)).
+ * fixed summation order) and scores pooled q.k * (1/sqrt(d)):
+ * score_row (attention.cpp:17-31) at block granularity.
  * scores_out: fp32 device [num_q_heads][ceil(n/bq)][ceil(n/bk)], causally
  * invisible blocks = -inf. (Exposed for parity; the layer call fuses it.) */
 int shplb_block_scores(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
@@ -284,7 +290,9 @@ int shplb_dense_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, 
  * host->device into context-owned device memory, runs kernels 1-3, copies out
  * device->host and synchronises the stream. Pinned host memory makes the
  * copies asynchronous DMA. This is the entry a host-side caller of the
- * reference API binds. */
+ * reference API binds: it replaces the per-head
+ * sparse_attention(head, {kind, b_h}, causal) loop of run_skyline
+ * (commands.cpp:464-470) on the reference's host-resident HeadData. */
 int shplb_sparse_attention_layer_host(shplb_ctx* ctx, const shplb_layer_shape* shape,
                                       const uint16_t* q_host, const uint16_t* k_host,
                                       const uint16_t* v_host, const int64_t* budgets_tokens,
