@@ -568,7 +568,8 @@ def run_reference(args):
         "value": round(value, 3), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(value * args.layers, 3), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args, "uniform (reference uniform_allocate, same total B)"),
+        "config": config_dict(args, "uniform (reference uniform_allocate, same total B)",
+                              args.placement if world > 1 else "greedy"),
         "cpu_baseline": {"value": round(value, 3), "unit": "ms", "cores": threads,
                          "kind": "reference", "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "ms", "h2d_bytes_per_step": 0,
