@@ -21,7 +21,7 @@ resident in HBM (48 GiB for 32 layers; every layer's 1.5 GiB exceeds the
 at N > 1 it includes each layer's output all-gather, overlapped with the next
 layer's compute (`compute_only_ms` without it). Timing: W warm-up steps, then
 K steps bracketed by barrier + synchronize, CUDA events on the launching
-stream. `e2e` runs the first --e2e-layers layers through the public
+stream. `e2e` runs the stack (or its first --e2e-layers layers) through the public
 host-buffer API with inputs copied host(pinned)->device and the output
 device->host inside the timed region, every step (ms per layer).
 
@@ -64,8 +64,9 @@ def parse_args():
     p.add_argument("--layers", type=int, default=32,
                    help="distinct attention layers per step (C3: the 32-layer stack); each has its "
                         "own inputs, budget table and head plan")
-    p.add_argument("--e2e-layers", type=int, default=8,
-                   help="layers timed through the host-buffer entry for e2e (ms/layer)")
+    p.add_argument("--e2e-layers", type=int, default=0,
+                   help="layers timed through the host-buffer entry for e2e (ms/layer); 0 = the whole "
+                        "stack (--layers), i.e. the same step as `value`")
     p.add_argument("--allocation-json", default=None,
                    help="budget table from an allocation.json (reference format) instead of profiling")
     p.add_argument("--assignment-json", default=None,
@@ -444,7 +445,12 @@ def time_e2e(ctx, shards, steps, warmup, world, stream):
     synchronised — every step. Returns ms per layer and bytes per layer."""
     import torch
     shards = [ls for ls in shards if ls.heads]
-    host = [tuple(t.cpu().pin_memory() for t in (ls.q, ls.k, ls.v)) for ls in shards]
+    def pinned(t):  # device -> pinned host by DMA (no pageable staging copy)
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        return h
+
+    host = [tuple(pinned(t) for t in (ls.q, ls.k, ls.v)) for ls in shards]
 
     outs = [torch.empty(ls.q.shape, dtype=ls.q.dtype, pin_memory=True) for ls in shards]  # per layer
 
@@ -689,7 +695,7 @@ def main():
                 res["ms_with_gather"] = time_stack_gathered(ctx, shards, plans, max(2, args.steps // 2),
                                                             1, world, stream)
         if name == headline and not args.no_e2e:
-            e2e_ms, h2d, d2h = time_e2e(ctx, shards[:max(1, args.e2e_layers)], max(2, args.steps // 2), 1,
+            e2e_ms, h2d, d2h = time_e2e(ctx, shards[:args.e2e_layers or L], max(2, args.steps // 2), 1,
                                         world, stream)
             res["e2e"] = (max(allgather_float(e2e_ms, world)), h2d, d2h)
         results[name] = res
