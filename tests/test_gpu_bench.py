@@ -57,3 +57,16 @@ def test_bench_two_ranks_debug_path():
     for k in ("naive_even_hp", "greedy_whole_head", "split_subhead"):
         assert line[k]["ms"] > 0, k
     assert line["e2e"]["value"] > 0
+
+
+def test_cpp_host_driver():
+    """tools/bench_layer (C++ over the C ABI only): profile -> max-min table ->
+    layer call on device and host buffers, one JSON line."""
+    binary = os.path.join(ROOT, "tools", "bin", "bench_layer")
+    if not os.path.exists(binary):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tools")], check=True)
+    r = subprocess.run([binary, "8192", "2", "2"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    (line,) = _lines(r.stdout)
+    assert line["tool"] == "bench_layer" and line["launches_per_layer"] == 4
+    assert 0 < line["device_ms_per_layer"] < line["host_buffers_ms_per_layer"] * 10
