@@ -318,13 +318,21 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
                         pe.y = ex2(x.y);
                     }
                 } else {
+#ifdef SHPLB_DIAG_NO_EX2  // dev-only diagnostic (wrong results): no MUFU, for energy accounting
+                    pe = x;
+#else
                     pe.x = ex2(x.x);
                     pe.y = ex2(x.y);
+#endif
                 }
                 sum2[e & 1] = fadd2(sum2[e & 1], pe);
                 pk[e] = pack_bf16x2(pe.x, pe.y);
             }
+#ifdef SHPLB_DIAG_NO_PST  // dev-only diagnostic (wrong results): P not written back to TMEM
+            if (__float_as_uint(sum2[0].x) == 0x7fc00001u) tmem_st16(s_addr + c * 16, pk);
+#else
             tmem_st16(s_addr + c * 16, pk);
+#endif
         };
         // O_hf *= alpha (this half's previous P.V must have completed).
         auto rescale_o = [&](float alpha) {
