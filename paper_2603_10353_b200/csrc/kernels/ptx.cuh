@@ -367,6 +367,167 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         : "memory");
 }
 
+// ------------------------------------------------ CTA pair (cta_group::2) --
+// A 2-CTA cluster runs one tcgen05.mma over both SMs: M = 256 rows (128 in each
+// CTA's TMEM), the B operand split by N across the two CTAs' shared memory at
+// the same offsets. Only the leader (rank 0) issues MMAs and commits.
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// shared::cluster address of the variable at shared::cta address `addr` in CTA `rank`.
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+// Warp-uniform remote arrive (one elected lane) with release at cluster scope.
+__device__ __forceinline__ void mbar_arrive_cluster_warp(uint32_t cluster_addr) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n\t}" ::"r"(cluster_addr)
+        : "memory");
+}
+
+// Wait with acquire at cluster scope (arrivals came from the peer CTA).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* dst_smem) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "n"(kCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+
+template <uint32_t kCols>
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
+}
+
+// One CTA's share of a pair TMA load: `nchunks` boxes (d offsets 0, 64, ...)
+// of a 3-D map into this CTA's smem (chunk stride `chunk_bytes`); completion
+// bytes go to the LEADER's barrier (`leader_bar`, a shared::cluster address).
+__device__ __forceinline__ void tma_load_pair_warp(void* dst, const CUtensorMap* m, uint32_t leader_bar,
+                                                   int32_t d0, int32_t row, int32_t plane, int nchunks,
+                                                   uint32_t chunk_bytes) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];\n\t}" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(d0), "r"(row), "r"(plane)
+        : "memory");
+    if (nchunks > 1) {
+        asm volatile(
+            "{\n\t.reg .pred e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "@e cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4, %5}], [%2];\n\t}" ::"r"(smem_u32(dst) + chunk_bytes),
+            "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(d0 + 64), "r"(row), "r"(plane)
+            : "memory");
+    }
+}
+
+// Warp-uniform arm: one elected lane adds `bytes` to this CTA's barrier.
+__device__ __forceinline__ void mbar_expect_tx_warp(uint64_t* bar, uint32_t bytes) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)), "r"(bytes)
+        : "memory");
+}
+
+// Pair S = Q K^T over d = 128 (8 k-steps): A K-major SW128 with 16 KB d-chunks
+// (128 rows per CTA), B K-major SW128 with 8 KB d-chunks (64 keys per CTA).
+__device__ __forceinline__ void mma_pair_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a, b;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.u32 t, 0, 0;\n\t"
+        "mov.b64 a, %1;\n\tmov.b64 b, %2;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, p;\n\t"
+        "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, a, 1018;\n\tadd.s64 b, b, 506;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t"
+        "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a, b, %3, t;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Pair O += P V over 128 keys: A = P from TMEM (+8 columns per k-step), B = V
+// MN-major SW128 (64 d-columns per CTA; +2 KB per 16 keys).
+__device__ __forceinline__ void mma_pair_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p, t;\n\t.reg .b64 b;\n\t.reg .b32 a;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "setp.eq.u32 t, 0, 0;\n\t"
+        "mov.b32 a, %1;\n\tmov.b64 b, %2;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, p;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t"
+        "add.u32 a, a, 8;\n\tadd.s64 b, b, 128;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a], b, %3, t;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// Commit of the leader's MMAs, arriving on the barrier at the same offset in
+// both CTAs of the pair.
+__device__ __forceinline__ void mma_commit_pair_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+}
+
 // ------------------------------------------------------------ descriptors --
 
 // UMMA shared-memory descriptor for a 128B-swizzled operand tile

@@ -86,13 +86,13 @@ uintptr_t allocation_base(const void* p) {
 // [heads][n][128] bf16 as a 3-D tensor map with a {64, 128, 1} box and 128-byte
 // swizzle: one box is one 128-row x 128-byte UMMA K-major chunk. Rows past n
 // are zero-filled on load and clipped on store.
-CUtensorMap make_tmap(const void* base, int64_t heads, int64_t n) {
+CUtensorMap make_tmap(const void* base, int64_t heads, int64_t n, uint32_t box_rows = kern::kBlock) {
     CUtensorMap m;
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kern::kHeadDim), static_cast<cuuint64_t>(n),
                                 static_cast<cuuint64_t>(heads)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(kern::kHeadDim) * 2,
                                    static_cast<cuuint64_t>(n) * kern::kHeadDim * 2};
-    const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(kern::kBlock), 1};
+    const cuuint32_t box[3] = {64, box_rows, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode_tiled()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
                                       const_cast<void*>(base), dims, strides, box, estr,
@@ -371,6 +371,16 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
 //       under plain LPT, 1.4% faster;
 //   0 = LPT over all tiles (heaviest first);
 //   2 = LPT over power-of-two work buckets, kv-grouped inside a bucket.
+// Kernel-3 variant (SHPLB_K3): 0 = single-CTA two-half kernel (fa_sm100.cu,
+// default), 1 = "pair", the CTA-pair kernel (fa_pair_sm100.cu) for block_q = 256.
+int k3_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("SHPLB_K3");
+        return (e && std::string(e) == "pair") ? 1 : 0;
+    }();
+    return v;
+}
+
 int tile_order_mode() {
     static const int mode = [] {
         const char* e = std::getenv("SHPLB_TILE_ORDER");
@@ -451,6 +461,8 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     p.tm_q = make_tmap(q, s->num_q_heads, s->seq_len);
     p.tm_k = make_tmap(k, s->num_kv_heads, s->seq_len);
     p.tm_v = make_tmap(v, s->num_kv_heads, s->seq_len);
+    const bool pair = s->block_q == 256 && k3_variant() == 1;
+    if (pair) p.tm_k_half = make_tmap(k, s->num_kv_heads, s->seq_len, 64);
     p.out = out;
     p.idx = idx;
     p.cnt = cnt;
@@ -469,7 +481,12 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
         p.n_out_peers = s->n_out_peers;
     }
     p.scale_log2 = static_cast<float>((1.0 / std::sqrt(static_cast<double>(s->head_dim))) * 1.4426950408889634);
-    if (ctx->current->num_tiles > 0) kern::launch_fa(p, ctx->current->num_tiles, st);
+    if (ctx->current->num_tiles > 0) {
+        if (pair)
+            kern::launch_fa_pair(p, ctx->current->num_tiles, st);
+        else
+            kern::launch_fa(p, ctx->current->num_tiles, st);
+    }
     check_launch(ctx);
 }
 

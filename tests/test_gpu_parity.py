@@ -369,3 +369,17 @@ def test_zero_q_gives_uniform_weights_over_kept_keys(cuda_ctx):
         ref[i] = vf[: last + 1].mean(0)
     mx, rel = _errors(out[0], ref)
     assert mx <= MAX_ABS and rel <= MEAN_REL, (mx, rel)
+
+
+def test_cta_pair_kernel_variant():
+    """The experimental CTA-pair kernel 3 (SHPLB_K3=pair, fa_pair_sm100.cu) on the
+    parity cases of this file, in a subprocess (the variant is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-q", "-x",
+                        "-k", "small_gqa_layer or ragged_lengths or mha_and_wide or kv_map or zero_q"],
+                       cwd=root, env=dict(os.environ, SHPLB_K3="pair"), capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
