@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
 
 }  // namespace
 
-void launch_fa_pair(const FaParams& p, int num_tiles, cudaStream_t s) {
+cudaError_t launch_fa_pair(const FaParams& p, int num_tiles, cudaStream_t s) {
     cudaFuncSetAttribute(fa_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPSmemTotal));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * static_cast<unsigned>(num_tiles));
@@ -364,7 +364,7 @@ void launch_fa_pair(const FaParams& p, int num_tiles, cudaStream_t s) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, fa_pair_kernel, p);
+    return cudaLaunchKernelEx(&cfg, fa_pair_kernel, p);
 }
 
 }  // namespace shplb::kern

@@ -67,7 +67,7 @@ struct FaParams {
 };
 void launch_fa(const FaParams& p, int num_tiles, cudaStream_t s);
 // The CTA-pair variant (fa_pair_sm100.cu): bq = 256 only; one 2-CTA cluster per tile.
-void launch_fa_pair(const FaParams& p, int num_tiles, cudaStream_t s);
+cudaError_t launch_fa_pair(const FaParams& p, int num_tiles, cudaStream_t s);
 
 // GPU recovery-curve profiler (profiler.cu). q_rows bf16 [hq][n_rows][128],
 // k bf16 [hkv][n_k][128]; units = hq * n_rows.

@@ -483,7 +483,7 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     p.scale_log2 = static_cast<float>((1.0 / std::sqrt(static_cast<double>(s->head_dim))) * 1.4426950408889634);
     if (ctx->current->num_tiles > 0) {
         if (pair)
-            kern::launch_fa_pair(p, ctx->current->num_tiles, st);
+            SHPLB_CUDA(kern::launch_fa_pair(p, ctx->current->num_tiles, st));
         else
             kern::launch_fa(p, ctx->current->num_tiles, st);
     }
