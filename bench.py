@@ -445,6 +445,29 @@ def time_stack_p2p(ctx, shards, hq, steps, warmup, world, rank, stream):
     return max(allgather_float(e0.elapsed_time(e1) / (steps * len(shards)), world))
 
 
+def e2e_layer_budget(shards, wanted: int, local_ranks: int = 1) -> int:
+    """Layers the e2e leg can pin on this host: each needs its Q/K/V and output
+    in pinned host memory; stay within half of MemAvailable shared by the
+    ranks of the node (at least 2 layers, so the async pipeline still overlaps)."""
+    per_layer = [sum(t.numel() * t.element_size() for t in (ls.q, ls.k, ls.v)) + ls.q.numel() * ls.q.element_size()
+                 for ls in shards if ls.heads]
+    if not per_layer:
+        return 0
+    try:
+        with open("/proc/meminfo") as f:
+            avail = next(int(x.split()[1]) * 1024 for x in f if x.startswith("MemAvailable:"))
+    except (OSError, StopIteration, ValueError):
+        return min(wanted, len(per_layer))
+    budget = avail // 2 // max(1, local_ranks)
+    n, used = 0, 0
+    for b in per_layer[:wanted]:
+        if n >= 2 and used + b > budget:
+            break
+        used += b
+        n += 1
+    return n
+
+
 def time_e2e(ctx, shards, steps, warmup, world, stream):
     """End to end through the reference-facing C-ABI call with HOST buffers
     (shplb_sparse_attention_layer_host): for every layer of `shards`, pinned
@@ -702,9 +725,9 @@ def main():
                 res["ms_with_gather"] = time_stack_gathered(ctx, shards, plans, max(2, args.steps // 2),
                                                             1, world, stream)
         if name == headline and not args.no_e2e:
-            e2e_ms, h2d, d2h = time_e2e(ctx, shards[:args.e2e_layers or L], max(2, args.steps // 2), 1,
-                                        world, stream)
-            res["e2e"] = (max(allgather_float(e2e_ms, world)), h2d, d2h)
+            n_e2e = e2e_layer_budget(shards, args.e2e_layers or L, local_ranks=world)
+            e2e_ms, h2d, d2h = time_e2e(ctx, shards[:n_e2e], max(2, args.steps // 2), 1, world, stream)
+            res["e2e"] = (max(allgather_float(e2e_ms, world)), h2d, d2h, n_e2e)
         results[name] = res
         del shards
         torch.cuda.empty_cache()
@@ -785,9 +808,9 @@ def main():
         "clocks": g["clocks"],
     }
     if "e2e" in g:
-        e2e_ms, h2d, d2h = g["e2e"]
+        e2e_ms, h2d, d2h, n_e2e = g["e2e"]
         line["e2e"] = {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d,
-                       "d2h_bytes_per_step": d2h}
+                       "d2h_bytes_per_step": d2h, "layers": n_e2e}
     if world > 1:
         nv = results["naive"]
         def _vg(r):
