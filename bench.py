@@ -81,6 +81,9 @@ def parse_args():
     p.add_argument("--gather", choices=["nccl", "p2p"], default="p2p",
                    help="N>1 output reassembly: NCCL all-gather + reorder on a comm stream, or the "
                         "fused gather (kernel 3 stores rows into every rank's buffer over NVLink)")
+    p.add_argument("--policy", choices=["per_query_topk", "column_aggregate_topk"], default="per_query_topk",
+                   help="selection policy (SelectionKind) of the profile and the layer: per (head, query "
+                        "block) top-k blocks, or one kept block set per head (block granularity)")
     p.add_argument("--placement", choices=["greedy", "split"], default="split",
                    help="N>1 headline plan: 'greedy' = the reference's whole-head greedy_assign (LPT on "
                         "budgets, bit-exact); 'split' = the sub-head balancer (shplb_plan_split). "
@@ -246,10 +249,10 @@ def make_budgets(q, k, args, world, rank):
         grid = P.default_budget_grid(n, 128)
         if getattr(q, "is_cuda", False):  # GPU profiler (shplb_profile_curves)
             pctx = P.Context(q.device.index or 0)
-            curves = pctx.profile_curves(rows.contiguous(), k, grid)
+            curves = pctx.profile_curves(rows.contiguous(), k, grid, kind=args.policy)
             pctx.close()
         else:
-            curves = P.profile_curves(bf16_bits(rows), bf16_bits(k), grid)
+            curves = P.profile_curves(bf16_bits(rows), bf16_bits(k), grid, kind=args.policy)
         alloc = P.maxmin_allocate(curves, total, quantum=128, floor=128)
         budgets = alloc.budgets.astype(np.int64)
         info = {"calibration_rows": args.calib_rows, "profile_s": round(time.time() - t0, 3),
@@ -286,11 +289,14 @@ class LayerShard:
         self.flops = 0.0
 
 
+KIND = 0  # selection kind of every layer call (--policy)
+
+
 def run_layer(ctx, ls, out, stream):
     if not ls.heads:
         return
     ctx.sparse_attention_layer(ls.q, ls.k, ls.v, ls.budgets, causal=True, out=out, kv_map=ls.kv_map,
-                               stream=stream, q_block_range=ls.ranges)
+                               stream=stream, q_block_range=ls.ranges, kind=KIND)
 
 
 def time_stack(ctx, shards, steps, warmup, world, stream):
@@ -414,7 +420,7 @@ def time_stack_p2p(ctx, shards, hq, steps, warmup, world, rank, stream):
             if ls.heads:
                 ctx.sparse_attention_layer(ls.q, ls.k, ls.v, ls.budgets, causal=True, kv_map=ls.kv_map,
                                            stream=stream, q_block_range=ls.ranges,
-                                           gather=(po.ptrs(b), ls.heads, hq))
+                                           gather=(po.ptrs(b), ls.heads, hq), kind=KIND)
             if DEBUG_GLOO:  # exercising the path with every rank on one GPU: host barrier
                 torch.cuda.synchronize()
                 dist.barrier()
@@ -488,7 +494,7 @@ def time_e2e(ctx, shards, steps, warmup, world, stream):
         for ls, (hq_, hk_, hv_), o in zip(shards, host, outs):
             ctx.sparse_attention_layer_host(hq_, hk_, hv_, ls.budgets, causal=True, out=o,
                                             stream=stream, kv_map=ls.kv_map, q_block_range=ls.ranges,
-                                            asynchronous=True)
+                                            asynchronous=True, kind=KIND)
         stream.synchronize()
 
     for _ in range(warmup):
@@ -631,6 +637,7 @@ def config_dict(args, budgets_desc, headline="greedy"):
         "layers": args.layers,
         "seq_len": args.seq_len, "q_heads": args.q_heads, "kv_heads": args.kv_heads,
         "head_dim": 128, "budget_fraction": args.budget_fraction, "budgets": budgets_desc,
+        "policy": args.policy,
         "placement": PLACEMENTS[headline],
         "l2": "each layer's inputs (1.5 GiB at 128K) exceed the 126 MB L2; layers run back to back",
     }
@@ -651,6 +658,8 @@ def main():
     from paper_2603_10353_b200.head_parallel import rank_segments, rank_shard
     from paper_2603_10353_b200.workload import LayerSpec, make_layer
 
+    global KIND
+    KIND = P.selection_kind(args.policy)
     world, rank, local = dist_setup(args.gpus, args.debug_one_device)
     if args.force_gather and world == 1:
         init_single_rank_group(local)

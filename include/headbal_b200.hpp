@@ -162,13 +162,15 @@ inline BudgetAllocation maxmin_allocate(const std::vector<RecoveryCurve>& curves
     return a;
 }
 
-// ----- recovery curves (profiler.hpp:86-89): build_profiles for PerQueryTopK on the
-// workload's query rows (all n_k keys, no causal mask as the reference's
-// profile command), through the GPU profiler when a context is given, else the
-// host C++ one. Heads with equal K share a kv head. Curves agree with the
-// reference to rounding (1e-12).
+// ----- recovery curves (profiler.hpp:86-89): build_profiles for `kind`
+// (PerQueryTopK or ColumnAggregateTopK) on the workload's query rows (all n_k
+// keys, no causal mask as the reference's profile command), through the GPU
+// profiler when a context is given, else the host C++ one. Heads with equal K
+// share a kv head. Curves agree with the reference to rounding (1e-12).
 inline std::vector<RecoveryCurve> build_profiles(const AttentionWorkload& w, const std::vector<long>& grid,
-                                                 Context* ctx = nullptr) {
+                                                 Context* ctx = nullptr,
+                                                 SelectionKind kind = SelectionKind::PerQueryTopK) {
+    const int32_t sk = kind == SelectionKind::PerQueryTopK ? SHPLB_BLOCK_TOPK : SHPLB_COLUMN_AGGREGATE_TOPK;
     w.validate();
     const auto H = static_cast<int32_t>(w.num_heads());
     const auto rows = static_cast<int64_t>(w.num_queries());
@@ -198,14 +200,14 @@ inline std::vector<RecoveryCurve> build_profiles(const AttentionWorkload& w, con
         check(cudaMalloc(&dk, k.size() * 2) == cudaSuccess ? SHPLB_OK : SHPLB_CUDA_ERROR);
         cudaMemcpy(dq, q.data(), q.size() * 2, cudaMemcpyHostToDevice);
         cudaMemcpy(dk, k.data(), k.size() * 2, cudaMemcpyHostToDevice);
-        const int rc = shplb_profile_curves(ctx->get(), dq, dk, H, hkv, rows, n_k, d, gr.data(),
-                                            static_cast<int64_t>(gr.size()), rec.data(), nullptr);
+        const int rc = shplb_profile_curves_kind(ctx->get(), dq, dk, H, hkv, rows, n_k, d, gr.data(),
+                                                 static_cast<int64_t>(gr.size()), sk, rec.data(), nullptr);
         cudaFree(dq);
         cudaFree(dk);
         check(rc);
     } else {
-        check(shplb_profile_curves_host(q.data(), k.data(), H, hkv, rows, n_k, d, gr.data(),
-                                        static_cast<int64_t>(gr.size()), rec.data()));
+        check(shplb_profile_curves_host_kind(q.data(), k.data(), H, hkv, rows, n_k, d, gr.data(),
+                                             static_cast<int64_t>(gr.size()), sk, rec.data()));
     }
     std::vector<RecoveryCurve> curves(static_cast<size_t>(H));
     for (int32_t h = 0; h < H; ++h) {

@@ -103,6 +103,19 @@ int shplb_profile_curves(shplb_ctx* ctx, const void* q_rows, const void* k, int3
                          int32_t num_kv_heads, int64_t n_rows, int64_t n_k, int32_t d,
                          const int64_t* grid, int64_t n_grid, double* recovery_out, void* stream);
 
+/* Both profiles for a selection kind (build_profiles' SelectionKind argument,
+ * profiler.cpp:157-196; recovery_ratio, attention.cpp:151-184):
+ * SHPLB_BLOCK_TOPK = PerQueryTopK (the calls above), SHPLB_COLUMN_AGGREGATE_TOPK =
+ * ColumnAggregateTopK (per head, the k largest column sums of the calibration
+ * rows' weights, their mass averaged over rows). */
+int shplb_profile_curves_host_kind(const uint16_t* q_rows, const uint16_t* k, int32_t num_q_heads,
+                                   int32_t num_kv_heads, int64_t n_rows, int64_t n_k, int32_t d,
+                                   const int64_t* grid, int64_t n_grid, int32_t kind, double* recovery_out);
+int shplb_profile_curves_kind(shplb_ctx* ctx, const void* q_rows, const void* k, int32_t num_q_heads,
+                              int32_t num_kv_heads, int64_t n_rows, int64_t n_k, int32_t d,
+                              const int64_t* grid, int64_t n_grid, int32_t kind, double* recovery_out,
+                              void* stream);
+
 /* ======================================================================
  * Head -> GPU plan   (reference: proj/include/headbal/partitioner.hpp)
  * ====================================================================== */

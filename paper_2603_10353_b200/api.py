@@ -112,18 +112,21 @@ def default_budget_grid(context_length: int, stride: int) -> np.ndarray:
     return np.asarray(g, np.int64)
 
 
-def profile_curves(q_rows_bf16: np.ndarray, k_bf16: np.ndarray, grid: np.ndarray) -> list[RecoveryCurve]:
-    """PerQueryTopK recovery curves (build_profiles, profiler.cpp:157-196) from
-    calibration query rows. q_rows_bf16: uint16 [Hq][rows][d]; k_bf16: uint16
-    [Hkv][n_k][d] (bf16 bit patterns, host). Host C++, OpenMP."""
+def profile_curves(q_rows_bf16: np.ndarray, k_bf16: np.ndarray, grid: np.ndarray,
+                   kind=0) -> list[RecoveryCurve]:
+    """Recovery curves (build_profiles, profiler.cpp:157-196) from calibration
+    query rows for selection `kind` (PerQueryTopK = 0 / "per_query_topk",
+    ColumnAggregateTopK = 1 / "column_aggregate_topk"). q_rows_bf16: uint16
+    [Hq][rows][d]; k_bf16: uint16 [Hkv][n_k][d] (bf16 bit patterns, host).
+    Host C++, OpenMP."""
     q = np.ascontiguousarray(q_rows_bf16, np.uint16)
     k = np.ascontiguousarray(k_bf16, np.uint16)
     grid = _i64(grid)
     hq, rows, d = q.shape
     hkv, n_k, _ = k.shape
     out = np.empty((hq, grid.size), np.float64)
-    check(lib().shplb_profile_curves_host(_ptr(q), _ptr(k), hq, hkv, rows, n_k, d, _ptr(grid),
-                                          grid.size, _ptr(out)))
+    check(lib().shplb_profile_curves_host_kind(_ptr(q), _ptr(k), hq, hkv, rows, n_k, d, _ptr(grid),
+                                               grid.size, selection_kind(kind), _ptr(out)))
     return [RecoveryCurve(grid.copy(), out[h].copy(), n_k) for h in range(hq)]
 
 
@@ -320,8 +323,8 @@ class Context:
         return buf[:n.value].copy()
 
     # -- offline profiler (GPU) ---------------------------------------------
-    def profile_curves(self, q_rows, k, grid, stream=None) -> list[RecoveryCurve]:
-        """PerQueryTopK recovery curves on the GPU (shplb_profile_curves;
+    def profile_curves(self, q_rows, k, grid, stream=None, kind=0) -> list[RecoveryCurve]:
+        """Recovery curves for selection `kind` on the GPU (shplb_profile_curves_kind;
         build_profiles + recovery_ratio, profiler.cpp:157-196,
         attention.cpp:151-184). q_rows: bf16 CUDA [Hq, rows, d] (the
         calibration rows), k: bf16 CUDA [Hkv, n_k, d]. Same results as the
@@ -335,8 +338,9 @@ class Context:
         hq, rows, d = q_rows.shape
         hkv, n_k, _ = k.shape
         out = np.empty((hq, grid.size), np.float64)
-        check(lib().shplb_profile_curves(self._h, q_rows.data_ptr(), k.data_ptr(), hq, hkv, rows, n_k, d,
-                                         _ptr(grid), grid.size, _ptr(out), _stream_ptr(stream)))
+        check(lib().shplb_profile_curves_kind(self._h, q_rows.data_ptr(), k.data_ptr(), hq, hkv, rows, n_k, d,
+                                              _ptr(grid), grid.size, selection_kind(kind), _ptr(out),
+                                              _stream_ptr(stream)))
         return [RecoveryCurve(grid.copy(), out[h].copy(), n_k) for h in range(hq)]
 
     # -- kernel 1 ---------------------------------------------------------

@@ -78,6 +78,12 @@ void launch_profile_sort(const double* in, double* out, int64_t units, int64_t n
                          void* temp, size_t temp_bytes, cudaStream_t s);
 void launch_profile_prefix(const double* sorted, int64_t units, int64_t n_k, const int64_t* grid,
                            int64_t n_grid, double* mass, cudaStream_t s);
+// ColumnAggregateTopK profile of `heads` heads whose scores [heads*n_rows][n_k]
+// are in `scores` (overwritten with weights): col / sorted [heads][n_k] scratch,
+// recovery [heads][n_grid] out (launch_profile_sort's offsets / temp reused).
+void launch_profile_colagg(double* scores, int heads, int64_t n_rows, int64_t n_k, double* col, double* sorted,
+                           int64_t* offsets, void* temp, size_t temp_bytes, const int64_t* grid, int64_t n_grid,
+                           double* recovery, cudaStream_t s);
 void launch_profile_rows(const double* mass, int hq, int64_t n_rows, const int64_t* grid, int64_t n_grid,
                          double* recovery, cudaStream_t s);
 

@@ -128,6 +128,81 @@ __global__ void __launch_bounds__(kPrefixThreads) profile_prefix_kernel(
     }
 }
 
+// ColumnAggregateTopK: scores of each unit (row) -> softmax weights in place
+// (one CTA per row: max, Z = sum exp(s - max), w = exp(s - max) / Z).
+__global__ void __launch_bounds__(kPrefixThreads) profile_weights_kernel(double* __restrict__ scores, int64_t n_k) {
+    __shared__ double red[kPrefixThreads];
+    double* s = scores + static_cast<int64_t>(blockIdx.x) * n_k;
+    double m = -INFINITY;
+    for (int64_t j = threadIdx.x; j < n_k; j += kPrefixThreads) m = fmax(m, s[j]);
+    red[threadIdx.x] = m;
+    __syncthreads();
+    for (int off = kPrefixThreads / 2; off > 0; off >>= 1) {
+        if (threadIdx.x < off) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + off]);
+        __syncthreads();
+    }
+    m = red[0];
+    __syncthreads();
+    double z = 0.0;
+    for (int64_t j = threadIdx.x; j < n_k; j += kPrefixThreads) z += exp(s[j] - m);
+    red[threadIdx.x] = z;
+    __syncthreads();
+    for (int off = kPrefixThreads / 2; off > 0; off >>= 1) {
+        if (threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+        __syncthreads();
+    }
+    const double inv = 1.0 / red[0];
+    for (int64_t j = threadIdx.x; j < n_k; j += kPrefixThreads) s[j] = exp(s[j] - m) * inv;
+}
+
+// Column sums per head over its rows, rows ascending (column_sums, attention.cpp:66-73).
+__global__ void profile_colsum_kernel(const double* __restrict__ w, int heads, int64_t n_rows, int64_t n_k,
+                                      double* __restrict__ col) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<int64_t>(heads) * n_k) return;
+    const int64_t h = t / n_k, j = t % n_k;
+    double acc = 0.0;
+    for (int64_t i = 0; i < n_rows; ++i) acc += w[(h * n_rows + i) * n_k + j];
+    col[t] = acc;
+}
+
+// Per head (one CTA): sorted-descending column sums -> recovery at every grid
+// point = prefix sum / rows.
+__global__ void __launch_bounds__(kPrefixThreads) profile_colagg_prefix_kernel(
+    const double* __restrict__ sorted, int64_t n_k, const int64_t* __restrict__ grid, int64_t n_grid,
+    double inv_rows, double* __restrict__ recovery) {
+    __shared__ double part[kPrefixThreads];
+    const int64_t head = blockIdx.x;
+    const double* s = sorted + head * n_k;
+    const int64_t per = (n_k + kPrefixThreads - 1) / kPrefixThreads;
+    const int64_t lo = threadIdx.x * per, hi = min(lo + per, n_k);
+    double local = 0.0;
+    for (int64_t i = lo; i < hi; ++i) local += s[i];
+    part[threadIdx.x] = local;
+    __syncthreads();
+    for (int off = 1; off < kPrefixThreads; off <<= 1) {
+        const double add = threadIdx.x >= off ? part[threadIdx.x - off] : 0.0;
+        __syncthreads();
+        part[threadIdx.x] += add;
+        __syncthreads();
+    }
+    double run = part[threadIdx.x] - local;
+    int64_t a = 0, b = n_grid;
+    while (a < b) {
+        const int64_t mid = (a + b) / 2;
+        if (grid[mid] <= lo) a = mid + 1; else b = mid;
+    }
+    int64_t gi = a;
+    if (threadIdx.x == 0 && n_grid > 0 && grid[0] == 0) recovery[head * n_grid] = 0.0;
+    for (int64_t i = lo; i < hi && gi < n_grid; ++i) {
+        run += s[i];
+        if (grid[gi] == i + 1) {
+            recovery[head * n_grid + gi] = run * inv_rows;
+            ++gi;
+        }
+    }
+}
+
 __global__ void profile_rows_kernel(const double* __restrict__ mass, int hq, int64_t n_rows,
                                     const int64_t* __restrict__ grid, int64_t n_grid,
                                     double* __restrict__ recovery) {
@@ -187,6 +262,21 @@ void launch_profile_rows(const double* mass, int hq, int64_t n_rows, const int64
     const int64_t n = static_cast<int64_t>(hq) * n_grid;
     profile_rows_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(mass, hq, n_rows, grid, n_grid,
                                                                               recovery);
+}
+
+}  // namespace shplb::kern
+
+namespace shplb::kern {
+
+void launch_profile_colagg(double* scores, int heads, int64_t n_rows, int64_t n_k, double* col, double* sorted,
+                           int64_t* offsets, void* temp, size_t temp_bytes, const int64_t* grid, int64_t n_grid,
+                           double* recovery, cudaStream_t s) {
+    profile_weights_kernel<<<static_cast<unsigned>(heads * n_rows), kPrefixThreads, 0, s>>>(scores, n_k);
+    const int64_t cols = static_cast<int64_t>(heads) * n_k;
+    profile_colsum_kernel<<<static_cast<unsigned>((cols + 255) / 256), 256, 0, s>>>(scores, heads, n_rows, n_k, col);
+    launch_profile_sort(col, sorted, heads, n_k, offsets, temp, temp_bytes, s);
+    profile_colagg_prefix_kernel<<<static_cast<unsigned>(heads), kPrefixThreads, 0, s>>>(
+        sorted, n_k, grid, n_grid, 1.0 / static_cast<double>(n_rows), recovery);
 }
 
 }  // namespace shplb::kern

@@ -944,11 +944,15 @@ int shplb_layer_work(const shplb_layer_shape* shape, const int64_t* budgets_toke
     });
 }
 
-int shplb_profile_curves(shplb_ctx* ctx, const void* q_rows, const void* k, int32_t num_q_heads,
-                         int32_t num_kv_heads, int64_t n_rows, int64_t n_k, int32_t d,
-                         const int64_t* grid, int64_t n_grid, double* recovery_out, void* stream) {
+int shplb_profile_curves_kind(shplb_ctx* ctx, const void* q_rows, const void* k, int32_t num_q_heads,
+                              int32_t num_kv_heads, int64_t n_rows, int64_t n_k, int32_t d,
+                              const int64_t* grid, int64_t n_grid, int32_t kind, double* recovery_out,
+                              void* stream) {
     return guarded([&] {
         require(ctx != nullptr, "ctx is null");
+        if (kind != SHPLB_BLOCK_TOPK && kind != SHPLB_COLUMN_AGGREGATE_TOPK)
+            throw InvalidArgument("unknown selection kind " + std::to_string(kind));
+        const bool colagg = kind == SHPLB_COLUMN_AGGREGATE_TOPK;
         require(num_q_heads >= 1 && num_kv_heads >= 1 && num_q_heads % num_kv_heads == 0,
                 "num_q_heads must be a positive multiple of num_kv_heads");
         require(n_rows >= 1 && n_k >= 1 && d >= 1, "profile needs at least one row, key and dim");
@@ -977,7 +981,9 @@ int shplb_profile_curves(shplb_ctx* ctx, const void* q_rows, const void* k, int3
         kv_batch = std::min<int64_t>(kv_batch, num_kv_heads);
         const int64_t units_b = kv_batch * units_per_kv;
         grow(ctx->prof_scores, ctx->prof_scores_bytes, sizeof(double) * units_b * n_k);
-        grow(ctx->prof_sorted, ctx->prof_sorted_bytes, sizeof(double) * units_b * n_k);
+        const int64_t heads_b = kv_batch * group;
+        grow(ctx->prof_sorted, ctx->prof_sorted_bytes,
+             sizeof(double) * std::max(units_b, colagg ? 2 * heads_b : int64_t(0)) * n_k);
         grow(ctx->prof_mass, ctx->prof_mass_bytes, sizeof(double) * (units_total * n_grid + int64_t(num_q_heads) * n_grid));
         grow(ctx->prof_aux, ctx->prof_aux_bytes, sizeof(int64_t) * (units_b + 1 + n_grid));
         const size_t temp = kern::profile_sort_temp_bytes(units_b, n_k);
@@ -994,18 +1000,36 @@ int shplb_profile_curves(shplb_ctx* ctx, const void* q_rows, const void* k, int3
             const auto* kb = static_cast<const uint16_t*>(k) + g0 * n_k * d;
             kern::launch_profile_scores(qb, kb, static_cast<int>(nb * group), static_cast<int>(nb), n_rows, n_k,
                                         scale, ctx->prof_scores, st);
+            if (colagg) {
+                const int64_t hb = nb * group;
+                kern::launch_profile_colagg(ctx->prof_scores, static_cast<int>(hb), n_rows, n_k, ctx->prof_sorted,
+                                            ctx->prof_sorted + hb * n_k, offsets, ctx->prof_temp,
+                                            ctx->prof_temp_bytes, grid_dev, n_grid,
+                                            recovery_dev + g0 * group * n_grid, st);
+                check_launch(ctx, 6);
+                continue;
+            }
             kern::launch_profile_sort(ctx->prof_scores, ctx->prof_sorted, units, n_k, offsets, ctx->prof_temp,
                                       ctx->prof_temp_bytes, st);
             kern::launch_profile_prefix(ctx->prof_sorted, units, n_k, grid_dev, n_grid,
                                         ctx->prof_mass + g0 * units_per_kv * n_grid, st);
             check_launch(ctx, 4);
         }
-        kern::launch_profile_rows(ctx->prof_mass, num_q_heads, n_rows, grid_dev, n_grid, recovery_dev, st);
-        check_launch(ctx);
+        if (!colagg) {
+            kern::launch_profile_rows(ctx->prof_mass, num_q_heads, n_rows, grid_dev, n_grid, recovery_dev, st);
+            check_launch(ctx);
+        }
         SHPLB_CUDA(cudaMemcpyAsync(recovery_out, recovery_dev, sizeof(double) * num_q_heads * n_grid,
                                    cudaMemcpyDeviceToHost, st));
         SHPLB_CUDA(cudaStreamSynchronize(st));
     });
+}
+
+int shplb_profile_curves(shplb_ctx* ctx, const void* q_rows, const void* k, int32_t num_q_heads,
+                         int32_t num_kv_heads, int64_t n_rows, int64_t n_k, int32_t d,
+                         const int64_t* grid, int64_t n_grid, double* recovery_out, void* stream) {
+    return shplb_profile_curves_kind(ctx, q_rows, k, num_q_heads, num_kv_heads, n_rows, n_k, d, grid, n_grid,
+                                     SHPLB_BLOCK_TOPK, recovery_out, stream);
 }
 
 // IPC handle layout (SHPLB_IPC_HANDLE_BYTES = 72): the CUDA IPC handle of the

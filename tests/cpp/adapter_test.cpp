@@ -108,6 +108,14 @@ static int run_cpu() {
             for (size_t i = 0; i < grid.size(); ++i)
                 worst = std::max(worst, std::fabs(ref[h].curve.points[i].recovery - got[h].points[i].recovery));
         EXPECT(worst < 1e-12, "build_profiles (host) vs reference");
+        const auto ref_ca = build_profiles(w, grid, SelectionKind::ColumnAggregateTopK, Provenance{"r", "t"});
+        const auto got_ca = b200::build_profiles(w, grid, nullptr, SelectionKind::ColumnAggregateTopK);
+        double worst_ca = 0.0;
+        for (int h = 0; h < 4; ++h)
+            for (size_t i = 0; i < grid.size(); ++i)
+                worst_ca = std::max(worst_ca,
+                                    std::fabs(ref_ca[h].curve.points[i].recovery - got_ca[h].points[i].recovery));
+        EXPECT(worst_ca < 1e-12, "build_profiles ColumnAggregateTopK (host) vs reference");
     }
     std::printf("cpu checks: %d failures\n", failures);
     return failures == 0 ? 0 : 1;

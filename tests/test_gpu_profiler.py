@@ -1,6 +1,7 @@
-"""GPU recovery-curve profiler (shplb_profile_curves) against
-the host restatement and the compiled reference's build_profiles
-(profiler.cpp:157-196, recovery_ratio PerQueryTopK attention.cpp:151-184).
+"""GPU recovery-curve profiler (shplb_profile_curves[_kind])
+against the host restatement and the compiled reference's build_profiles
+(profiler.cpp:157-196, recovery_ratio attention.cpp:151-184) for both
+PerQueryTopK and ColumnAggregateTopK.
 
 Curves are fp64; the reference sums each top-k in nth_element's arbitrary
 order, so agreement is to rounding (1e-12 absolute). The max-min budget
@@ -24,32 +25,34 @@ def _rand_bf16(rng, shape, scale=1.0):
     return torch.from_numpy((rng.standard_normal(shape) * scale).astype(np.float32)).to(torch.bfloat16)
 
 
+@pytest.mark.parametrize("kind", [0, 1])
 @pytest.mark.parametrize("hq,hkv,rows,n_k,stride", [(4, 2, 6, 300, 32), (8, 8, 3, 1000, 64),
                                                     (4, 1, 16, 4096, 128), (2, 1, 1, 129, 1)])
-def test_gpu_profile_matches_host(cuda_ctx, hq, hkv, rows, n_k, stride):
+def test_gpu_profile_matches_host(cuda_ctx, hq, hkv, rows, n_k, stride, kind):
     rng = np.random.default_rng(hq * 1000 + n_k)
     q = _rand_bf16(rng, (hq, rows, 128)) * torch.from_numpy(
         rng.uniform(0.05, 0.5, (hq, 1, 1)).astype(np.float32)).to(torch.bfloat16)
     k = _rand_bf16(rng, (hkv, n_k, 128))
     grid = P.default_budget_grid(n_k, stride)
-    host = P.profile_curves(bf16_bits(q), bf16_bits(k), grid)
-    gpu = cuda_ctx.profile_curves(q.cuda(), k.cuda(), grid)
+    host = P.profile_curves(bf16_bits(q), bf16_bits(k), grid, kind=kind)
+    gpu = cuda_ctx.profile_curves(q.cuda(), k.cuda(), grid, kind=kind)
     for h in range(hq):
         assert np.abs(gpu[h].recovery - host[h].recovery).max() < TOL, f"head {h}"
         assert gpu[h].recovery[0] == 0.0 and abs(gpu[h].recovery[-1] - 1.0) < 1e-9
 
 
 @pytest.mark.skipif(not O.ref_available(), reason="reference library not built")
-def test_gpu_profile_matches_reference_build_profiles(cuda_ctx):
+@pytest.mark.parametrize("kind", [0, 1])
+def test_gpu_profile_matches_reference_build_profiles(cuda_ctx, kind):
     rng = np.random.default_rng(11)
     hq, hkv, rows, n_k = 4, 2, 5, 700
     q = _rand_bf16(rng, (hq, rows, 128), 0.3)
     k = _rand_bf16(rng, (hkv, n_k, 128))
     grid = P.default_budget_grid(n_k, 64)
-    gpu = cuda_ctx.profile_curves(q.cuda(), k.cuda(), grid)
+    gpu = cuda_ctx.profile_curves(q.cuda(), k.cuda(), grid, kind=kind)
     Q = q.float().numpy().astype(np.float64)
     K = np.repeat(k.float().numpy().astype(np.float64), hq // hkv, axis=0)
-    ref = O.ref.build_profiles(Q, K, np.zeros_like(K), grid)
+    ref = O.ref.build_profiles(Q, K, np.zeros_like(K), grid, kind=kind)
     for h in range(hq):
         assert np.abs(gpu[h].recovery - ref[h]).max() < TOL
 

@@ -199,22 +199,28 @@ def test_metric_on_measured_latencies():
 # ------------------------------------------------------------ profiler ----
 
 @pytest.mark.skipif(not O.ref_available(), reason="reference library not built here")
-def test_profile_curves_match_reference_build_profiles():
-    """PerQueryTopK recovery curves (build_profiles, profiler.cpp:157-196) on
-    bf16-exact inputs agree with the reference to rounding."""
+@pytest.mark.parametrize("kind", [0, 1])
+def test_profile_curves_match_reference_build_profiles(kind):
+    """PerQueryTopK (0) and ColumnAggregateTopK (1) recovery curves
+    (build_profiles, profiler.cpp:157-196) on bf16-exact inputs agree with the
+    reference to rounding."""
     rng = np.random.default_rng(5)
     hq, hkv, rows, n_k, d = 4, 2, 6, 300, 128
     q = rng.standard_normal((hq, rows, d)).astype(np.float32) * rng.uniform(0.05, 0.4, (hq, 1, 1)).astype(np.float32)
     k = rng.standard_normal((hkv, n_k, d)).astype(np.float32)
     qb, kb = O.f32_to_bf16_bits(q), O.f32_to_bf16_bits(k)
     grid = P.default_budget_grid(n_k, 32)
-    curves = P.profile_curves(qb, kb, grid)
+    curves = P.profile_curves(qb, kb, grid, kind=kind)
     Q = O.bf16_bits_to_f32(qb).astype(np.float64)
     K = np.repeat(O.bf16_bits_to_f32(kb).astype(np.float64), hq // hkv, axis=0)
-    ref = O.ref.build_profiles(Q, K, np.zeros_like(K), grid)
+    ref = O.ref.build_profiles(Q, K, np.zeros_like(K), grid, kind=kind)
     for h in range(hq):
         assert np.abs(curves[h].recovery - ref[h]).max() < 1e-12
         assert curves[h].recovery[-1] == pytest.approx(1.0, abs=1e-9)
+    if kind == 1:  # one shared key set can never beat each row's own top-k
+        per_query = P.profile_curves(qb, kb, grid, kind="per_query_topk")
+        for h in range(hq):
+            assert np.all(curves[h].recovery <= per_query[h].recovery + 1e-12)
 
 
 def test_layer_work_counts_selected_tiles():
