@@ -57,7 +57,7 @@ def _time(fn, steps: int, repeats: int = 3) -> float:
     return float(np.median(times))
 
 
-def shard_latency_ms(ctx, q, k, v, shard, steps: int = 3, block_q: int = api.BLOCK_Q) -> float:
+def shard_latency_ms(ctx, q, k, v, shard, steps: int = 3, block_q: int = api.BLOCK_Q, kind=0) -> float:
     """Device time of one rank's shard (its q heads, the kv heads they read,
     optional query-block ranges)."""
     import torch
@@ -68,21 +68,22 @@ def shard_latency_ms(ctx, q, k, v, shard, steps: int = 3, block_q: int = api.BLO
     out = torch.empty_like(ql)
     ranges = getattr(shard, "q_block_range", None)
     return _time(lambda: ctx.sparse_attention_layer(ql, kl, vl, shard.budgets, out=out, kv_map=shard.kv_map,
-                                                    q_block_range=ranges, block_q=block_q), steps)
+                                                    q_block_range=ranges, block_q=block_q, kind=kind), steps)
 
 
-def measured_barrier(ctx, q, k, v, budgets, device_of_head, devices: int, steps: int = 3):
+def measured_barrier(ctx, q, k, v, budgets, device_of_head, devices: int, steps: int = 3, kind=0):
     """(per-rank ms, SimulationResult-like barrier/bubble) of a whole-head plan."""
     group = q.shape[0] // k.shape[0]
-    per = [shard_latency_ms(ctx, q, k, v, rank_shard(device_of_head, r, group, budgets), steps)
+    per = [shard_latency_ms(ctx, q, k, v, rank_shard(device_of_head, r, group, budgets), steps, kind=kind)
            for r in range(devices)]
     return per, api.barrier(per)
 
 
-def measured_split_barrier(ctx, q, k, v, budgets, devices: int, steps: int = 3):
+def measured_split_barrier(ctx, q, k, v, budgets, devices: int, steps: int = 3, kind=0):
     group = q.shape[0] // k.shape[0]
     sp = api.split_assign(budgets, devices, q.shape[1])
-    per = [shard_latency_ms(ctx, q, k, v, rank_segments(sp, r, group, budgets), steps) for r in range(devices)]
+    per = [shard_latency_ms(ctx, q, k, v, rank_segments(sp, r, group, budgets), steps, kind=kind)
+           for r in range(devices)]
     return per, api.barrier(per), sp
 
 
@@ -163,11 +164,12 @@ def output_error(sparse, dense) -> float:
 
 
 def measured_skyline(ctx, q, k, v, curves, devices: int, totals=None, quantum: int = 128, floor: int = 128,
-                     steps: int = 3, causal: bool = True) -> list:
+                     steps: int = 3, causal: bool = True, policy=0) -> list:
     """run_skyline (commands.cpp:411-489) on measured latency: for each total
     budget (default 0.25/0.5/0.75/1.0 of Hq*n) and allocator (uniform,
     max-min), the mean per-head output error against dense attention and the
-    greedy / naive barrier latency of the budgets at `devices` ranks."""
+    greedy / naive barrier latency of the budgets at `devices` ranks, under
+    selection `policy` (the SelectionKind of commands.cpp:464-470)."""
     import torch
     hq, n, _ = q.shape
     if totals is None:
@@ -185,12 +187,14 @@ def measured_skyline(ctx, q, k, v, curves, devices: int, totals=None, quantum: i
                 budgets = api.uniform_allocate(hq, total, floor, n).budgets.astype(np.int64)
             else:
                 budgets = api.maxmin_allocate(curves, total, quantum=quantum, floor=floor).budgets.astype(np.int64)
-            ctx.sparse_attention_layer(q, k, v, budgets, out=out, causal=causal)
+            ctx.sparse_attention_layer(q, k, v, budgets, out=out, causal=causal, kind=policy)
             torch.cuda.synchronize()
             errs = [output_error(out[h], dense[h]) for h in range(hq)]
             err = float(np.mean(errs))
-            _, rg = measured_barrier(ctx, q, k, v, budgets, api.greedy_assign(budgets, devices), devices, steps)
-            _, rn = measured_barrier(ctx, q, k, v, budgets, api.naive_assign(budgets, devices), devices, steps)
+            _, rg = measured_barrier(ctx, q, k, v, budgets, api.greedy_assign(budgets, devices), devices, steps,
+                                     kind=policy)
+            _, rn = measured_barrier(ctx, q, k, v, budgets, api.naive_assign(budgets, devices), devices, steps,
+                                     kind=policy)
             points.append(SkylinePoint(int(total), kind, err, rg.barrier_latency, rn.barrier_latency,
                                        float(np.max(errs))))
     return points

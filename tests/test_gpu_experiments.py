@@ -58,3 +58,13 @@ def test_measured_sweep_and_skyline_small(cuda_ctx):
         assert all(a >= b for a, b in zip(e, e[1:])), (kind, e)
     with pytest.raises(P.InvalidArgument, match="infeasible"):
         X.measured_skyline(cuda_ctx, q, k, v, curves, devices=2, totals=[10])
+    # ColumnAggregateTopK skyline (run_skyline's policy): its own curves, full budget exact,
+    # and on this (seeded) workload one shared key set per head is no more accurate than
+    # per-query block selection at the same uniform budgets
+    ca_curves = cuda_ctx.profile_curves(q[:, n - 16:, :].contiguous(), k, P.default_budget_grid(n, 128),
+                                        kind="column_aggregate_topk")
+    ca = X.measured_skyline(cuda_ctx, q, k, v, ca_curves, devices=2, steps=1, policy="column_aggregate_topk")
+    assert all(p.mean_output_error == 0.0 for p in ca if p.total_budget == 8 * n)
+    pq_uniform = [p.mean_output_error for p in pts if p.allocator == "uniform"]
+    ca_uniform = [p.mean_output_error for p in ca if p.allocator == "uniform"]
+    assert all(c >= q_ - 1e-6 for c, q_ in zip(ca_uniform, pq_uniform))
