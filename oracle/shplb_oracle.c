@@ -204,8 +204,15 @@ void orc_colagg_select(const float* scores, int64_t n_q, int64_t n_k, int32_t bq
         const float* row = scores + qb * nkb;
         float mx = -INFINITY;
         for (int64_t j = 0; j < vis; ++j) mx = row[j] > mx ? row[j] : mx;
+        /* z: 32 strided partial sums (partial l over j = l, l+32, ... ascending), then
+         * added in lane order from 0.0f — the GPU's warp-per-row order. */
+        float part[32];
+        for (int l = 0; l < 32; ++l) {
+            part[l] = 0.0f;
+            for (int64_t j = l; j < vis; j += 32) part[l] = part[l] + orc_det_ex2((row[j] - mx) * log2e);
+        }
         float sum = 0.0f;
-        for (int64_t j = 0; j < vis; ++j) sum = sum + orc_det_ex2((row[j] - mx) * log2e);
+        for (int l = 0; l < 32; ++l) sum = sum + part[l];
         m[qb] = mx;
         z[qb] = sum;
     }

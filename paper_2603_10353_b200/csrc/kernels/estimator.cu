@@ -347,20 +347,33 @@ __device__ __forceinline__ float det_ex2(float x) {
 
 constexpr float kLog2e = 1.44269504088896340736f;
 
-// Per (head, query block): m = max visible score, z = sum of det_ex2((s - m) log2 e).
+// Per (head, query block), one warp: m = max visible score, z = sum of
+// det_ex2((s - m) log2 e) as 32 lane-strided partial sums (coalesced reads)
+// added in lane order — the order orc_colagg_select restates.
 __global__ void colagg_rowstats_kernel(const float* __restrict__ scores, int hq, int64_t nqb, int64_t nkb,
                                        int64_t n, int bq, int causal, float* __restrict__ m_out,
                                        float* __restrict__ z_out) {
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (row >= hq * nqb) return;
     const int64_t vis = visible_blocks(row % nqb, n, nkb, bq, causal != 0);
     const float* s = scores + row * nkb;
     float mx = -INFINITY;
-    for (int64_t j = 0; j < vis; ++j) mx = s[j] > mx ? s[j] : mx;
+    for (int64_t j = lane; j < vis; j += 32) mx = s[j] > mx ? s[j] : mx;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const float o = __shfl_xor_sync(0xffffffffu, mx, off);
+        mx = o > mx ? o : mx;
+    }
+    float part = 0.0f;
+    for (int64_t j = lane; j < vis; j += 32) part = __fadd_rn(part, det_ex2(__fmul_rn(__fsub_rn(s[j], mx), kLog2e)));
     float sum = 0.0f;
-    for (int64_t j = 0; j < vis; ++j) sum = __fadd_rn(sum, det_ex2(__fmul_rn(__fsub_rn(s[j], mx), kLog2e)));
-    m_out[row] = mx;
-    z_out[row] = sum;
+#pragma unroll
+    for (int l = 0; l < 32; ++l) sum = __fadd_rn(sum, __shfl_sync(0xffffffffu, part, l));
+    if (lane == 0) {
+        m_out[row] = mx;
+        z_out[row] = sum;
+    }
 }
 
 // Per (head, key block): column sum of the block weights over query blocks, ascending.
@@ -418,8 +431,8 @@ void launch_colagg_select(const float* scores, int hq, int64_t n, int bq, bool c
     float* c = z + hq * nqb;
     int32_t* kk = kept + hq * kmax;
     const int cz = causal ? 1 : 0;
-    colagg_rowstats_kernel<<<static_cast<unsigned>((hq * nqb + 127) / 128), 128, 0, s>>>(scores, hq, nqb, nkb, n,
-                                                                                         bq, cz, m, z);
+    colagg_rowstats_kernel<<<static_cast<unsigned>((hq * nqb * 32 + 127) / 128), 128, 0, s>>>(scores, hq, nqb, nkb,
+                                                                                              n, bq, cz, m, z);
     colagg_colsum_kernel<<<static_cast<unsigned>((hq * nkb + 127) / 128), 128, 0, s>>>(scores, m, z, hq, nqb,
                                                                                        nkb, n, bq, cz, c);
     colagg_select_kernel<<<static_cast<unsigned>((hq * 32 + 127) / 128), 128, 0, s>>>(c, hq, nkb, ht, kmax, kept,
