@@ -79,6 +79,14 @@ int shplb_maxmin_allocate(int32_t num_heads, int64_t context_length,
 int shplb_recovery_at(int64_t n_points, const int64_t* curve_budgets,
                       const double* curve_recovery, int64_t budget, double* recovery_out);
 
+/* budget_for_recovery(curve, p) (profiler.hpp:90, profiler.cpp:198-209): the
+ * smallest sampled budget whose recovery reaches p (within 1e-9) — a per-head
+ * top-p budget fixed offline. Validates the curve (RecoveryCurve::validate) and
+ * p in (0, 1] with the reference's messages; SHPLB_RUNTIME_ERROR when p
+ * exceeds the curve's maximum. */
+int shplb_budget_for_recovery(int64_t n_points, const int64_t* curve_budgets, const double* curve_recovery,
+                              int64_t context_length, double p, int64_t* budget_out);
+
 /* build_profiles + recovery_ratio for PerQueryTopK (profiler.cpp:157-196,
  * attention.cpp:151-184), restated in host C++ (fp64, OpenMP over heads x
  * rows). Offline budget-table input, not the hot path. q_rows: bf16

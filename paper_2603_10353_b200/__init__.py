@@ -7,7 +7,7 @@ from ._native import (CudaError, InvalidArgument, LogicError, NotSupported, Shpl
 from .api import (BLOCK, BLOCK_Q, BLOCK_TOPK, COLUMN_AGGREGATE_TOPK, HEAD_DIM, BudgetAllocation, Context, LoadReport, RecoveryCurve,
                   SimulationResult, barrier, default_budget_grid, greedy_assign, imbalance,
                   layer_work, maxmin_allocate, naive_assign, profile_curves, simulate,
-                  selection_kind, split_assign, uniform_allocate)
+                  selection_kind, split_assign, top_p_budgets, uniform_allocate)
 from . import formats  # noqa: E402  (allocation / assignment / profiles JSON, reference layout)
 from . import experiments  # noqa: E402  (sweep / skyline on measured latency)
 
@@ -17,5 +17,5 @@ __all__ = [
     "SimulationResult",
     "barrier", "build", "default_budget_grid", "greedy_assign", "imbalance", "layer_work", "lib",
     "maxmin_allocate", "naive_assign", "profile_curves", "simulate", "split_assign",
-    "uniform_allocate",
+    "uniform_allocate", "top_p_budgets", "selection_kind", "BLOCK_TOPK", "COLUMN_AGGREGATE_TOPK",
 ]

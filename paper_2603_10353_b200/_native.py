@@ -17,7 +17,7 @@ CSRC_DIR = os.path.join(PKG_DIR, "csrc")
 # Every symbol include/shplb.h declares (checked by the CPU test suite).
 EXPORTS = (
     "shplb_last_error", "shplb_version",
-    "shplb_uniform_allocate", "shplb_maxmin_allocate", "shplb_recovery_at",
+    "shplb_uniform_allocate", "shplb_maxmin_allocate", "shplb_recovery_at", "shplb_budget_for_recovery",
     "shplb_profile_curves_host", "shplb_profile_curves",
     "shplb_profile_curves_host_kind", "shplb_profile_curves_kind",
     "shplb_plan_naive", "shplb_plan_greedy", "shplb_plan_split", "shplb_imbalance",
@@ -135,6 +135,7 @@ def lib() -> C.CDLL:
     L.shplb_maxmin_allocate.argtypes = [i32, i64, vp, vp, vp, i64, i64, i64, i64, vp,
                                         P(MaxminDiag)]
     L.shplb_recovery_at.argtypes = [i64, vp, vp, i64, P(f64)]
+    L.shplb_budget_for_recovery.argtypes = [i64, vp, vp, i64, f64, P(i64)]
     L.shplb_profile_curves_host.argtypes = [vp, vp, i32, i32, i64, i64, i32, vp, i64, vp]
     L.shplb_profile_curves.argtypes = [vp, vp, vp, i32, i32, i64, i64, i32, vp, i64, vp, vp]
     L.shplb_profile_curves_host_kind.argtypes = [vp, vp, i32, i32, i64, i64, i32, vp, i64, i32, vp]

@@ -61,6 +61,22 @@ class RecoveryCurve:
         check(lib().shplb_recovery_at(b.size, _ptr(b), _ptr(r), int(budget), C.byref(out)))
         return float(out.value)
 
+    def budget_for_recovery(self, p: float) -> int:
+        """budget_for_recovery (profiler.cpp:198-209): smallest sampled budget
+        reaching recovery p — a per-head top-p budget fixed offline."""
+        out = C.c_int64()
+        b, r = _i64(self.budgets), _f64(self.recovery)
+        check(lib().shplb_budget_for_recovery(b.size, _ptr(b), _ptr(r), int(self.context_length), float(p),
+                                              C.byref(out)))
+        return int(out.value)
+
+
+def top_p_budgets(curves, p: float) -> np.ndarray:
+    """Per-head budgets of an offline top-p policy (the paper's top-p comparison,
+    PAPER.md:174-177): each head gets the budget its own curve needs to reach
+    recovery p, so the total and the per-head loads are whatever p implies."""
+    return np.asarray([c.budget_for_recovery(p) for c in curves], np.int64)
+
 
 @dataclass
 class BudgetAllocation:

@@ -100,6 +100,30 @@ extern "C" int shplb_recovery_at(int64_t n_points, const int64_t* curve_budgets,
     });
 }
 
+extern "C" int shplb_budget_for_recovery(int64_t n_points, const int64_t* curve_budgets,
+                                         const double* curve_recovery, int64_t context_length, double p,
+                                         int64_t* budget_out) {
+    // budget_for_recovery (profiler.cpp:198-209): the smallest sampled budget
+    // whose recovery reaches p (within 1e-9) — the per-head budget of a top-p
+    // policy fixed offline. Same validation and messages.
+    return guarded([&] {
+        require(budget_out != nullptr && (n_points == 0 || (curve_budgets && curve_recovery)), "bad curve");
+        const CurveView c{curve_budgets, curve_recovery, n_points};
+        validate_curve(c, context_length);
+        if (!(p > 0.0) || p > 1.0)
+            throw InvalidArgument("recovery target p must lie in (0, 1], got " + std::to_string(p));
+        for (int64_t i = 0; i < n_points; ++i) {
+            if (curve_recovery[i] >= p - kEndpointTol) {
+                *budget_out = curve_budgets[i];
+                return;
+            }
+        }
+        double mx = 0.0;
+        for (int64_t i = 0; i < n_points; ++i) mx = std::max(mx, curve_recovery[i]);
+        throw RuntimeError("recovery target " + std::to_string(p) + " exceeds curve maximum " + std::to_string(mx));
+    });
+}
+
 extern "C" int shplb_maxmin_allocate(int32_t num_heads, int64_t context_length,
                                      const int64_t* curve_offsets, const int64_t* curve_budgets,
                                      const double* curve_recovery, int64_t total,

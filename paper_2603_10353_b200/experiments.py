@@ -200,6 +200,46 @@ def measured_skyline(ctx, q, k, v, curves, devices: int, totals=None, quantum: i
     return points
 
 
+@dataclass
+class TopPPoint:
+    """One offline top-p operating point: every head gets the
+    budget its own curve needs to reach recovery p."""
+    p: float
+    total_budget: int
+    mean_output_error: float
+    naive_barrier_latency: float
+    naive_bubble: float
+    greedy_barrier_latency: float
+    greedy_bubble: float
+
+
+def measured_top_p(ctx, q, k, v, curves, devices: int, ps=(0.8, 0.9, 0.95), steps: int = 3,
+                   causal: bool = True, policy=0) -> list:
+    """The paper's top-p comparison on measured latency: per-head budgets from
+    budget_for_recovery(curve, p) (profiler.cpp:198-209), their output error
+    against dense attention, and the barrier latency / bubble of those budgets
+    placed by even head parallelism (naive) and by the greedy balancer — the
+    cross-GPU imbalance a per-head top-p budget creates."""
+    import torch
+    hq = q.shape[0]
+    dense = ctx.dense_attention_layer(q, k, v, causal=causal)
+    out = torch.empty_like(q)
+    points = []
+    for p in ps:
+        budgets = api.top_p_budgets(curves, p)
+        budgets = np.maximum(budgets, 1)
+        ctx.sparse_attention_layer(q, k, v, budgets, out=out, causal=causal, kind=policy)
+        torch.cuda.synchronize()
+        err = float(np.mean([output_error(out[h], dense[h]) for h in range(hq)]))
+        _, rn = measured_barrier(ctx, q, k, v, budgets, api.naive_assign(budgets, devices), devices, steps,
+                                 kind=policy)
+        _, rg = measured_barrier(ctx, q, k, v, budgets, api.greedy_assign(budgets, devices), devices, steps,
+                                 kind=policy)
+        points.append(TopPPoint(float(p), int(budgets.sum()), err, rn.barrier_latency, rn.bubble_fraction,
+                                rg.barrier_latency, rg.bubble_fraction))
+    return points
+
+
 def write_skyline_csv(path_or_file, rows) -> None:
     """write_skyline_csv (commands.cpp:491-499); barrier_latency in ms."""
     lines = ["total_budget,allocator,mean_output_error,barrier_latency"]

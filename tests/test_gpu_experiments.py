@@ -68,3 +68,22 @@ def test_measured_sweep_and_skyline_small(cuda_ctx):
     pq_uniform = [p.mean_output_error for p in pts if p.allocator == "uniform"]
     ca_uniform = [p.mean_output_error for p in ca if p.allocator == "uniform"]
     assert all(c >= q_ - 1e-6 for c, q_ in zip(ca_uniform, pq_uniform))
+
+
+def test_measured_top_p(cuda_ctx):
+    """The offline top-p comparison: budgets from each head's
+    curve; a larger p never lowers any head's budget or raises the error, and
+    the greedy balancer is never worse than even head parallelism on them."""
+    spec = LayerSpec(num_q_heads=8, num_kv_heads=2, seq_len=2048, seed=5)
+    q, k, v = make_layer(spec, "cuda")
+    n = spec.seq_len
+    curves = cuda_ctx.profile_curves(q[:, n - 16:, :].contiguous(), k, P.default_budget_grid(n, 128))
+    pts = X.measured_top_p(cuda_ctx, q, k, v, curves, devices=2, ps=(0.5, 0.9, 1.0), steps=1)
+    assert [p.p for p in pts] == [0.5, 0.9, 1.0]
+    assert pts[-1].total_budget == 8 * n and pts[-1].mean_output_error == 0.0  # p = 1 keeps everything
+    for a, b in zip(pts, pts[1:]):
+        assert a.total_budget <= b.total_budget and a.mean_output_error >= b.mean_output_error - 1e-9
+    b5, b9 = P.top_p_budgets(curves, 0.5), P.top_p_budgets(curves, 0.9)
+    assert np.all(b5 <= b9)
+    for p in pts:
+        assert p.greedy_barrier_latency <= p.naive_barrier_latency * 1.05

@@ -274,3 +274,33 @@ def test_split_plan_beats_whole_head_plans():
     tiles_per_head = [P.layer_work(1, 1, 131072, [b], kv_map=[0])[0] for b in budgets]
     g_loads = np.bincount(g, weights=tiles_per_head, minlength=8)
     assert sp.loads.max() / sp.loads.mean() < 1.01 < g_loads.max() / g_loads.mean()
+
+
+def test_budget_for_recovery_known_answers():
+    """test_profiler.cpp:123-141 ('budget_for_recovery walks the sampled grid')."""
+    uniform = P.RecoveryCurve(np.arange(1025, dtype=np.int64), np.arange(1025) / 1024.0, 1024)
+    assert uniform.budget_for_recovery(0.9) == 922
+    assert uniform.budget_for_recovery(1.0) == 1024
+    onehot = P.RecoveryCurve(np.array([1, 1024], np.int64), np.array([1.0, 1.0]), 1024)
+    assert onehot.budget_for_recovery(0.9) == 1
+    with pytest.raises(P.InvalidArgument, match=r"recovery target p must lie in \(0, 1\], got 0.000000"):
+        uniform.budget_for_recovery(0.0)
+    with pytest.raises(P.InvalidArgument, match=r"got 1.500000"):
+        uniform.budget_for_recovery(1.5)
+    with pytest.raises(P.InvalidArgument, match="final recovery must be 1"):
+        P.RecoveryCurve(np.array([512, 1024], np.int64), np.array([0.5, 0.9]), 1024).budget_for_recovery(0.5)
+
+
+def test_budget_for_recovery_matches_scan_of_real_curves():
+    """'matches the prefix-sum scan oracle' (test_profiler.cpp:143-151): on
+    profiled curves the top-p budget is the first grid point at or above p,
+    and top_p_budgets applies it per head."""
+    rng = np.random.default_rng(3)
+    q = O.f32_to_bf16_bits(rng.standard_normal((3, 4, 128)).astype(np.float32) * 0.4)
+    k = O.f32_to_bf16_bits(rng.standard_normal((1, 256, 128)).astype(np.float32))
+    curves = P.profile_curves(q, k, P.default_budget_grid(256, 1))
+    for p in (0.5, 0.9, 0.99):
+        b = P.top_p_budgets(curves, p)
+        for h, c in enumerate(curves):
+            first = int(c.budgets[np.argmax(c.recovery >= p - 1e-9)])
+            assert b[h] == first
