@@ -111,6 +111,8 @@ def _load_ref():
                                           C.POINTER(C.c_int64)]
         L.ref_budget_for_recovery.argtypes = [C.c_int64, C.c_int64, _i64p, _f64p, C.c_double,
                                               C.POINTER(C.c_int64)]
+        L.ref_stability_score.argtypes = [C.c_int32, C.c_int32, _i32p, _i32p, C.c_int64, _i64p, _i64p, _f64p,
+                                          C.c_char_p, C.c_double, C.c_int, C.POINTER(C.c_double)]
         L.ref_naive_assign.argtypes = [_i64p, C.c_int32, C.c_int32, C.c_int, _i32p]
         L.ref_greedy_assign.argtypes = [_i64p, C.c_int32, C.c_int32, _i32p]
         L.ref_optimal_assign.argtypes = [_i64p, C.c_int32, C.c_int32, _i32p]
@@ -409,6 +411,26 @@ class ref:
         _ref_check(_load_ref().ref_build_profiles(Q, K, V, h, n_q, K.shape[1], d, grid, grid.size,
                                                   kind, int(causal), out))
         return out
+
+    @staticmethod
+    def stability_score(groups, p, norm="max"):
+        """groups: [(request name, [(layer, head)], [curve])] with curves having
+        .budgets / .recovery and one shared context length."""
+        n_groups, n_heads = len(groups), len(groups[0][1])
+        layers = np.array([lh[0] for _, ids, _ in groups for lh in ids], np.int32)
+        heads = np.array([lh[1] for _, ids, _ in groups for lh in ids], np.int32)
+        curves = [c for _, _, cs in groups for c in cs]
+        offsets = np.zeros(len(curves) + 1, np.int64)
+        for i, c in enumerate(curves):
+            offsets[i + 1] = offsets[i] + len(c.budgets)
+        b = np.ascontiguousarray(np.concatenate([np.asarray(c.budgets, np.int64) for c in curves]))
+        r = np.ascontiguousarray(np.concatenate([np.asarray(c.recovery, np.float64) for c in curves]))
+        names = b"".join(name.encode().ljust(64, b"\0")[:64] for name, _, _ in groups)
+        out = C.c_double()
+        _ref_check(_load_ref().ref_stability_score(n_groups, n_heads, layers, heads, int(curves[0].context_length),
+                                                   offsets, b, r, names, float(p), 0 if norm == "max" else 1,
+                                                   C.byref(out)))
+        return float(out.value)
 
     @staticmethod
     def uniform_allocate(n, total, floor, n_k):

@@ -229,6 +229,32 @@ int ref_budget_for_recovery(int64_t n_points, int64_t context_length, const int6
     });
 }
 
+// headbal::stability_score (profiler.cpp:233-292). n_groups requests of n_heads
+// profiles each; profile (g, h) has id (layers[g*n_heads+h], heads[...]) and the
+// curve offsets[g*n_heads+h] .. +1 into budgets / recovery; names: n_groups
+// request names, each in a 64-byte slot. norm 0 = Max, 1 = Sum.
+int ref_stability_score(int32_t n_groups, int32_t n_heads, const int32_t* layers, const int32_t* heads,
+                        int64_t context_length, const int64_t* offsets, const int64_t* budgets,
+                        const double* recovery, const char* names, double p, int norm, double* out) {
+    return guarded([&] {
+        std::vector<std::vector<headbal::HeadProfile>> groups(static_cast<std::size_t>(n_groups));
+        for (int32_t g = 0; g < n_groups; ++g) {
+            for (int32_t h = 0; h < n_heads; ++h) {
+                const int64_t i = static_cast<int64_t>(g) * n_heads + h;
+                headbal::HeadProfile hp;
+                hp.curve.id = headbal::HeadId{layers[i], heads[i]};
+                hp.curve.context_length = context_length;
+                for (int64_t q = offsets[i]; q < offsets[i + 1]; ++q) hp.curve.points.push_back({budgets[q], recovery[q]});
+                hp.provenance = {std::string(names + 64 * g), "parity"};
+                hp.policy = headbal::SelectionKind::PerQueryTopK;
+                groups[static_cast<std::size_t>(g)].push_back(hp);
+            }
+        }
+        *out = headbal::stability_score(groups, p,
+                                        norm == 0 ? headbal::BudgetNormalization::Max : headbal::BudgetNormalization::Sum);
+    });
+}
+
 // headbal::naive_assign / greedy_assign / optimal_assign (partitioner.cpp:130-234).
 int ref_naive_assign(const int64_t* budgets, int32_t n, int32_t devices, int round_robin,
                      int32_t* device_of_head) {

@@ -367,3 +367,62 @@ def load_profiles(path: str) -> LoadedProfiles:
         heads.append(hid)
         prov.append((req, tsk))
     return LoadedProfiles(curves, heads, policy, n_k, prov)
+
+
+def _pearson(a, b) -> float:
+    # pearson (profiler.cpp:212-229), same accumulation order
+    n = float(len(a))
+    mean_a = mean_b = 0.0
+    for x, y in zip(a, b):
+        mean_a += x
+        mean_b += y
+    mean_a /= n
+    mean_b /= n
+    cov = var_a = var_b = 0.0
+    for x, y in zip(a, b):
+        da, db = x - mean_a, y - mean_b
+        cov += da * db
+        var_a += da * da
+        var_b += db * db
+    return cov / math.sqrt(var_a * var_b)
+
+
+def stability_score(request_groups, p: float, normalization: str = "max") -> float:
+    """stability_score (profiler.hpp:98-104, profiler.cpp:233-292): the paper's
+    cross-request stability of relative head sparsity. Each
+    group is one calibration request's LoadedProfiles; per request the per-head
+    budget_for_recovery(p) vector (heads in (layer, head) order) is normalised
+    by its max ("max") or sum ("sum"), and the minimum pairwise Pearson
+    correlation is returned. Same errors and messages as the reference."""
+    if len(request_groups) < 2:
+        raise InvalidArgument("stability_score needs at least 2 calibration requests")
+    if normalization not in ("max", "sum"):
+        raise InvalidArgument('normalization must be "max" or "sum"')
+    vectors, id_sets = [], []
+    for g, group in enumerate(request_groups):
+        prov = getattr(group, "provenance", None) or []
+        name = prov[0][0] if prov and prov[0][0] else f"request #{g}"
+        if not group.curves:
+            raise InvalidArgument(f"{name}: empty profile group")
+        heads = group.heads or [(0, h) for h in range(len(group.curves))]
+        order = sorted(range(len(group.curves)), key=lambda i: tuple(heads[i]))
+        budgets, ids = [], []
+        for i in order:
+            c = group.curves[i]
+            budgets.append(float(c.budget_for_recovery(p)))
+            ids.append(tuple(heads[i]))
+        if g > 0 and ids != id_sets[0]:
+            raise InvalidArgument(f"{name}: head set differs from the first request")
+        denom = max(budgets) if normalization == "max" else sum(budgets)  # std::accumulate order
+        if denom <= 0.0:
+            raise InvalidArgument(f"{name}: budget vector cannot be normalized")
+        budgets = [b / denom for b in budgets]
+        if all(b == budgets[0] for b in budgets):
+            raise InvalidArgument(f"{name}: budget vector has zero variance, correlation undefined")
+        vectors.append(budgets)
+        id_sets.append(ids)
+    worst = 1.0
+    for i in range(len(vectors)):
+        for j in range(i + 1, len(vectors)):
+            worst = min(worst, _pearson(vectors[i], vectors[j]))
+    return worst

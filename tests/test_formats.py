@@ -3,6 +3,7 @@ profiles.json written by the reference library load unchanged here, files
 written here load in the reference and are byte-identical to the reference's
 own output, and malformed files fail with the reference's messages
 (allocator.cpp:223-275, partitioner.cpp:268-336, profiler.cpp:300-383)."""
+import ctypes as C
 import json
 import os
 
@@ -189,3 +190,83 @@ def test_missing_file_and_bad_policy(tmp_path):
     with pytest.raises(P.InvalidArgument, match='unknown selection policy "top_p"'):
         F.load_profiles(p)
     assert os.path.exists(p)
+
+
+# ---------------------------------------------------------------------------
+# stability_score (profiler.cpp:233-292): the paper's cross-request stability
+# ---------------------------------------------------------------------------
+
+def _step_curve(n_k, knee):
+    """Recovery 0 below `knee` tokens, 1 from it on (test_profiler.cpp step_curve)."""
+    b = sorted({0, knee, n_k})
+    return P.RecoveryCurve(np.array(b, np.int64), np.array([0.0 if x < knee else 1.0 for x in b]), n_k)
+
+
+def _group(curves, request, heads=None):
+    from paper_2603_10353_b200.formats import LoadedProfiles
+    heads = heads or [(0, h) for h in range(len(curves))]
+    return LoadedProfiles(curves, heads, "per_query_topk", curves[0].context_length,
+                          [(request, "parity")] * len(curves))
+
+
+def test_stability_identical_and_rescaled_requests():
+    """'stability is 1 for identical and for rescaled requests' (test_profiler.cpp:167-178)."""
+    from paper_2603_10353_b200.formats import stability_score
+    base = _group([_step_curve(1024, 64), _step_curve(1024, 256), _step_curve(1024, 512)], "req-a")
+    assert stability_score([base, base, base], 0.9) == pytest.approx(1.0, abs=1e-12)
+    doubled = _group([_step_curve(2048, 128), _step_curve(2048, 512), _step_curve(2048, 1024)], "req-b")
+    assert stability_score([base, doubled], 0.9) == pytest.approx(1.0, abs=1e-12)
+    assert stability_score([base, doubled], 0.9, "sum") == pytest.approx(1.0, abs=1e-12)
+
+
+def test_stability_rejects_degenerate_and_mismatched_groups():
+    """test_profiler.cpp:208-221, with the reference's messages."""
+    from paper_2603_10353_b200.formats import stability_score
+    degenerate = _group([_step_curve(64, 16), _step_curve(64, 16)], "flat-request")
+    good = _group([_step_curve(64, 8), _step_curve(64, 32)], "ok-request")
+    with pytest.raises(P.InvalidArgument, match="flat-request: budget vector has zero variance"):
+        stability_score([good, degenerate], 0.9)
+    with pytest.raises(P.InvalidArgument, match="needs at least 2 calibration requests"):
+        stability_score([good], 0.9)
+    other = _group([_step_curve(64, 8), _step_curve(64, 32)], "req-x", heads=[(0, 0), (0, 5)])
+    with pytest.raises(P.InvalidArgument, match="req-x: head set differs from the first request"):
+        stability_score([good, other], 0.9)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built")
+def test_stability_matches_reference_on_profiled_requests():
+    """Three calibration 'requests' (different query rows of one synthetic head
+    set), profiled here: the score equals the reference's stability_score."""
+    from paper_2603_10353_b200.formats import stability_score
+    rng = np.random.default_rng(17)
+    k = O.f32_to_bf16_bits(rng.standard_normal((2, 512, 128)).astype(np.float32))
+    temps = rng.uniform(0.05, 0.6, (8, 1, 1)).astype(np.float32)
+    groups, ref_groups = [], []
+    for req in range(3):
+        q = O.f32_to_bf16_bits(rng.standard_normal((8, 6, 128)).astype(np.float32) * temps)
+        curves = P.profile_curves(q, k, P.default_budget_grid(512, 8))
+        heads = [(1, h) for h in range(8)][::-1]  # out of order on purpose: sorted by id inside
+        curves = curves[::-1]
+        groups.append(_group(curves, f"request-{req}", heads))
+        ref_groups.append((f"request-{req}", heads, curves))
+    for p in (0.5, 0.9):
+        for norm in ("max", "sum"):
+            ours = stability_score(groups, p, norm)
+            ref = O.ref.stability_score(ref_groups, p, norm)
+            assert ours == pytest.approx(ref, abs=1e-12), (p, norm, ours, ref)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built")
+def test_budget_for_recovery_matches_reference_on_random_curves():
+    rng = np.random.default_rng(4)
+    for _ in range(50):
+        n_k = int(rng.integers(2, 400))
+        pts = np.unique(np.concatenate([[n_k], rng.integers(0, n_k, rng.integers(1, 20))]))
+        rec = np.sort(rng.uniform(0, 1, pts.size))
+        rec[-1] = 1.0
+        c = P.RecoveryCurve(pts.astype(np.int64), rec, n_k)
+        for p in rng.uniform(0.01, 1.0, 5):
+            out = C.c_int64()
+            O._load_ref().ref_budget_for_recovery(pts.size, n_k, np.ascontiguousarray(pts, np.int64),
+                                                  np.ascontiguousarray(rec), float(p), C.byref(out))
+            assert c.budget_for_recovery(float(p)) == out.value
