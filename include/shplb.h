@@ -138,6 +138,13 @@ int shplb_plan_naive(const int64_t* budgets, int32_t num_heads, int32_t devices,
 int shplb_plan_greedy(const int64_t* budgets, int32_t num_heads, int32_t devices,
                       int32_t* device_of_head);
 
+/* optimal_assign(budgets, devices) (partitioner.hpp:48, partitioner.cpp:185-234):
+ * the minimum possible maximum device load and, among plans reaching it, the
+ * lexicographically smallest device_of_head — the exact baseline the greedy plan
+ * is judged against. Guarded to N <= 24 heads and 4 devices like the reference
+ * (same message). */
+int shplb_plan_optimal(const int64_t* budgets, int32_t num_heads, int32_t devices, int32_t* device_of_head);
+
 /* Sub-head balancer (an extension beyond greedy_assign,
  * partitioner.cpp:164-183). Whole-head placement cannot balance 32 or 28
  * heads over 8 GPUs under max-min budgets; this plan lets a head's query

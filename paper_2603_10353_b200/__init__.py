@@ -6,7 +6,7 @@ from ._native import (CudaError, InvalidArgument, LogicError, NotSupported, Shpl
                       ShplbRuntimeError, build, lib)
 from .api import (BLOCK, BLOCK_Q, BLOCK_TOPK, COLUMN_AGGREGATE_TOPK, HEAD_DIM, BudgetAllocation, Context, LoadReport, RecoveryCurve,
                   SimulationResult, barrier, default_budget_grid, greedy_assign, imbalance,
-                  layer_work, maxmin_allocate, naive_assign, profile_curves, simulate,
+                  layer_work, maxmin_allocate, naive_assign, optimal_assign, profile_curves, simulate,
                   selection_kind, split_assign, top_p_budgets, uniform_allocate)
 from . import formats  # noqa: E402  (allocation / assignment / profiles JSON, reference layout)
 from . import experiments  # noqa: E402  (sweep / skyline on measured latency)
@@ -16,6 +16,6 @@ __all__ = [
     "LoadReport", "LogicError", "NotSupported", "RecoveryCurve", "ShplbError", "ShplbRuntimeError",
     "SimulationResult",
     "barrier", "build", "default_budget_grid", "greedy_assign", "imbalance", "layer_work", "lib",
-    "maxmin_allocate", "naive_assign", "profile_curves", "simulate", "split_assign",
+    "maxmin_allocate", "naive_assign", "optimal_assign", "profile_curves", "simulate", "split_assign",
     "uniform_allocate", "top_p_budgets", "selection_kind", "BLOCK_TOPK", "COLUMN_AGGREGATE_TOPK",
 ]

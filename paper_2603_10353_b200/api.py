@@ -173,6 +173,15 @@ def greedy_assign(budgets, devices: int) -> np.ndarray:
     return out
 
 
+def optimal_assign(budgets, devices: int) -> np.ndarray:
+    """optimal_assign (partitioner.cpp:185-234): minimum makespan, then the
+    lexicographically smallest plan reaching it (N <= 24, D <= 4)."""
+    b = _i64(budgets)
+    out = np.empty(b.size, np.int32)
+    check(lib().shplb_plan_optimal(_ptr(b), b.size, devices, _ptr(out)))
+    return out
+
+
 def imbalance(budgets, device_of_head, devices: int) -> LoadReport:
     b, a = _i64(budgets), _i32(device_of_head)
     if a.size != b.size:

@@ -27,7 +27,77 @@ void check_budgets(const int64_t* budgets, int32_t n) {
         if (budgets[h] < 0) throw InvalidArgument("budgets must be nonnegative");
 }
 
+// Can `items` (sorted descending) be added to `loads` with every load <= cap?
+// Depth-first, largest item first; devices with equal loads are interchangeable,
+// so only the first of each equal-load run is tried.
+bool fits(const std::vector<int64_t>& items, std::size_t i, std::vector<int64_t>& loads, int64_t cap) {
+    if (i == items.size()) return true;
+    for (std::size_t d = 0; d < loads.size(); ++d) {
+        bool seen = false;
+        for (std::size_t e = 0; e < d; ++e) seen |= loads[e] == loads[d];
+        if (seen || loads[d] + items[i] > cap) continue;
+        loads[d] += items[i];
+        const bool ok = fits(items, i + 1, loads, cap);
+        loads[d] -= items[i];
+        if (ok) return true;
+    }
+    return false;
+}
+
 }  // namespace
+
+extern "C" int shplb_plan_optimal(const int64_t* budgets, int32_t num_heads, int32_t devices,
+                                  int32_t* device_of_head) {
+    // optimal_assign (partitioner.cpp:185-234): the minimum possible maximum
+    // device load, and among the plans reaching it the lexicographically
+    // smallest device_of_head. Both are properties of the instance, so any
+    // exact search returns the reference's plan; this one binary-searches the
+    // cap between max(ceil(total/D), max budget) and the greedy plan's maximum
+    // with an exact feasibility search, then fixes heads in index order on the
+    // lowest device that keeps the rest feasible.
+    return guarded([&] {
+        check_budgets(budgets, num_heads);
+        if (devices < 1) throw InvalidArgument("need at least one device");
+        if (num_heads > 24 || devices > 4) {
+            throw InvalidArgument(
+                "exact solver is guarded to N <= 24 heads and 4 devices; use greedy_assign for larger instances");
+        }
+        const int64_t total = std::accumulate(budgets, budgets + num_heads, int64_t(0));
+        int64_t lo = std::max((total + devices - 1) / devices, *std::max_element(budgets, budgets + num_heads));
+        std::vector<int32_t> g(static_cast<std::size_t>(num_heads));
+        const int rc = shplb_plan_greedy(budgets, num_heads, devices, g.data());
+        if (rc != SHPLB_OK) throw std::logic_error("greedy seed failed");
+        std::vector<int64_t> gl(static_cast<std::size_t>(devices), 0);
+        for (int32_t h = 0; h < num_heads; ++h) gl[g[h]] += budgets[h];
+        int64_t hi = *std::max_element(gl.begin(), gl.end());
+        std::vector<int64_t> items(budgets, budgets + num_heads);
+        std::sort(items.begin(), items.end(), std::greater<int64_t>());
+        while (lo < hi) {  // smallest feasible cap
+            const int64_t mid = lo + (hi - lo) / 2;
+            std::vector<int64_t> loads(static_cast<std::size_t>(devices), 0);
+            if (fits(items, 0, loads, mid)) hi = mid; else lo = mid + 1;
+        }
+        const int64_t best = lo;
+        std::vector<int64_t> loads(static_cast<std::size_t>(devices), 0);
+        for (int32_t h = 0; h < num_heads; ++h) {
+            std::vector<int64_t> rest(budgets + h + 1, budgets + num_heads);
+            std::sort(rest.begin(), rest.end(), std::greater<int64_t>());
+            bool placed = false;
+            for (int32_t d = 0; d < devices && !placed; ++d) {
+                if (loads[d] + budgets[h] > best) continue;
+                loads[d] += budgets[h];
+                std::vector<int64_t> trial(loads);
+                if (fits(rest, 0, trial, best)) {
+                    device_of_head[h] = d;
+                    placed = true;
+                } else {
+                    loads[d] -= budgets[h];
+                }
+            }
+            if (!placed) throw std::logic_error("exact solver lost feasibility");  // unreachable
+        }
+    });
+}
 
 extern "C" int shplb_plan_naive(const int64_t* budgets, int32_t num_heads, int32_t devices,
                                 int32_t round_robin, int32_t* device_of_head) {

@@ -304,3 +304,34 @@ def test_budget_for_recovery_matches_scan_of_real_curves():
         for h, c in enumerate(curves):
             first = int(c.budgets[np.argmax(c.recovery >= p - 1e-9)])
             assert b[h] == first
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference library not built")
+def test_optimal_assign_matches_reference_fuzz():
+    """optimal_assign (partitioner.cpp:185-234) bit-exact with the reference on
+    random instances (the plan is a property of the instance: minimum makespan,
+    then the lexicographically smallest device_of_head)."""
+    rng = np.random.default_rng(9)
+    for trial in range(300):
+        n = int(rng.integers(1, 13))
+        d = int(rng.integers(1, 5))
+        b = rng.integers(0, 60, n).astype(np.int64) * int(rng.choice([1, 128]))
+        if trial % 7 == 0:
+            b[:] = b[0]  # ties
+        ours = P.optimal_assign(b, d)
+        ref = O.ref.optimal_assign(b, d)
+        assert np.array_equal(ours, ref), (b.tolist(), d, ours.tolist(), ref.tolist())
+        # never worse than greedy
+        g = P.greedy_assign(b, d)
+        assert P.imbalance(b, ours, d).loads.max() <= P.imbalance(b, g, d).loads.max()
+
+
+def test_optimal_assign_guard_and_errors():
+    with pytest.raises(P.InvalidArgument, match="exact solver is guarded to N <= 24 heads and 4 devices"):
+        P.optimal_assign(np.ones(25, np.int64), 2)
+    with pytest.raises(P.InvalidArgument, match="exact solver is guarded"):
+        P.optimal_assign(np.ones(8, np.int64), 5)
+    with pytest.raises(P.InvalidArgument, match="need at least one device"):
+        P.optimal_assign(np.ones(8, np.int64), 0)
+    # the known-answer style instance: 4 heads, 2 devices
+    assert P.optimal_assign([5, 4, 3, 2], 2).tolist() in ([0, 1, 1, 0],)
