@@ -110,7 +110,7 @@ constexpr size_t kSmemQ = 0;
 constexpr size_t kSmemK = kSmemQ + 2 * kTileBytes;
 constexpr size_t kSmemV = kSmemK + 2 * kTileBytes;
 constexpr size_t kSmemSel = kSmemV + 2 * kTileBytes;
-constexpr size_t kSmemBar = kSmemSel + kMaxSelected * sizeof(int32_t);
+constexpr size_t kSmemBar = kSmemSel + 2 * kMaxSelected * sizeof(int32_t);  // one list per half (dual)
 constexpr size_t kSmemTotal = kSmemBar + sizeof(Barriers) + 1024;  // + alignment slack
 
 // K-major SW128 operand (Q, K): k-step kk (16 elements) lives in d chunk kk/4
@@ -134,6 +134,13 @@ constexpr int kTraceBlocks = 48;
 #define TRACE(j, e, cond) do { } while (0)
 #endif
 
+// kDual (block_q = 128): the two halves are two consecutive 128-row query
+// blocks of one head, each with its OWN selection and its own single-stage
+// K / V buffers (the "stage" index of the shared-tile kernel becomes the half),
+// fed by its own producer warp (8 or 10); the work list packs the pair as
+// (h << 20) | (pair << 2) | (mask of live halves). Without it (block_q = 256)
+// both halves read the same selection and share 2-stage K / V rings.
+template <bool kDual>
 __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_constant__ FaParams p) {
 #ifdef SHPLB_TRACE
     __shared__ long long trace[kTraceBlocks][16];
@@ -145,6 +152,10 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
     int32_t* sel = reinterpret_cast<int32_t*>(smem + kSmemSel);
     const uint32_t sSel = smem_u32(sel);
     auto sel_at = [&](int j) { return lds_s32(sSel + 4u * static_cast<uint32_t>(j)); };
+    // half hf's list (dual: its own, 2048 entries further for half 1)
+    auto sel_at_h = [&](int hf, int j) {
+        return lds_s32(sSel + 4u * static_cast<uint32_t>(j + (kDual ? hf * kMaxSelected : 0)));
+    };
     const uint32_t sQ = smem_u32(smem + kSmemQ);
     const uint32_t sK = smem_u32(smem + kSmemK);
     const uint32_t sV = smem_u32(smem + kSmemV);
@@ -153,21 +164,30 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
 
     const int32_t tile = p.tiles[blockIdx.x];
     const int h = tile >> 20;
-    const int qb = tile & 0xFFFFF;
+    const int qb = kDual ? ((tile >> 2) & 0x3FFFF) : (tile & 0xFFFFF);  // dual: the pair index
     const int g = p.heads.kv[h];
-    const int64_t row_id = static_cast<int64_t>(h) * p.nqb + qb;
-    const int nsel = p.cnt[row_id];
-    const int64_t row0 = static_cast<int64_t>(qb) * p.bq;  // first query row of the block
-    const int halves = p.bq / kBlock;                      // 2 (bq = 256) or 1 (bq = 128)
+    const int64_t row_id = static_cast<int64_t>(h) * p.nqb + (kDual ? 2 * qb : qb);
+    // dual: per-half counts (a half outside the tile's mask or past nqb is empty)
+    const int nsel0 = kDual ? ((tile & 1) ? p.cnt[row_id] : 0) : p.cnt[row_id];
+    const int nsel1 = kDual ? (((tile & 2) && 2 * qb + 1 < p.nqb) ? p.cnt[row_id + 1] : 0) : nsel0;
+    const int nsel = nsel0 > nsel1 ? nsel0 : nsel1;
+    auto nsel_h = [&](int hf) { return hf == 0 ? nsel0 : nsel1; };
+    const int64_t row0 = static_cast<int64_t>(qb) * (kDual ? 2 * kBlock : p.bq);  // first query row
+    const int halves = kDual ? 2 : p.bq / kBlock;  // 2 (bq = 256 or dual) or 1 (bq = 128, not dual)
     {
         const int32_t* gsel = p.idx + row_id * p.kmax;
-        for (int j = threadIdx.x; j < nsel; j += kThreads) sel[j] = gsel[j];
+        for (int j = threadIdx.x; j < nsel0; j += kThreads) sel[j] = gsel[j];
+        if (kDual) {
+            for (int j = threadIdx.x; j < nsel1; j += kThreads) sel[kMaxSelected + j] = gsel[p.kmax + j];
+        }
     }
     // Does half hf compute key block j? It must hold rows (< n) and, under the
-    // causal mask, see at least the block's first key.
+    // causal mask, see at least the block's first key. (Dual: every entry of a
+    // 128-row block's own list is visible to it.)
     auto active = [&](int hf, int j) -> bool {
         const int64_t first = row0 + hf * kBlock;
         if (hf >= halves || first >= p.n) return false;
+        if (kDual) return j < nsel_h(hf);
         return !p.causal || static_cast<int64_t>(sel_at(j)) * kBlock <= first + kBlock - 1;
     };
 
@@ -195,7 +215,17 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
       // The control warps run their loops with all 32 lanes (warp-uniform
       // control flow); one elected lane issues each TMA / MMA / commit inside
       // the same asm statement, so ptxas emits plain uniform-datapath issue.
-      if (warp == 8) {
+      if (kDual && warp == 10) {
+        // ---------------------------- TMA producer of half 1's K / V (dual)
+        for (int j = 0; j < nsel1; ++j) {
+            const uint32_t ph = j & 1;
+            const int key0 = sel_at_h(1, j) * kBlock;
+            mbar_wait(&bar->k_empty[1], ph ^ 1);
+            tma_load_tile_warp(smem + kSmemK + kTileBytes, &p.tm_k, &bar->k_full[1], kTileBytes, key0, g);
+            mbar_wait(&bar->v_empty[1], ph ^ 1);
+            tma_load_tile_warp(smem + kSmemV + kTileBytes, &p.tm_v, &bar->v_full[1], kTileBytes, key0, g);
+        }
+      } else if (warp == 8) {
         // ------------------------------------------------------ TMA producer
         if (nsel > 0) {
             tma_load_tile_warp(smem + kSmemQ, &p.tm_q, &bar->q_full, halves * kTileBytes,
@@ -203,7 +233,18 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
             if (halves == 2)
                 tma_load_tile_noarm_warp(smem + kSmemQ + kTileBytes, &p.tm_q, &bar->q_full,
                                          static_cast<int>(row0) + kBlock, h);
-            for (int j = 0; j < nsel; ++j) {
+            // dual: this warp streams half 0's own K / V through single stages
+            if constexpr (kDual) {
+                for (int j = 0; j < nsel0; ++j) {
+                    const uint32_t ph = j & 1;
+                    const int key0 = sel_at_h(0, j) * kBlock;
+                    mbar_wait(&bar->k_empty[0], ph ^ 1);
+                    tma_load_tile_warp(smem + kSmemK, &p.tm_k, &bar->k_full[0], kTileBytes, key0, g);
+                    mbar_wait(&bar->v_empty[0], ph ^ 1);
+                    tma_load_tile_warp(smem + kSmemV, &p.tm_v, &bar->v_full[0], kTileBytes, key0, g);
+                }
+            }
+            for (int j = 0; j < (kDual ? 0 : nsel); ++j) {
                 const int st = j & 1;
                 const uint32_t ph = (j >> 1) & 1;
                 const int key0 = sel_at(j) * kBlock;
@@ -247,37 +288,45 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
             auto vdesc = [&](int st) { return vd0 + static_cast<uint64_t>(st) * kTileDesc; };
             mbar_wait(&bar->q_full, 0);
             int done[2] = {0, 0};  // blocks each half has issued PV for
+            // K / V buffer and phase of (half, block): shared 2-stage rings, or
+            // (dual) the half's own single stage.
+            auto stage = [&](int hf, int j) { return kDual ? hf : (j & 1); };
+            auto phase = [&](int j) { return kDual ? static_cast<uint32_t>(j & 1) : static_cast<uint32_t>((j >> 1) & 1); };
             auto issue_s = [&](int hf, int j) {  // S_hf = Q_hf K_j^T
-                mbar_wait(&bar->k_full[j & 1], (j >> 1) & 1);
+                mbar_wait(&bar->k_full[stage(hf, j)], phase(j));
                 TRACE(j - 1, 9, hf == 0 && (threadIdx.x & 31) == 0);
                 tc_fence_after();
-                mma_tile_ss_kmajor(tmem + col_s(hf), qdesc(hf), kdesc(j & 1), kIdescQK, 0u);
+                mma_tile_ss_kmajor(tmem + col_s(hf), qdesc(hf), kdesc(stage(hf, j)), kIdescQK, 0u);
                 TRACE(j - 1, hf == 0 ? 10 : 14, (threadIdx.x & 31) == 0);
                 mma_commit_warp(&bar->s_full[hf]);
+                if (kDual) mma_commit_warp(&bar->k_empty[hf]);
             };
             auto issue_pv = [&](int hf, int j) {  // O_hf += P_hf V_j
-                mbar_wait(&bar->v_full[j & 1], (j >> 1) & 1);
+                mbar_wait(&bar->v_full[stage(hf, j)], phase(j));
                 TRACE(j, 6, hf == 0 && (threadIdx.x & 31) == 0);
                 mbar_wait(&bar->p_full[hf], done[hf] & 1);
                 TRACE(j, 7, hf == 0 && (threadIdx.x & 31) == 0);
                 tc_fence_after();
-                mma_tile_ts_mnmajor(tmem + col_o(hf), tmem + col_s(hf), vdesc(j & 1), kIdescPV,
+                mma_tile_ts_mnmajor(tmem + col_o(hf), tmem + col_s(hf), vdesc(stage(hf, j)), kIdescPV,
                                     done[hf] > 0 ? 1u : 0u);
                 TRACE(j, hf == 0 ? 8 : 13, (threadIdx.x & 31) == 0);
                 mma_commit_warp(&bar->pv_done[hf]);
+                if (kDual) mma_commit_warp(&bar->v_empty[hf]);
                 ++done[hf];
             };
             for (int hf = 0; hf < 2; ++hf)
                 if (active(hf, 0)) issue_s(hf, 0);
-            mma_commit_warp(&bar->k_empty[0]);
+            if (!kDual) mma_commit_warp(&bar->k_empty[0]);
             for (int j = 0; j < nsel; ++j) {
                 const bool next = j + 1 < nsel;
                 for (int hf = 0; hf < 2; ++hf) {
                     if (active(hf, j)) issue_pv(hf, j);
                     if (next && active(hf, j + 1)) issue_s(hf, j + 1);
                 }
-                mma_commit_warp(&bar->v_empty[j & 1]);
-                if (next) mma_commit_warp(&bar->k_empty[(j + 1) & 1]);
+                if (!kDual) {
+                    mma_commit_warp(&bar->v_empty[j & 1]);
+                    if (next) mma_commit_warp(&bar->k_empty[(j + 1) & 1]);
+                }
                 TRACE(j, 15, (threadIdx.x & 31) == 0);
             }
         }
@@ -350,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
         };
         for (int j = 0; j < nsel; ++j) {
             if (!active(hf, j)) continue;
-            const int64_t key0 = static_cast<int64_t>(sel_at(j)) * kBlock;
+            const int64_t key0 = static_cast<int64_t>(sel_at_h(hf, j)) * kBlock;
             const bool need_mask = key0 + kBlock - 1 > lim;  // keys past the query / sequence end
             uint32_t sv[kBlock];
             float* s = reinterpret_cast<float*>(sv);
@@ -427,8 +476,9 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
         // live across the block loop, which is register-bound.)
         const int32_t tile_e = p.tiles[blockIdx.x];
         const int h_e = tile_e >> 20;
-        const int64_t qrow_e = static_cast<int64_t>(tile_e & 0xFFFFF) * p.bq + hf * kBlock + r;
-        const bool live = hf < halves && qrow_e < p.n;
+        const int64_t qrow_e = (kDual ? static_cast<int64_t>((tile_e >> 2) & 0x3FFFF) * (2 * kBlock)
+                                      : static_cast<int64_t>(tile_e & 0xFFFFF) * p.bq) + hf * kBlock + r;
+        const bool live = hf < halves && qrow_e < p.n && (!kDual || ((tile_e >> hf) & 1));
         const int ndst = p.n_out_peers > 0 ? p.n_out_peers : 1;
         auto dst_row = [&](int i) -> __nv_bfloat16* {
             if (p.n_out_peers == 0)
@@ -497,11 +547,18 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
 
 }  // namespace
 
-void launch_fa(const FaParams& p, int num_tiles, cudaStream_t s) {
+void launch_fa(const FaParams& p, int num_tiles, bool dual, cudaStream_t s) {
     // Per launch (not cached in a static): the attribute belongs to the current
     // device's context, and the call costs microseconds against a long kernel.
-    cudaFuncSetAttribute(fa_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemTotal));
-    fa_sparse_kernel<<<num_tiles, kThreads, kSmemTotal, s>>>(p);
+    if (dual) {
+        cudaFuncSetAttribute(fa_sparse_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kSmemTotal));
+        fa_sparse_kernel<true><<<num_tiles, kThreads, kSmemTotal, s>>>(p);
+    } else {
+        cudaFuncSetAttribute(fa_sparse_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kSmemTotal));
+        fa_sparse_kernel<false><<<num_tiles, kThreads, kSmemTotal, s>>>(p);
+    }
 }
 
 }  // namespace shplb::kern

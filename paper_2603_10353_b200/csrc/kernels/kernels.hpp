@@ -65,7 +65,9 @@ struct FaParams {
     void* out_peers[kMaxPeers];
     int32_t n_out_peers;
 };
-void launch_fa(const FaParams& p, int num_tiles, cudaStream_t s);
+// dual: block_q = 128 with two query blocks per CTA (tiles packed as pairs, see
+// fa_sm100.cu); otherwise one tile per query block.
+void launch_fa(const FaParams& p, int num_tiles, bool dual, cudaStream_t s);
 // The CTA-pair variant (fa_pair_sm100.cu): bq = 256 only; one 2-CTA cluster per tile.
 cudaError_t launch_fa_pair(const FaParams& p, int num_tiles, cudaStream_t s);
 

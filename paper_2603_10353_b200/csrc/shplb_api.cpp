@@ -381,6 +381,17 @@ int k3_variant() {
     return v;
 }
 
+// block_q = 128: two query blocks per kernel-3 CTA (each with its own selection
+// and K / V stream, fa_sm100.cu kDual). SHPLB_DUAL=0 (diagnostic) restores one
+// block per CTA.
+bool dual_mode(const shplb_layer_shape* s) {
+    static const bool on = [] {
+        const char* e = std::getenv("SHPLB_DUAL");
+        return !(e && std::string(e) == "0");
+    }();
+    return on && s->block_q == kern::kBlock;
+}
+
 int tile_order_mode() {
     static const int mode = [] {
         const char* e = std::getenv("SHPLB_TILE_ORDER");
@@ -395,7 +406,8 @@ int tile_order_mode() {
 // share K/V in L2.
 void build_tiles(shplb_ctx* ctx, const shplb_layer_shape* s, const std::vector<int32_t>& kblocks) {
     const int64_t nqb = cdiv(s->seq_len, s->block_q);
-    std::vector<int64_t> key = {s->seq_len, s->causal, s->block_q, s->num_q_heads};
+    const bool dual = dual_mode(s);
+    std::vector<int64_t> key = {s->seq_len, s->causal, s->block_q, s->num_q_heads, dual ? 1 : 0};
     key.insert(key.end(), kblocks.begin(), kblocks.end());
     if (s->q_block_range) key.insert(key.end(), s->q_block_range, s->q_block_range + 2 * s->num_q_heads);
     if (s->kv_head_of_q) key.insert(key.end(), s->kv_head_of_q, s->kv_head_of_q + s->num_q_heads);  // tile order
@@ -416,10 +428,22 @@ void build_tiles(shplb_ctx* ctx, const shplb_layer_shape* s, const std::vector<i
                                   ") out of [0, " + std::to_string(nqb) + "]");
         }
         for (int64_t qb = qb_lo; qb < qb_hi; ++qb) {
-            tiles.push_back((h << 20) | static_cast<int32_t>(qb));
-            work.push_back(static_cast<int32_t>(
+            const int32_t w = static_cast<int32_t>(
                 std::min<int64_t>(kblocks[h], visible_blocks(qb, s->seq_len, s->block_q, s->causal != 0)) *
-                live_halves(qb, s->seq_len, s->block_q)));
+                live_halves(qb, s->seq_len, s->block_q));
+            if (dual) {  // (h << 20) | (pair << 2) | live-half mask
+                const int32_t pair_tile = (h << 20) | static_cast<int32_t>((qb >> 1) << 2);
+                if (!tiles.empty() && (tiles.back() & ~3) == pair_tile) {
+                    tiles.back() |= 1 << (qb & 1);
+                    work.back() += w;
+                } else {
+                    tiles.push_back(pair_tile | (1 << (qb & 1)));
+                    work.push_back(w);
+                }
+            } else {
+                tiles.push_back((h << 20) | static_cast<int32_t>(qb));
+                work.push_back(w);
+            }
         }
     }
     std::vector<size_t> order(tiles.size());
@@ -485,7 +509,7 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
         if (pair)
             SHPLB_CUDA(kern::launch_fa_pair(p, ctx->current->num_tiles, st));
         else
-            kern::launch_fa(p, ctx->current->num_tiles, st);
+            kern::launch_fa(p, ctx->current->num_tiles, dual_mode(s), st);
     }
     check_launch(ctx);
 }
