@@ -16,9 +16,10 @@
 // softmax_weighted_sum over the kept set (proj/src/attention.cpp:35-49), causal
 // mask (:28-30), zero row when nothing is visible (:40-41), lazy rescale.
 //
-// Per CTA: warps 0-3 softmax, warp 4 TMA producer (its own halves of Q, K, V;
-// completion bytes on the leader's barriers), warp 5 TMEM allocator and (in
-// the leader) MMA issuer. Shared memory: Q 32 KB, K 4 x 16 KB, V 4 x 16 KB.
+// Per CTA: warps 0-7 softmax (two warpgroups splitting each row's 128 keys,
+// row max exchanged through shared memory), warp 8 TMA producer (its own halves
+// of Q, K, V; completion bytes on the leader's barriers), warp 9 TMEM allocator
+// and (in the leader) MMA issuer. Shared memory: Q 32 KB, K 4 x 16 KB, V 4 x 16 KB.
 // TMEM (512 columns allocated): S [0,128), P buffers [128,192) and
 // [192,256), O [256,384).
 #include <cstdint>
@@ -35,7 +36,7 @@ namespace {
 
 using namespace shplb::ptx;
 
-constexpr int kPThreads = 192;
+constexpr int kPThreads = 320;  // warps 0-7 softmax (2 groups), 8 TMA, 9 TMEM + MMA
 constexpr int kPStages = 4;
 constexpr int kQHalfBytes = 32768;  // [2 d-chunks][128 rows][128 B]
 constexpr int kKHalfBytes = 16384;  // [2 d-chunks][64 keys][128 B]
@@ -66,7 +67,8 @@ constexpr size_t kPSmemK = kPSmemQ + kQHalfBytes;
 constexpr size_t kPSmemV = kPSmemK + kPStages * kKHalfBytes;
 constexpr size_t kPSmemSel = kPSmemV + kPStages * kVHalfBytes;
 constexpr size_t kPSmemBar = kPSmemSel + kMaxSelected * sizeof(int32_t);
-constexpr size_t kPSmemTotal = kPSmemBar + sizeof(PairBarriers) + 1024;
+constexpr size_t kPSmemX = kPSmemBar + ((sizeof(PairBarriers) + 15) / 16) * 16;  // row max / sum exchange
+constexpr size_t kPSmemTotal = kPSmemX + 3 * 256 * sizeof(float) + 1024;
 
 #ifdef SHPLB_PTRACE  // dev-only: per-block clock64 timeline of cluster SHPLB_PTRACE, printed at exit
 constexpr int kPTraceBlocks = 24;
@@ -110,15 +112,15 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
             mbar_init(&bar->v_empty[i], 1);
         }
         mbar_init(&bar->s_full, 1);
-        mbar_init(&bar->s_free, 8);
+        mbar_init(&bar->s_free, 16);
         for (int i = 0; i < 2; ++i) {
-            mbar_init(&bar->p_full[i][0], 4);
-            mbar_init(&bar->p_full[i][1], 4);
+            mbar_init(&bar->p_full[i][0], 8);
+            mbar_init(&bar->p_full[i][1], 8);
             mbar_init(&bar->pv_done[i], 1);
         }
         fence_mbar_init();
     }
-    if (warp == 5) tmem_alloc_pair<kPairTmemCols>(&bar->tmem_base);
+    if (warp == 9) tmem_alloc_pair<kPairTmemCols>(&bar->tmem_base);
     tc_fence_before();
     __syncthreads();
     cluster_sync_all();  // both CTAs' barriers exist before any remote arrive / TMA
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
     const uint32_t tmem = bar->tmem_base;
     auto leader = [&](const uint64_t* b) { return mapa_shared(smem_u32(b), 0); };
 
-    if (warp == 4) {
+    if (warp == 8) {
         // ------------------------------------------------------ TMA producer
         if (nsel > 0) {
             if (rank == 0) mbar_expect_tx_warp(&bar->q_full, 2 * kQHalfBytes);
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
                                    64 * static_cast<int>(rank), key0, g, 1, 0);
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         // ------------------------------------------- MMA issuer (leader only)
         if (rank == 0 && nsel > 0) {
             const uint32_t tm = __shfl_sync(0xffffffffu, static_cast<uint32_t>(lds_s32(smem_u32(&bar->tmem_base))), 0);
@@ -186,25 +188,32 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
             }
         }
     } else {
-        // --------------------------------------------------- softmax (warps 0-3)
-        const int r = threadIdx.x;  // row within this CTA's half == TMEM lane
+        // ------------------------------------------- softmax (warps 0-7)
+        // Two warpgroups per CTA share each row (thread = query row = TMEM
+        // lane): warpgroup ch takes keys [64 ch, 64 ch + 64) of S, the
+        // matching 32 packed columns of P and d-columns [64 ch, 64 ch + 64)
+        // of O; the row max is exchanged through shared memory once per block.
+        const int ch = warp >> 2;
+        const int r = threadIdx.x & 127;
         const int64_t qrow = row0 + 128 * static_cast<int64_t>(rank) + r;
-        const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-        const uint32_t s_addr = tmem + lane_base + kColS;
-        const uint32_t o_addr = tmem + lane_base + kColO;
+        const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const uint32_t c0 = 64u * static_cast<uint32_t>(ch);
+        const uint32_t s_addr = tmem + lane_base + kColS + c0;
+        const uint32_t o_addr = tmem + lane_base + kColO + c0;
         const float sl2 = p.scale_log2;
         const int64_t lim = p.causal ? min(qrow, p.n - 1) : p.n - 1;
         const uint32_t s_free_l = leader(&bar->s_free);
         const uint32_t p_full_l = leader(&bar->p_full[rank][0]);  // [rank][1] is 8 bytes further
         const float2 sc2 = make_float2(sl2, sl2);
-        float m = -INFINITY, l = 0.0f;
+        float* xmax = reinterpret_cast<float*>(smem + kPSmemX);  // [2 parities][2 groups][128 rows]
+        float m = -INFINITY, l = 0.0f;  // l: this group's part of the row sum
         for (int j = 0; j < nsel; ++j) {
-            const int64_t key0 = static_cast<int64_t>(sel_at(j)) * kBlock;
-            const bool need_mask = key0 + kBlock - 1 > lim;
-            uint32_t sv[kBlock];
+            const int64_t key0 = static_cast<int64_t>(sel_at(j)) * kBlock + c0;
+            const bool need_mask = key0 + 63 > lim;
+            uint32_t sv[64];
             float* s = reinterpret_cast<float*>(sv);
             mbar_wait(&bar->s_full, j & 1);
-            PTRACE(j, 4 + 3 * rank, r == 0);
+            PTRACE(j, 4 + 3 * rank, r == 0 && ch == 0);
             tc_fence_after();
 #ifdef SHPLB_PDIAG_SKIP_SOFTMAX  // dev-only diagnostic (wrong results): the MMA/TMA pipeline alone
             tc_fence_before();
@@ -214,24 +223,27 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
 #endif
             tmem_ld32(s_addr + 0, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
             tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
-            tmem_ld32(s_addr + 64, *reinterpret_cast<uint32_t(*)[32]>(&sv[64]));
-            tmem_ld32(s_addr + 96, *reinterpret_cast<uint32_t(*)[32]>(&sv[96]));
             tmem_wait_ld();
             tc_fence_before();
             mbar_arrive_cluster_warp(s_free_l);  // the leader may now compute S(j+1) over it
-            PTRACE(j, 5 + 3 * rank, r == 0);
+            PTRACE(j, 5 + 3 * rank, r == 0 && ch == 0);
             if (need_mask) {
 #pragma unroll
-                for (int c = 0; c < kBlock; ++c)
+                for (int c = 0; c < 64; ++c)
                     if (key0 + c > lim) s[c] = -INFINITY;
             }
             float mx8[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) mx8[e] = -INFINITY;
 #pragma unroll
-            for (int c = 0; c < kBlock; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
-            const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                                     fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+            for (int c = 0; c < 64; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
+            float mine = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+            float* xm = xmax + (j & 1) * 256;  // parity-buffered: the other group may still read j-1's
+            xm[ch * 128 + r] = mine;
+            named_bar_sync(1, 256);
+            const float mraw = fmaxf(mine, xm[(ch ^ 1) * 128 + r]);
+            PTRACE(j, 10, r == 0 && ch == 0 && rank == 0);
             const float mx = mraw * sl2;
             float alpha = 1.0f;
             if (mx > m + kPairRescaleThreshold || (m == -INFINITY && mx > -INFINITY)) {
@@ -239,11 +251,11 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
                 m = mx;
             }
             if (j >= 1 && __any_sync(0xffffffffu, alpha != 1.0f)) {
-                // O *= alpha once P(j-1).V(j-1) has landed in O.
+                // this group's half of O *= alpha once P(j-1).V(j-1) has landed
                 mbar_wait(&bar->pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
                 tc_fence_after();
 #pragma unroll
-                for (int c = 0; c < kHeadDim / 32; ++c) {
+                for (int c = 0; c < 2; ++c) {
                     uint32_t v[32];
                     tmem_ld32(o_addr + c * 32, v);
                     tmem_wait_ld();
@@ -258,10 +270,10 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
             }
             const float msub = (m == -INFINITY) ? 0.0f : m;
             const float2 nm2 = make_float2(-msub, -msub);
-            const uint32_t p_addr = tmem + lane_base + kColP + 64u * static_cast<uint32_t>(j & 1);
+            const uint32_t p_addr = tmem + lane_base + kColP + 64u * static_cast<uint32_t>(j & 1) + c0 / 2;
             float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 2; ++c) {
                 uint32_t pk[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
@@ -276,27 +288,33 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
             }
             const float2 sum = fadd2(sum2[0], sum2[1]);
             l = l * alpha + (sum.x + sum.y);
+            PTRACE(j, 11, r == 0 && ch == 0 && rank == 0);
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive_cluster_warp(p_full_l + 8u * static_cast<uint32_t>(j & 1));
-            PTRACE(j, 6 + 3 * rank, r == 0);
+            PTRACE(j, 6 + 3 * rank, r == 0 && ch == 0);
         }
 
         // -------------------------------------------------------- epilogue
+        // Row sum = group 0's part + group 1's part (the same order in both).
+        float* lsum = xmax + 512;
+        lsum[ch * 128 + r] = l;
+        named_bar_sync(2, 256);
+        const float ltot = lsum[r] + lsum[128 + r];
         const bool live = qrow < p.n;
         const int ndst = p.n_out_peers > 0 ? p.n_out_peers : 1;
         auto dst_row = [&](int i) -> __nv_bfloat16* {
             if (p.n_out_peers == 0)
-                return static_cast<__nv_bfloat16*>(p.out) + (static_cast<int64_t>(h) * p.n + qrow) * kHeadDim;
+                return static_cast<__nv_bfloat16*>(p.out) + (static_cast<int64_t>(h) * p.n + qrow) * kHeadDim + c0;
             return static_cast<__nv_bfloat16*>(p.out_peers[i]) +
-                   (static_cast<int64_t>(p.heads.k[h]) * p.n + qrow) * kHeadDim;
+                   (static_cast<int64_t>(p.heads.k[h]) * p.n + qrow) * kHeadDim + c0;
         };
         if (nsel > 0) {
             mbar_wait(&bar->pv_done[(nsel - 1) & 1], ((nsel - 1) >> 1) & 1);
             tc_fence_after();
-            const float inv = l > 0.0f ? 1.0f / l : 0.0f;
+            const float inv = ltot > 0.0f ? 1.0f / ltot : 0.0f;
 #pragma unroll 1
-            for (int c = 0; c < kHeadDim / 32; ++c) {
+            for (int c = 0; c < 2; ++c) {
                 uint32_t v[32];
                 tmem_ld32(o_addr + c * 32, v);
                 tmem_wait_ld();
@@ -322,7 +340,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
             for (int i = 0; i < ndst; ++i) {
                 __nv_bfloat16* out = dst_row(i);
 #pragma unroll
-                for (int u = 0; u < kHeadDim / 8; ++u) *reinterpret_cast<uint4*>(out + u * 8) = make_uint4(0, 0, 0, 0);
+                for (int u = 0; u < 8; ++u) *reinterpret_cast<uint4*>(out + u * 8) = make_uint4(0, 0, 0, 0);
             }
         }
         if (p.n_out_peers > 1) __threadfence_system();
@@ -333,16 +351,16 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
     if ((blockIdx.x >> 1) == SHPLB_PTRACE && threadIdx.x == 0) {
         const long long t0 = ptrace[0][rank == 0 ? 4 : 7];
         for (int j = 0; j < kPTraceBlocks && j < nsel; ++j)
-            printf("PTRACE r%u j %d mma %lld %lld %lld %lld sm0 %lld %lld %lld sm1 %lld %lld %lld\n", rank, j,
-                   ptrace[j][0] - t0, ptrace[j][1] - t0, ptrace[j][2] - t0, ptrace[j][3] - t0,
+            printf("PTRACE r%u j %d mma %lld %lld %lld %lld sm0 %lld %lld %lld sm1 %lld %lld %lld x %lld %lld\n", rank,
+                   j, ptrace[j][0] - t0, ptrace[j][1] - t0, ptrace[j][2] - t0, ptrace[j][3] - t0,
                    ptrace[j][4] - t0, ptrace[j][5] - t0, ptrace[j][6] - t0, ptrace[j][7] - t0,
-                   ptrace[j][8] - t0, ptrace[j][9] - t0);
+                   ptrace[j][8] - t0, ptrace[j][9] - t0, ptrace[j][10] - t0, ptrace[j][11] - t0);
     }
 #endif
     tc_fence_before();
     __syncthreads();
     cluster_sync_all();  // the peer is done with this CTA's barriers and operands
-    if (warp == 5) {
+    if (warp == 9) {
         tc_fence_after();
         tmem_dealloc_pair<kPairTmemCols>(tmem);
     }

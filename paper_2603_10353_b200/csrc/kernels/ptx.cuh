@@ -389,22 +389,25 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
     return r;
 }
 
-// Warp-uniform remote arrive (one elected lane) with release at cluster scope.
+// Warp-uniform remote arrive (one elected lane) on a barrier of the cluster. The
+// default (CTA-scope) semantics, as CUTLASS's ClusterBarrier: the handoffs order
+// tcgen05 work (fenced with tcgen05.fence), not generic memory, and a
+// cluster-scope release / acquire costs an L1 invalidate per poll.
 __device__ __forceinline__ void mbar_arrive_cluster_warp(uint32_t cluster_addr) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
-        "@e mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n\t}" ::"r"(cluster_addr)
+        "@e mbarrier.arrive.shared::cluster.b64 _, [%0];\n\t}" ::"r"(cluster_addr)
         : "memory");
 }
 
-// Wait with acquire at cluster scope (arrivals came from the peer CTA).
+// Wait on a barrier whose arrivals may come from the peer CTA.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
     uint32_t ok = 0;
     while (!ok) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(ok)
             : "r"(smem_u32(bar)), "r"(parity)
