@@ -1,8 +1,16 @@
-import sys, os, numpy as np, torch
-sys.path.insert(0, '/root/repo')
-import paper_2603_10353_b200 as P
-from paper_2603_10353_b200.workload import LayerSpec, make_layer
-from paper_2603_10353_b200 import experiments as X
+"""Kernel 2's score and select parts timed separately on the C3 128K layer (dev
+tool, GPU box): block_scores (pool + score, writing the score matrix),
+select_blocks on it, and the fused layer's stage times."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2603_10353_b200 as P  # noqa: E402
+from paper_2603_10353_b200.workload import LayerSpec, make_layer  # noqa: E402
+from paper_2603_10353_b200 import experiments as X  # noqa: E402
 n=131072
 q,k,v = make_layer(LayerSpec(seq_len=n, seed=2603), "cuda")
 ctx=P.Context(0)
