@@ -166,7 +166,14 @@ inline BudgetAllocation maxmin_allocate(const std::vector<RecoveryCurve>& curves
 // (PerQueryTopK or ColumnAggregateTopK) on the workload's query rows (all n_k
 // keys, no causal mask as the reference's profile command), through the GPU
 // profiler when a context is given, else the host C++ one. Heads with equal K
-// share a kv head. Curves agree with the reference to rounding (1e-12).
+// share a kv head. Q and K are ROUNDED TO BF16 first (the device layout); the
+// dot products, sort and masses are then fp64. So the curves equal the
+// reference's build_profiles to rounding (1e-12) when the workload is
+// bf16-exact (as the kernels' inputs always are, and as adapter_test.cpp
+// checks); on arbitrary fp64 workloads they are the curves of the
+// bf16-rounded heads. maxmin_allocate returns budgets, hit_iteration_cap and
+// off_grid_evaluations; the reference's per-step `transfers` and
+// `min_recovery_trace` diagnostics are not reproduced (left empty).
 inline std::vector<RecoveryCurve> build_profiles(const AttentionWorkload& w, const std::vector<long>& grid,
                                                  Context* ctx = nullptr,
                                                  SelectionKind kind = SelectionKind::PerQueryTopK) {
@@ -243,6 +250,14 @@ inline Assignment naive_assign(const std::vector<long>& budgets, int devices,
 }
 
 inline LoadReport imbalance(const std::vector<long>& budgets, const Assignment& assignment) {
+    // The reference's checks and messages before anything is sized or read
+    // (Assignment::validate, partitioner.cpp:38-48; imbalance, :236-242).
+    if (assignment.num_devices < 1) throw std::invalid_argument("need at least one device");
+    if (assignment.device_of_head.empty()) throw std::invalid_argument("assignment covers no heads");
+    if (assignment.device_of_head.size() != budgets.size()) {
+        throw std::invalid_argument("assignment covers " + std::to_string(assignment.device_of_head.size()) +
+                                    " heads but " + std::to_string(budgets.size()) + " budgets were given");
+    }
     const std::vector<int64_t> b(budgets.begin(), budgets.end());
     const std::vector<int32_t> dev(assignment.device_of_head.begin(), assignment.device_of_head.end());
     std::vector<int64_t> loads(static_cast<size_t>(assignment.num_devices));

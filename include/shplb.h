@@ -343,8 +343,11 @@ int shplb_sparse_attention_layer_host_async(shplb_ctx* ctx, const shplb_layer_sh
                                             uint16_t* out_host, void* stream);
 
 /* Device pointers of the selection made by the last shplb_sparse_attention_layer
- * call on this context (valid until the next call): idx [Hq][nqb][kmax],
- * cnt [Hq][nqb]. */
+ * or shplb_sparse_attention_layer_host[_async] call on this context (valid until
+ * the next call; after an async host call, once its stream completed):
+ * idx [Hq][nqb][kmax], cnt [Hq][nqb], kmax = the layer's largest k_h in blocks.
+ * The host-buffer entries run the layer in KV-head chunks; each chunk writes its
+ * heads' rows of this one whole-layer selection. */
 int shplb_last_selection(const shplb_ctx* ctx, const int32_t** idx, const int32_t** cnt,
                          int64_t* kmax);
 

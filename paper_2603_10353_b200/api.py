@@ -473,6 +473,9 @@ class Context:
         if out is None:
             out = torch.empty_like(q)
         b = _i64(budgets_tokens)
+        if b.size != hq:
+            from ._native import InvalidArgument
+            raise InvalidArgument(f"need one budget per query head ({hq}), got {b.size}")
         sh = _shape(hq, k.shape[0], n, causal, False, kv_map, d, block_q, q_block_range, kind=kind)
         self._last_block_q = block_q
         fn = (lib().shplb_sparse_attention_layer_host_async if asynchronous

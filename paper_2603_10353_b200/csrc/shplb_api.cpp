@@ -678,35 +678,55 @@ int shplb_block_sparse_attention(shplb_ctx* ctx, const shplb_layer_shape* shape,
     });
 }
 
+namespace {
+// One layer call over `shape`'s heads. The selection goes to the context's
+// idx/cnt at head offset `head_off` with row stride `kmax_stride` (0 = this
+// call's own largest k), so the host-buffer entry's KV-head chunks together
+// leave the whole layer's selection behind for shplb_last_selection.
+void sparse_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q, const void* k,
+                  const void* v, const int64_t* budgets_tokens, void* out, cudaStream_t st,
+                  int64_t head_off, int64_t kmax_stride) {
+    require(ctx != nullptr, "ctx is null");
+    check_shape(shape);
+    check_ptr(q, "q");
+    check_ptr(k, "k");
+    check_ptr(v, "v");
+    if (!fused_gather(shape)) check_ptr(out, "out");
+    std::vector<int32_t> kbl;
+    const kern::HeadTable kb = budgets_to_blocks(shape, budgets_tokens, kbl);
+    const int64_t kmax = std::max<int64_t>(kmax_stride, *std::max_element(kbl.begin(), kbl.end()));
+    DeviceGuard g(ctx->device);
+    if (shape->validate) validate_inputs(ctx, shape, q, k, v, st);
+    const int64_t nqb = cdiv(shape->seq_len, shape->block_q);
+    const int64_t rows_total = (head_off + shape->num_q_heads) * nqb;
+    if (head_off == 0) {
+        grow(ctx->idx, ctx->idx_bytes, sizeof(int32_t) * rows_total * kmax);
+        grow(ctx->cnt, ctx->cnt_bytes, sizeof(int32_t) * rows_total);
+    } else {
+        require(ctx->idx_bytes >= sizeof(int32_t) * rows_total * kmax &&
+                    ctx->cnt_bytes >= sizeof(int32_t) * rows_total,
+                "selection buffer not sized for the chunked layer");
+    }
+    int32_t* idx = ctx->idx + head_off * nqb * kmax;
+    int32_t* cnt = ctx->cnt + head_off * nqb;
+    build_tiles(ctx, shape, kbl);
+    pool_and_score(ctx, shape, q, k, kb, kmax, nullptr, true, idx, cnt, st);
+    run_fa(ctx, shape, q, k, v, idx, cnt, kmax, out, st);
+    mark(ctx, 3, st);
+    ctx->last_kmax = kmax;
+    ctx->last_rows = rows_total;
+    ctx->last_n = shape->seq_len;
+    ctx->last_nqb = nqb;
+    ctx->last_bq = shape->block_q;
+    ctx->last_causal = shape->causal;
+}
+}  // namespace
+
 int shplb_sparse_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
                                  const void* k, const void* v, const int64_t* budgets_tokens,
                                  void* out, void* stream) {
     return guarded([&] {
-        require(ctx != nullptr, "ctx is null");
-        check_shape(shape);
-        check_ptr(q, "q");
-        check_ptr(k, "k");
-        check_ptr(v, "v");
-        if (!fused_gather(shape)) check_ptr(out, "out");
-        std::vector<int32_t> kbl;
-        const kern::HeadTable kb = budgets_to_blocks(shape, budgets_tokens, kbl);
-        const int64_t kmax = *std::max_element(kbl.begin(), kbl.end());
-        DeviceGuard g(ctx->device);
-        auto st = static_cast<cudaStream_t>(stream);
-        if (shape->validate) validate_inputs(ctx, shape, q, k, v, st);
-        const int64_t nqb = cdiv(shape->seq_len, shape->block_q);
-        grow(ctx->idx, ctx->idx_bytes, sizeof(int32_t) * shape->num_q_heads * nqb * kmax);
-        grow(ctx->cnt, ctx->cnt_bytes, sizeof(int32_t) * shape->num_q_heads * nqb);
-        build_tiles(ctx, shape, kbl);
-        pool_and_score(ctx, shape, q, k, kb, kmax, nullptr, true, ctx->idx, ctx->cnt, st);
-        run_fa(ctx, shape, q, k, v, ctx->idx, ctx->cnt, kmax, out, st);
-        mark(ctx, 3, st);
-        ctx->last_kmax = kmax;
-        ctx->last_rows = shape->num_q_heads * nqb;
-        ctx->last_n = shape->seq_len;
-        ctx->last_nqb = nqb;
-        ctx->last_bq = shape->block_q;
-        ctx->last_causal = shape->causal;
+        sparse_layer(ctx, shape, q, k, v, budgets_tokens, out, static_cast<cudaStream_t>(stream), 0, 0);
     });
 }
 
@@ -757,8 +777,7 @@ namespace {
 int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q_host,
                const uint16_t* k_host, const uint16_t* v_host, const int64_t* budgets_tokens,
                uint16_t* out_host, void* stream, bool async_call) {
-    int rc = SHPLB_OK;
-    const int err = guarded([&] {
+    return guarded([&] {
         require(ctx != nullptr, "ctx is null");
         check_shape(shape);
         require(q_host && k_host && v_host && out_host, "null host buffer");
@@ -769,19 +788,23 @@ int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q
         const size_t q_off = 0, k_off = (qb + al - 1) / al * al, v_off = k_off + (kb + al - 1) / al * al,
                      o_off = v_off + (kb + al - 1) / al * al, total = o_off + qb;
         DeviceGuard g(ctx->device);
+        // The staging buffer is two slots of a FIXED stride (host_io_bytes / 2),
+        // whatever this call's shape: a call whose layer is smaller than the
+        // previous one's must not place its slot 1 over the previous call's
+        // slot 0 while that call's kernels and copy-back are still in flight.
         const size_t slot_bytes = (total + al - 1) / al * al;
-        const size_t need = async_call ? 2 * slot_bytes : slot_bytes;
-        if (need > ctx->host_io_bytes) {
+        if (2 * slot_bytes > ctx->host_io_bytes) {
             if (ctx->host_io) {
                 SHPLB_CUDA(cudaDeviceSynchronize());  // in-flight async calls may still use it
                 SHPLB_CUDA(cudaFree(ctx->host_io));
             }
             ctx->host_io = nullptr;
-            SHPLB_CUDA(cudaMalloc(&ctx->host_io, need));
-            ctx->host_io_bytes = need;
+            SHPLB_CUDA(cudaMalloc(&ctx->host_io, 2 * slot_bytes));
+            ctx->host_io_bytes = 2 * slot_bytes;
         }
+        const size_t slot_stride = ctx->host_io_bytes / 2;
         const int slot = async_call ? (ctx->host_slot ^= 1) : 0;
-        auto* base = static_cast<uint8_t*>(ctx->host_io) + slot * slot_bytes;
+        auto* base = static_cast<uint8_t*>(ctx->host_io) + slot * slot_stride;
         auto st = static_cast<cudaStream_t>(stream);
         // Pipeline by KV-head chunks (standard GQA grouping only): chunk c's
         // H2D copies on a copy stream overlap chunk c-1's kernels on the
@@ -792,6 +815,17 @@ int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q
         // that q range is contiguous when the kv map is non-decreasing (the
         // standard grouping, and every head-parallel shard built by rank_shard).
         const int32_t hkv = shape->num_kv_heads, hq = shape->num_q_heads;
+        // Budgets are checked for the whole layer up front (messages name the
+        // layer's head index); every chunk strides its selection by the layer's
+        // largest k so the chunks leave one whole-layer selection behind.
+        std::vector<int32_t> kbl_layer;
+        budgets_to_blocks(shape, budgets_tokens, kbl_layer);
+        const int64_t kmax_layer = *std::max_element(kbl_layer.begin(), kbl_layer.end());
+        {
+            const int64_t rows = int64_t(hq) * cdiv(shape->seq_len, shape->block_q);
+            grow(ctx->idx, ctx->idx_bytes, sizeof(int32_t) * rows * kmax_layer);
+            grow(ctx->cnt, ctx->cnt_bytes, sizeof(int32_t) * rows);
+        }
         kern::HeadTable map{};
         fill_kv_map(shape, map);
         bool monotone = true;
@@ -833,6 +867,14 @@ int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q
             SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_in, start, 0));
             SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_out, start, 0));
             if (async_call) SHPLB_CUDA(cudaStreamWaitEvent(ks, start, 0));
+            // Earlier async calls may have completed `stream` on another stream
+            // than this call's: order after both slots' last users as well
+            // (waiting on a never-recorded event is a no-op).
+            for (cudaEvent_t e : ctx->slot_done) {
+                SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_in, e, 0));
+                SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_out, e, 0));
+                if (async_call) SHPLB_CUDA(cudaStreamWaitEvent(ks, e, 0));
+            }
         }
         const size_t row_bytes = sizeof(uint16_t) * shape->seq_len * shape->head_dim;  // one head
         for (int32_t c = 0; c < chunks; ++c) {
@@ -855,14 +897,15 @@ int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q
             cs.num_kv_heads = g1 - g0;
             cs.kv_head_of_q = sub.data();
             if (shape->q_block_range) cs.q_block_range = shape->q_block_range + 2 * h0;
-            rc = shplb_sparse_attention_layer(ctx, &cs, base + q_off + h0 * row_bytes,
-                                              base + k_off + g0 * row_bytes, base + v_off + g0 * row_bytes,
-                                              budgets_tokens + h0, base + o_off + h0 * row_bytes, ks);
-            if (rc != SHPLB_OK) {  // message already recorded; drain before returning
+            try {
+                sparse_layer(ctx, &cs, base + q_off + h0 * row_bytes, base + k_off + g0 * row_bytes,
+                             base + v_off + g0 * row_bytes, budgets_tokens + h0, base + o_off + h0 * row_bytes,
+                             ks, h0, kmax_layer);
+            } catch (...) {  // drain before reporting
                 cudaStreamSynchronize(ctx->copy_in);
                 cudaStreamSynchronize(ks);
                 ctx->launches_after_async = -1;
-                return;
+                throw;
             }
             SHPLB_CUDA(cudaEventRecord(comp_done, ks));
             SHPLB_CUDA(cudaStreamWaitEvent(ctx->copy_out, comp_done, 0));
@@ -880,7 +923,6 @@ int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q
             ctx->launches_after_async = -1;
         }
     });
-    return rc != SHPLB_OK ? rc : err;
 }
 }  // namespace
 

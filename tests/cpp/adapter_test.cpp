@@ -86,6 +86,21 @@ static int run_cpu() {
     try { naive_assign({1, 2}, 3); } catch (const std::invalid_argument& e) { ref_msg = e.what(); }
     try { b200::naive_assign({1, 2}, 3); } catch (const std::invalid_argument& e) { got_msg = e.what(); }
     EXPECT(!ref_msg.empty() && ref_msg == got_msg, "devices > heads: invalid_argument with the reference text");
+    // imbalance: short assignment, no devices, empty assignment.
+    {
+        Assignment short_a, no_dev, empty_a;
+        short_a.num_devices = 2;
+        short_a.device_of_head = {0, 1};
+        no_dev.num_devices = -1;
+        no_dev.device_of_head = {0, 0, 0};
+        empty_a.num_devices = 2;
+        for (const Assignment* a : {&short_a, &no_dev, &empty_a}) {
+            ref_msg.clear(), got_msg.clear();
+            try { imbalance({5, 6, 7}, *a); } catch (const std::invalid_argument& e) { ref_msg = e.what(); }
+            try { b200::imbalance({5, 6, 7}, *a); } catch (const std::invalid_argument& e) { got_msg = e.what(); }
+            EXPECT(!ref_msg.empty() && ref_msg == got_msg, "imbalance: invalid_argument with the reference text");
+        }
+    }
     // build_profiles (host path) vs the reference's on a bf16-exact workload.
     {
         std::mt19937_64 r2(11);

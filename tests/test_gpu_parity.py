@@ -299,6 +299,56 @@ def test_async_host_entry_matches_sync_over_layers(cuda_ctx):
         assert torch.equal(a, s_)
 
 
+def test_async_host_entry_shape_shrinks_and_grows(cuda_ctx):
+    """Chained async host calls whose layer shrinks, then grows within the staging
+    buffer, then shrinks again: every call's two-slot staging must stay disjoint
+    from the in-flight previous call's (a per-call slot stride let slot 1
+    of a smaller layer overlap slot 0 of a larger one). Outputs == sync calls."""
+    sizes = [(8, 4, 2304), (4, 2, 1024), (4, 2, 640), (8, 4, 1536), (2, 1, 896), (8, 4, 2304), (4, 2, 384)]
+    layers, want = [], []
+    for li, (hq, hk, n) in enumerate(sizes):
+        q, k, v = make_layer(LayerSpec(num_q_heads=hq, num_kv_heads=hk, seq_len=n, seed=500 + li), "cpu")
+        b = np.array([min(n, 128 * (1 + (3 * h + li) % 7)) for h in range(hq)], np.int64)
+        q, k, v = (t.contiguous().pin_memory() for t in (q, k, v))
+        layers.append((q, k, v, b))
+    for q, k, v, b in layers:
+        want.append(cuda_ctx.sparse_attention_layer_host(q, k, v, b).clone())
+    stream = torch.cuda.Stream()
+    for rep in range(2):
+        outs = []
+        for q, k, v, b in layers:
+            o = torch.full(q.shape, float("nan"), dtype=q.dtype).pin_memory()
+            outs.append(cuda_ctx.sparse_attention_layer_host(q, k, v, b, stream=stream, out=o, asynchronous=True))
+        stream.synchronize()
+        for i, (o, w) in enumerate(zip(outs, want)):
+            assert torch.equal(o, w), f"rep {rep} layer {i} {sizes[i]}"
+
+
+def test_host_entry_leaves_whole_layer_selection(cuda_ctx):
+    """After a host-buffer call (run in KV-head chunks) last_selection describes
+    the whole layer, equal to the device call's selection, and last_selection_work
+    counts every chunk's tiles."""
+    q, k, v = make_layer(LayerSpec(num_q_heads=8, num_kv_heads=4, seq_len=2048, seed=77), "cpu")
+    b = np.array([128, 2048, 384, 640, 1024, 256, 128, 1536], np.int64)
+    cuda_ctx.sparse_attention_layer(q.cuda(), k.cuda(), v.cuda(), b)
+    torch.cuda.synchronize()
+    idx_d, cnt_d = (t.clone() for t in cuda_ctx.last_selection(8, 2048))
+    work_d = cuda_ctx.last_selection_work()
+    cuda_ctx.sparse_attention_layer_host(q.contiguous(), k.contiguous(), v.contiguous(), b)
+    idx_h, cnt_h = cuda_ctx.last_selection(8, 2048)
+    assert torch.equal(cnt_h, cnt_d)
+    assert torch.equal(idx_h, idx_d)
+    assert cuda_ctx.last_selection_work() == work_d
+
+
+def test_host_entry_budget_count_checked(cuda_ctx):
+    q, k, v = make_layer(LayerSpec(num_q_heads=4, num_kv_heads=2, seq_len=512, seed=3), "cpu")
+    with pytest.raises(P.InvalidArgument, match="need one budget per query head"):
+        cuda_ctx.sparse_attention_layer_host(q, k, v, np.array([128, 128], np.int64))
+    with pytest.raises(P.InvalidArgument, match="head 3: budget k = 0 out of range"):
+        cuda_ctx.sparse_attention_layer_host(q, k, v, np.array([128, 128, 128, 0], np.int64))
+
+
 def test_async_host_entry_interleaved_with_device_calls(cuda_ctx):
     """Async host calls run their kernels on the context's own stream; device
     calls on the caller's stream in between (sharing the context workspace)
