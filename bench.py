@@ -59,7 +59,12 @@ def parse_args():
     p.add_argument("--q-heads", type=int, default=32)
     p.add_argument("--kv-heads", type=int, default=8)
     p.add_argument("--budget-fraction", type=float, default=0.25)
-    p.add_argument("--calib-rows", type=int, default=16)
+    p.add_argument("--calib-rows", type=int, default=128,
+                   help="calibration rows per head, evenly spaced through the sequence (SURVEY d2)")
+    p.add_argument("--profile-kind", choices=["token", "block"], default="token",
+                   help="recovery curves of the budget table: 'token' = the reference's build_profiles "
+                        "(PerQueryTopK, per-token top-k mass), 'block' = the kernels' own block selection "
+                        "(shplb_profile_curves_block, causal rows)")
     p.add_argument("--seed", type=int, default=2603)
     p.add_argument("--layers", type=int, default=32,
                    help="distinct attention layers per step (C3: the 32-layer stack); each has its "
@@ -78,6 +83,9 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0,
                    help="target CPU time of the bounded reference sample")
+    p.add_argument("--c1-repeats", type=int, default=1,
+                   help="--impl reference: time the whole C1 layer (8K) this many times, best reported "
+                        "(0 = skip)")
     p.add_argument("--gather", choices=["nccl", "p2p"], default="p2p",
                    help="N>1 output reassembly: NCCL all-gather + reorder on a comm stream, or the "
                         "fused gather (kernel 3 stores rows into every rank's buffer over NVLink)")
@@ -231,10 +239,10 @@ def allgather_float(x: float, world):
 # budgets
 # ---------------------------------------------------------------------------
 
-def make_budgets(q, k, args, world, rank):
+def make_budgets(q, k, args, world, rank, pctx=None):
     """Max-min budget table from calibration rows (rank 0), broadcast to all ranks."""
     import paper_2603_10353_b200 as P
-    from paper_2603_10353_b200.workload import bf16_bits
+    from paper_2603_10353_b200 import calibrate
     n, hq = args.seq_len, args.q_heads
     total = int(round(args.budget_fraction * hq * n))
     info = {}
@@ -242,23 +250,12 @@ def make_budgets(q, k, args, world, rank):
         la = P.formats.load_allocation(args.allocation_json)
         if la.budgets.size != hq:
             raise SystemExit(f"{args.allocation_json}: {la.budgets.size} budgets for {hq} heads")
-        return la.budgets.astype(np.int64), la.total, {"source": args.allocation_json}
+        return la.budgets.astype(np.int64), la.total, {"source": args.allocation_json,
+                                                       "digest": calibrate.table_digest(la.budgets)}
     if rank == 0:
-        t0 = time.time()
-        rows = q[:, n - args.calib_rows:, :]
-        grid = P.default_budget_grid(n, 128)
-        if getattr(q, "is_cuda", False):  # GPU profiler (shplb_profile_curves)
-            pctx = P.Context(q.device.index or 0)
-            curves = pctx.profile_curves(rows.contiguous(), k, grid, kind=args.policy)
-            pctx.close()
-        else:
-            curves = P.profile_curves(bf16_bits(rows), bf16_bits(k), grid, kind=args.policy)
-        alloc = P.maxmin_allocate(curves, total, quantum=128, floor=128)
-        budgets = alloc.budgets.astype(np.int64)
-        info = {"calibration_rows": args.calib_rows, "profile_s": round(time.time() - t0, 3),
-                "profiler": "gpu" if getattr(q, "is_cuda", False) else "host",
-                "transfers": alloc.transfers, "min_recovery_uniform": alloc.min_recovery_start,
-                "min_recovery_maxmin": alloc.min_recovery_end}
+        kind = "colagg" if args.policy == "column_aggregate_topk" else args.profile_kind
+        budgets, info, _ = calibrate.layer_budgets(q, k, args.budget_fraction, kind=kind, rows=args.calib_rows,
+                                                   quantum=128, floor=128, ctx=pctx)
     else:
         budgets = np.zeros(hq, np.int64)
     if world > 1:
@@ -576,7 +573,121 @@ def cpu_reference_serial_head(q, k, v, budgets, group, rows=8):
     return (_t.time() - t0) / rows * n * 1e3
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _ref_f64(bits):
+    return (bits.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
+def committed_reference_table(hq, hkv, n, seed, calib_rows, fraction):
+    """(budgets, path) of a reference-written allocation.json for this layer
+    under oracle/tables (tools/ref_budget_table.py), or None."""
+    from oracle import oracle as O
+    from paper_2603_10353_b200 import calibrate
+    pos = calibrate.calibration_rows(n, calib_rows)
+    name = f"hq{hq}_kv{hkv}_n{n}_seed{seed}_rows{pos.size}_q128.f{fraction}.allocation.json"
+    path = os.path.join(ROOT, "oracle", "tables", name)
+    if not os.path.exists(path) or not O.ref_available():
+        return None
+    b, _, tot, _ = O.ref.load_allocation(path)
+    if tot != int(round(fraction * hq * n)) or b.size != hq:
+        return None
+    return b.astype(np.int64), f"oracle/tables/{name}"
+
+
+def reference_table(q, k, v, args, seed, fraction=None):
+    """The layer's max-min budget table as the REFERENCE builds it:
+    headbal::build_profiles (PerQueryTopK, the calibration rows, grid stride
+    128) -> headbal::maxmin_allocate (quantum 128, floor 128). Read from the
+    reference-written files under oracle/tables/ (tools/ref_budget_table.py;
+    headbal::save_allocation / save_profiles) when present — the reference's
+    profile of a 128K layer takes minutes — else computed here by the reference.
+    Returns (budgets, source)."""
+    from oracle import oracle as O
+    from paper_2603_10353_b200 import calibrate
+    from paper_2603_10353_b200.workload import bf16_bits
+    hq, n, _ = q.shape
+    f = args.budget_fraction if fraction is None else fraction
+    total = int(round(f * hq * n))
+    pos = calibrate.calibration_rows(n, args.calib_rows)
+    tag = f"hq{hq}_kv{k.shape[0]}_n{n}_seed{seed}_rows{pos.size}_q128"
+    tables = os.path.join(ROOT, "oracle", "tables")
+    prof = os.path.join(tables, f"{tag}.profiles.json")
+    hit = committed_reference_table(hq, k.shape[0], n, seed, args.calib_rows, f)
+    if hit is not None:
+        return hit[0], f"{hit[1]} (headbal::load_allocation)"
+    if os.path.exists(prof):
+        curves = O.ref.load_profiles(prof)[0]
+        src = f"headbal::maxmin_allocate on oracle/tables/{os.path.basename(prof)} (headbal::load_profiles)"
+    else:
+        import torch
+        group = hq // k.shape[0]
+        idx = torch.as_tensor(pos, device=q.device)
+        Q = np.stack([_ref_f64(bf16_bits(q[h].index_select(0, idx))) for h in range(hq)])
+        K = np.stack([_ref_f64(bf16_bits(k[h // group])) for h in range(hq)])
+        V = np.stack([_ref_f64(bf16_bits(v[h // group])) for h in range(hq)])
+        grid = np.asarray(list(range(0, n, 128)) + [n], np.int64)
+        rec = O.ref.build_profiles(Q, K, V, grid, causal=False, kind=0)
+        curves = [(grid, r) for r in rec]
+        src = "headbal::build_profiles -> headbal::maxmin_allocate, computed in this run"
+    b, _, _ = O.ref.maxmin_allocate(curves, n, total, quantum=128, floor=128)
+    return b.astype(np.int64), src
+
+
+def c1_full_layer(args, repeats=1):
+    """C1 (BASELINE.json configs[0], the reference's own CPU-runnable case):
+    one Llama-3-8B-shaped layer (32 q / 8 kv heads, d = 128) of 8192 tokens,
+    causal, every head through headbal::sparse_attention with its own budget
+    (the run_skyline loop, commands.cpp:464-470) — timed in full, no
+    extrapolation, best of `repeats` (bench_attention.cpp:71-90). Budgets: the
+    reference's build_profiles -> maxmin_allocate at the bench's fraction. Also
+    the bench's sampled estimator on the same layer, to check the
+    extrapolation C3's value relies on."""
+    import torch
+    from oracle import oracle as O
+    from paper_2603_10353_b200.workload import LayerSpec, bf16_bits, make_layer
+    hq, hkv, n = 32, 8, 8192
+    q, k, v = make_layer(LayerSpec(num_q_heads=hq, num_kv_heads=hkv, seq_len=n, seed=args.seed), "cuda")
+    budgets, src = reference_table(q, k, v, args, args.seed)
+    group = hq // hkv
+    Qh = [_ref_f64(bf16_bits(q[h])) for h in range(hq)]
+    Kg = [_ref_f64(bf16_bits(k[g])) for g in range(hkv)]
+    Vg = [_ref_f64(bf16_bits(v[g])) for g in range(hkv)]
+    runs = []
+    for _ in range(max(1, repeats)):
+        t0 = time.perf_counter()
+        for h in range(hq):
+            O.ref.sparse_attention(Qh[h], Kg[h // group], Vg[h // group], int(budgets[h]), causal=True)
+        runs.append((time.perf_counter() - t0) * 1e3)
+    est, _, est_sample = cpu_reference_sample(q, k, v, budgets, group, 3.0, rng_seed=7)
+    del q, k, v
+    torch.cuda.empty_cache()
+    return {"what": ("C1: 32 q / 8 kv heads x 8192 tokens, causal, headbal::sparse_attention per head "
+                     "(PerQueryTopK, fp64) with its max-min budget, whole layer timed, no extrapolation"),
+            "ms": round(min(runs), 1), "runs_ms": [round(x, 1) for x in runs], "best_of": len(runs),
+            "budget_table": src, "budgets_min_max": [int(budgets.min()), int(budgets.max())],
+            "sampled_estimate_ms": round(est, 1), "sampled_estimate_over_measured": round(est / min(runs), 4),
+            "sampled_estimate": est_sample}
+
+
 def run_reference(args):
+    """The reference arm: headbal::sparse_attention (compiled unmodified into
+    oracle/_ref) on the box's host cores. A step = a bounded sample of (head,
+    row) pairs of layer 0 of the C3 stack with the budgets the reference's own
+    build_profiles -> maxmin_allocate produced for that layer; `value` is that
+    sample extrapolated linearly to ms per layer (per-row cost is O(n_k d)
+    whatever the budget or mask, attention.cpp:22-30), `ms_per_step` the
+    sample's measured wall time. `cpu_baseline.c1_full_layer` is a measured,
+    unextrapolated whole C1 layer."""
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -588,36 +699,54 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/libheadbal_ref.so not built (make -C oracle with /root/reference)"}))
         return
+    c1 = c1_full_layer(args, args.c1_repeats) if args.c1_repeats > 0 else None
     spec = LayerSpec(num_q_heads=args.q_heads, num_kv_heads=args.kv_heads, seq_len=args.seq_len,
                      seed=args.seed)
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     q, k, v = make_layer(spec, dev)
-    n, hq = args.seq_len, args.q_heads
-    total = int(round(args.budget_fraction * hq * n))
-    budgets = O.ref.uniform_allocate(hq, total, 128, n)
-    group = hq // args.kv_heads
+    budgets, table_src = reference_table(q, k, v, args, args.seed)
+    from paper_2603_10353_b200 import calibrate
+    group = args.q_heads // args.kv_heads
     per_step = max(1.0, args.cpu_seconds / max(1, args.steps))
-    vals = []
+    vals, walls = [], []
     threads, sample = 1, ""
     for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         ms, threads, sample = cpu_reference_sample(q, k, v, budgets, group, per_step, rng_seed=i)
         if i >= args.warmup:
             vals.append(ms)
+            walls.append((time.perf_counter() - t0) * 1e3)
     value = float(np.mean(vals))
+    step_ms = float(np.mean(walls))
+    cpu = {"value": round(value, 3), "unit": "ms", "cores": threads, "kind": "reference",
+           "cpu_model": cpu_model(),
+           "sample": (f"per step: {sample}; layer 0 of the stack, whose per-layer CPU cost stands for every "
+                      f"layer (budget- and mask-independent); step wall time = ms_per_step"),
+           "budget_table": table_src, "budget_table_digest": calibrate.table_digest(budgets)}
+    if c1:
+        cpu["c1_full_layer"] = c1
     line = {
         "impl": "reference",
         "metric": "attention ms/layer at 128K ctx (max over ranks)",
         "value": round(value, 3), "unit": "ms", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(value * args.layers, 3), "higher_is_better": False,
+        "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_dict(args, "uniform (reference uniform_allocate, same total B)",
-                              args.placement if world > 1 else "greedy"),
-        "cpu_baseline": {"value": round(value, 3), "unit": "ms", "cores": threads,
-                         "kind": "reference", "sample": sample},
+        "config": config_dict(args, budgets_desc(args), args.placement if world > 1 else "greedy"),
+        "cpu_baseline": cpu,
         "e2e": {"value": round(value, 3), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def budgets_desc(args):
+    """The budget table both arms use (the same string in both lines' config)."""
+    if args.allocation_json:
+        return f"from {args.allocation_json} (reference allocation.json)"
+    kind = ("ColumnAggregateTopK" if args.policy == "column_aggregate_topk"
+            else "PerQueryTopK (token level)" if args.profile_kind == "token" else "block selection")
+    return (f"max-min at {args.budget_fraction} x Hq x n tokens, quantum 128, floor 128, on {kind} recovery "
+            f"curves of {args.calib_rows} evenly spaced calibration rows per head, grid stride 128")
 
 
 PLACEMENTS = {
@@ -667,18 +796,18 @@ def main():
     hq, n, group = args.q_heads, args.seq_len, args.q_heads // args.kv_heads
     L = max(1, args.layers)
     layers, budgets_l, binfo = [], [], {}
+    ctx = P.Context(local)
     for li in range(L):  # distinct layers: own seeds, own budget tables
         spec = LayerSpec(num_q_heads=hq, num_kv_heads=args.kv_heads, seq_len=n,
                          seed=args.seed + 7919 * li)
         q, k, v = make_layer(spec, "cuda")
-        b_l, total, info_l = make_budgets(q, k, args, world, rank)
+        b_l, total, info_l = make_budgets(q, k, args, world, rank, pctx=ctx)
         layers.append((q, k, v))
         budgets_l.append(b_l)
         if li == 0:
             binfo = info_l
     torch.cuda.synchronize()
     budgets = budgets_l[0]
-    ctx = P.Context(local)
     stream = torch.cuda.Stream()
 
     plans_l = {"greedy": [P.greedy_assign(b, world) for b in budgets_l]}
@@ -762,10 +891,19 @@ def main():
         try:
             ms_cpu, cores, sample = cpu_reference_sample(q, k, v, budgets, group, args.cpu_seconds)
             cpu = {"value": round(ms_cpu, 1), "unit": "ms", "cores": cores, "kind": "reference",
-                   "sample": sample,
+                   "sample": sample, "cpu_model": cpu_model(),
                    "serial_one_head_ms": round(cpu_reference_serial_head(q, k, v, budgets, group), 1),
                    "serial_one_head_note": ("reference::sparse_attention (serial) on the largest-budget "
                                             "head, 8 rows timed, extrapolated to n rows")}
+            # The reference's own table for layer 0 (oracle/tables, written by headbal), if committed:
+            # same config as the reference arm iff this run's table equals it.
+            if not args.allocation_json and args.profile_kind == "token" and args.policy == "per_query_topk":
+                from paper_2603_10353_b200 import calibrate
+                hit = committed_reference_table(hq, args.kv_heads, n, args.seed, args.calib_rows,
+                                                args.budget_fraction)
+                if hit is not None:
+                    cpu["reference_table"] = {"file": hit[1], "digest": calibrate.table_digest(hit[0]),
+                                              "equal_to_this_run": bool(np.array_equal(hit[0], budgets))}
         except Exception as e:  # reference library missing: report, do not fail the bench
             cpu = {"value": None, "unit": "ms", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -790,7 +928,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(value * args.layers, 3), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded bf16 Q/K/V with per-head temperature, block-local structure)",
-        "config": config_dict(args, "max-min (calibration-profiled curves), quantum 128, floor 128", headline),
+        "config": config_dict(args, budgets_desc(args), headline),
         "tflops": round(flops_total / (value * 1e-3) / 1e12, 1),
         "layers_per_step": args.layers,
         "compute_only_ms": round(g["ms"], 3),

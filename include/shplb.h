@@ -124,6 +124,22 @@ int shplb_profile_curves_kind(shplb_ctx* ctx, const void* q_rows, const void* k,
                               const int64_t* grid, int64_t n_grid, int32_t kind, double* recovery_out,
                               void* stream);
 
+/* Recovery curves of the kernels' OWN selection (block granularity), the
+ * curve the layer call realises: for every calibration row at position rows[r]
+ * (strictly increasing, in [0, n)) of every q head, recovery(b) = the fraction
+ * of the row's exact softmax mass (fp64, keys j <= rows[r] when causal) inside
+ * the ceil(b/128) key blocks kernel 2 keeps for the row's query block (pooled
+ * fp32 block scores, (score desc, index asc), the visible blocks only) —
+ * recovery_ratio's kept-set mass (attention.cpp:151-184) with the block
+ * selector's kept set; averaged over rows as build_profiles does
+ * (profiler.cpp:157-196). q [Hq][n][d], k [Hkv][n][d] DEVICE bf16 (the whole
+ * layer: pooled query blocks need every row); rows / grid host int64;
+ * recovery_out host double [Hq][n_grid]. Synchronises `stream`. */
+int shplb_profile_curves_block(shplb_ctx* ctx, const void* q, const void* k, int32_t num_q_heads,
+                               int32_t num_kv_heads, int64_t n, int32_t d, int32_t block_q, int32_t causal,
+                               const int64_t* rows, int64_t n_rows, const int64_t* grid, int64_t n_grid,
+                               double* recovery_out, void* stream);
+
 /* ======================================================================
  * Head -> GPU plan   (reference: proj/include/headbal/partitioner.hpp)
  * ====================================================================== */

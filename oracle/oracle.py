@@ -305,6 +305,50 @@ def pooled_scores_rows(q_bits_h, kp, qbs, *, bq=128, bk=128, causal=True):
 # Budget table / plan / metric restatement
 # --------------------------------------------------------------------------
 
+def block_selection_profile(q_bits, k_bits, rows, grid, *, bq=128, causal=True):
+    """Recovery curves of the block selector (restates shplb_profile_curves_block):
+    per q head h and calibration row at position p, the kept blocks at budget b
+    are the ceil(b/128) best of the row's query block under kernel 2's rule
+    (pooled fp32 scores from the C restatement, (score desc, index asc), visible
+    blocks only); recovery = the row's exact fp64 softmax mass over keys j <= p
+    (causal) inside them (recovery_ratio's kept-set mass, attention.cpp:151-184),
+    averaged over rows (build_profiles, profiler.cpp:157-196).
+
+    q_bits [Hq, n, d], k_bits [Hkv, n, d] bf16 bit patterns -> [Hq, len(grid)]."""
+    q_bits = np.ascontiguousarray(q_bits, np.uint16)
+    k_bits = np.ascontiguousarray(k_bits, np.uint16)
+    hq, n, d = q_bits.shape
+    hkv = k_bits.shape[0]
+    group = hq // hkv
+    nkb = nblocks(n, 128)
+    grid = np.asarray(grid, np.int64)
+    rows = np.asarray(rows, np.int64)
+    out = np.zeros((hq, grid.size))
+    for g in range(hkv):
+        K = bf16_bits_to_f32(k_bits[g]).astype(np.float64)
+        kp = pool_blocks(k_bits[g], 128)
+        for h in range(g * group, (g + 1) * group):
+            bs = block_scores(pool_blocks(q_bits[h], bq), kp, n, bq, 128, causal)
+            Q = bf16_bits_to_f32(q_bits[h][rows]).astype(np.float64)
+            S = (Q @ K.T) * (1.0 / np.sqrt(d))
+            for r, p in enumerate(rows):
+                end = p + 1 if causal else n
+                s = S[r, :end]
+                w = np.exp(s - s.max())
+                mass = np.zeros(nkb)
+                np.add.at(mass, np.arange(end) // 128, w)
+                mass /= w.sum()
+                qb = p // bq
+                vis = visible_blocks(qb, n, bq, 128, causal)
+                sc = bs[qb, :vis].astype(np.float32)
+                sc = np.where(sc == 0, np.float32(0), sc)  # -0.0 ties with +0.0
+                order = np.lexsort((np.arange(vis), -sc.astype(np.float64)))
+                cum = np.concatenate([[0.0], np.cumsum(mass[order])])
+                kb = np.minimum((grid + 127) // 128, vis)
+                out[h] += np.minimum(cum[kb], 1.0)
+    return out / rows.size
+
+
 def _flatten_curves(curves):
     offsets = np.zeros(len(curves) + 1, np.int64)
     for h, (b, _) in enumerate(curves):

@@ -19,7 +19,7 @@ EXPORTS = (
     "shplb_last_error", "shplb_version",
     "shplb_uniform_allocate", "shplb_maxmin_allocate", "shplb_recovery_at", "shplb_budget_for_recovery",
     "shplb_profile_curves_host", "shplb_profile_curves",
-    "shplb_profile_curves_host_kind", "shplb_profile_curves_kind",
+    "shplb_profile_curves_host_kind", "shplb_profile_curves_kind", "shplb_profile_curves_block",
     "shplb_plan_naive", "shplb_plan_greedy", "shplb_plan_optimal", "shplb_plan_split", "shplb_imbalance",
     "shplb_simulate", "shplb_barrier",
     "shplb_ctx_create", "shplb_ctx_destroy", "shplb_ctx_launch_count",
@@ -140,6 +140,7 @@ def lib() -> C.CDLL:
     L.shplb_profile_curves.argtypes = [vp, vp, vp, i32, i32, i64, i64, i32, vp, i64, vp, vp]
     L.shplb_profile_curves_host_kind.argtypes = [vp, vp, i32, i32, i64, i64, i32, vp, i64, i32, vp]
     L.shplb_profile_curves_kind.argtypes = [vp, vp, vp, i32, i32, i64, i64, i32, vp, i64, i32, vp, vp]
+    L.shplb_profile_curves_block.argtypes = [vp, vp, vp, i32, i32, i64, i32, i32, i32, vp, i64, vp, i64, vp, vp]
     L.shplb_plan_naive.argtypes = [vp, i32, i32, i32, vp]
     L.shplb_plan_greedy.argtypes = [vp, i32, i32, vp]
     L.shplb_plan_optimal.argtypes = [vp, i32, i32, vp]

@@ -368,6 +368,27 @@ class Context:
                                               _stream_ptr(stream)))
         return [RecoveryCurve(grid.copy(), out[h].copy(), n_k) for h in range(hq)]
 
+    def profile_curves_block(self, q, k, rows, grid, block_q=BLOCK_Q, causal=True,
+                             stream=None) -> list[RecoveryCurve]:
+        """Recovery curves of the kernels' own block selection
+        (shplb_profile_curves_block): per q head, the mean over calibration rows
+        (positions `rows`, strictly increasing) of the exact softmax mass inside
+        the ceil(b/128) key blocks kernel 2 keeps for the row's query block.
+        q [Hq, n, d], k [Hkv, n, d] bf16 CUDA (the whole layer)."""
+        import torch
+        q = q.contiguous()
+        k = k.contiguous()
+        _dev_ptr(q, "q", torch.bfloat16)
+        _dev_ptr(k, "k", torch.bfloat16)
+        grid = _i64(grid)
+        rows = _i64(rows)
+        hq, n, d = q.shape
+        out = np.empty((hq, grid.size), np.float64)
+        check(lib().shplb_profile_curves_block(self._h, q.data_ptr(), k.data_ptr(), hq, k.shape[0], n, d,
+                                               block_q, int(bool(causal)), _ptr(rows), rows.size, _ptr(grid),
+                                               grid.size, _ptr(out), _stream_ptr(stream)))
+        return [RecoveryCurve(grid.copy(), out[h].copy(), n) for h in range(hq)]
+
     # -- kernel 1 ---------------------------------------------------------
     def block_scores(self, q, k, causal=True, stream=None, validate=False, out=None, kv_map=None,
                      block_q=BLOCK_Q):

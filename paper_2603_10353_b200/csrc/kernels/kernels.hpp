@@ -89,6 +89,17 @@ void launch_profile_colagg(double* scores, int heads, int64_t n_rows, int64_t n_
 void launch_profile_rows(const double* mass, int hq, int64_t n_rows, const int64_t* grid, int64_t n_grid,
                          double* recovery, cudaStream_t s);
 
+// Block-selection recovery (profiler.cu): scores = fp64 token scores of the
+// units of q heads [h0, h0 + heads) x calibration rows [units][n]; bscores =
+// kernel 2's block-score matrix [hq][nqb][nkb]; rows = device positions;
+// mass [hq*n_rows][n_grid] (rows of heads h0.. written).
+void launch_profile_block(const double* scores, const float* bscores, const int64_t* rows, int h0, int heads,
+                          int64_t n_rows, int64_t n, int bq, bool causal, const int64_t* grid, int64_t n_grid,
+                          double* mass, cudaStream_t s);
+// out [hq][n_rows][128] bf16 = q[h][rows[r]][:].
+void launch_gather_rows(const void* q, const int64_t* rows, int hq, int64_t n, int64_t n_rows, void* out,
+                        cudaStream_t s);
+
 // Block-level ColumnAggregateTopK from a score matrix [hq][nqb][nkb]: one kept
 // key-block set per head (largest block-weight column sums), each query block
 // gets its visible part. work: colagg_work_floats(...) floats; kept: hq*(kmax+1) int32.

@@ -21,6 +21,7 @@
 //
 // Results agree with the host restatement and the reference to rounding
 // (the reference itself sums the top-k in nth_element's arbitrary order).
+#include <algorithm>
 #include <cstdint>
 
 #include <cub/device/device_segmented_radix_sort.cuh>
@@ -219,7 +220,186 @@ __global__ void segment_offsets_kernel(int64_t* off, int64_t units, int64_t n_k)
     if (t <= units) off[t] = t * n_k;
 }
 
+// ---- Block-selection recovery (the kernels' own policy) --------------------
+//
+// The curve the layer actually realises: for calibration row i at position
+// pos (causal: keys j <= pos), kernel 2 keeps the k highest-scoring 128-key
+// blocks of i's query block (pooled fp32 scores, (score desc, index asc),
+// among the blocks visible to the query block). recovery(k) = the fraction of
+// row i's exact softmax mass (fp64, max-subtracted as attention.cpp:35-49)
+// inside those k blocks — recovery_ratio's "mass of the kept set"
+// (attention.cpp:151-184) with the kept set chosen by the block selector
+// instead of per-token top-k. Budgets in tokens map to ceil(b / 128) blocks,
+// as budgets_to_blocks does for the layer call.
+
+constexpr int kBlockProfThreads = 1024;
+
+__device__ __forceinline__ uint32_t prof_order_key(float s) {  // = estimator.cu order_key
+    const uint32_t u = __float_as_uint(__fadd_rn(s, 0.0f));
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ double block_reduce_sum(double v, double* red) {
+    // fixed order: warp xor-tree, then warp partials ascending by one thread
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kBlockProfThreads / 32; ++w) t += red[w];
+        red[32] = t;
+    }
+    __syncthreads();
+    return red[32];
+}
+
+__device__ __forceinline__ double block_reduce_max(double v, double* red) {
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = -INFINITY;
+        for (int w = 0; w < kBlockProfThreads / 32; ++w) t = fmax(t, red[w]);
+        red[32] = t;
+    }
+    __syncthreads();
+    return red[32];
+}
+
+// One CTA per (head, calibration row) of a kv batch. scores: fp64 token scores
+// of the batch's units [units][n] (unit = local head * n_rows + r); bscores:
+// kernel 2's fp32 block-score matrix [hq][nqb][nkb] (-inf where invisible).
+// Dynamic smem: keys u64[max(P, threads)] (reused as the scan scratch), mass
+// double[P] (P = next power of two >= nkb).
+__global__ void __launch_bounds__(kBlockProfThreads) profile_block_kernel(
+    const double* __restrict__ scores, const float* __restrict__ bscores, const int64_t* __restrict__ rows,
+    int h0, int64_t n_rows, int64_t n, int64_t nqb, int64_t nkb, int bq, int causal, int pow2,
+    const int64_t* __restrict__ grid, int64_t n_grid, double* __restrict__ mass_out) {
+    extern __shared__ __align__(16) unsigned char bp_smem[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(bp_smem);
+    double* mass = reinterpret_cast<double*>(keys + max(pow2, kBlockProfThreads));
+    __shared__ double red[33];
+    const int64_t unit = blockIdx.x;
+    const int h = h0 + static_cast<int>(unit / n_rows);
+    const int64_t r = unit % n_rows;
+    const int64_t pos = rows[r];
+    const double* s = scores + unit * n;
+    const int64_t tok_end = causal ? pos + 1 : n;
+    const int64_t qb = pos / bq;
+    const int64_t vis = causal ? min((min((qb + 1) * bq, n) - 1) / kBlock + 1, nkb) : nkb;
+
+    double m = -INFINITY;
+    for (int64_t j = threadIdx.x; j < tok_end; j += kBlockProfThreads) m = fmax(m, s[j]);
+    m = block_reduce_max(m, red);
+    // Unnormalised mass of every key block: warp w sums blocks w, w + 32, ...
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t b = warp; b < pow2; b += kBlockProfThreads / 32) {
+        double e = 0.0;
+        if (b < nkb) {
+            for (int i = 0; i < kBlock / 32; ++i) {
+                const int64_t j = b * kBlock + i * 32 + lane;
+                if (j < tok_end) e += exp(s[j] - m);
+            }
+            for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        }
+        if (lane == 0) mass[b] = e;
+    }
+    __syncthreads();
+    double zpart = 0.0;
+    for (int64_t b = threadIdx.x; b < nkb; b += kBlockProfThreads) zpart += mass[b];
+    const double inv_z = 1.0 / block_reduce_sum(zpart, red);
+    // Rank keys of the row's query block: (order key << 32) | ~index, so a
+    // descending sort is (score desc, index asc); invisible blocks sort last.
+    const float* brow = bscores + (static_cast<int64_t>(h) * nqb + qb) * nkb;
+    for (int64_t b = threadIdx.x; b < pow2; b += kBlockProfThreads) {
+        keys[b] = b < vis ? (static_cast<uint64_t>(prof_order_key(brow[b])) << 32) |
+                                static_cast<uint64_t>(0xFFFFFFFFu - static_cast<uint32_t>(b))
+                          : 0ull;
+    }
+    __syncthreads();
+    // Bitonic sort, descending by key, masses carried along.
+    for (int size = 2; size <= pow2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = threadIdx.x; t < pow2 / 2; t += kBlockProfThreads) {
+                const int lo = 2 * t - (t & (stride - 1));
+                const int hi = lo + stride;
+                const bool desc = (lo & size) == 0;
+                const uint64_t a = keys[lo], c = keys[hi];
+                if ((a < c) == desc) {
+                    keys[lo] = c;
+                    keys[hi] = a;
+                    const double x = mass[lo];
+                    mass[lo] = mass[hi];
+                    mass[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // Inclusive prefix of the ranked masses, serial per thread chunk then a
+    // fixed-order scan of the chunk totals.
+    const int per = (pow2 + kBlockProfThreads - 1) / kBlockProfThreads;
+    const int lo = threadIdx.x * per, hi = min(lo + per, pow2);
+    double local = 0.0;
+    for (int i = lo; i < hi; ++i) local += mass[i];
+    __syncthreads();
+    double* part = reinterpret_cast<double*>(keys);  // keys are no longer needed
+    part[threadIdx.x] = local;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double run = 0.0;
+        for (int t = 0; t < kBlockProfThreads; ++t) {
+            const double x = part[t];
+            part[t] = run;
+            run += x;
+        }
+    }
+    __syncthreads();
+    double run = part[threadIdx.x];
+    for (int i = lo; i < hi; ++i) {
+        run += mass[i];
+        mass[i] = run;
+    }
+    __syncthreads();
+    for (int64_t gi = threadIdx.x; gi < n_grid; gi += kBlockProfThreads) {
+        const int64_t kb = min((grid[gi] + kBlock - 1) / kBlock, vis);
+        mass_out[(static_cast<int64_t>(h) * n_rows + r) * n_grid + gi] = kb == 0 ? 0.0 : fmin(mass[kb - 1] * inv_z, 1.0);
+    }
+}
+
+__global__ void gather_rows_kernel(const uint4* __restrict__ q, const int64_t* __restrict__ rows, int hq,
+                                   int64_t n, int64_t n_rows, uint4* __restrict__ out) {
+    constexpr int kVec = kHeadDim * 2 / 16;  // 16-byte vectors per row
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= static_cast<int64_t>(hq) * n_rows * kVec) return;
+    const int64_t v = t % kVec, u = t / kVec, h = u / n_rows, r = u % n_rows;
+    out[t] = q[(h * n + rows[r]) * kVec + v];
+}
+
 }  // namespace
+
+void launch_gather_rows(const void* q, const int64_t* rows, int hq, int64_t n, int64_t n_rows, void* out,
+                        cudaStream_t s) {
+    const int64_t total = static_cast<int64_t>(hq) * n_rows * (kHeadDim * 2 / 16);
+    gather_rows_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+        static_cast<const uint4*>(q), rows, hq, n, n_rows, static_cast<uint4*>(out));
+}
+
+void launch_profile_block(const double* scores, const float* bscores, const int64_t* rows, int h0, int heads,
+                          int64_t n_rows, int64_t n, int bq, bool causal, const int64_t* grid, int64_t n_grid,
+                          double* mass, cudaStream_t s) {
+    const int64_t nkb = (n + kBlock - 1) / kBlock, nqb = (n + bq - 1) / bq;
+    int pow2 = 1;
+    while (pow2 < nkb) pow2 <<= 1;
+    pow2 = max(pow2, 2);
+    const size_t smem = static_cast<size_t>(std::max(pow2, kBlockProfThreads)) * sizeof(uint64_t) +
+                        static_cast<size_t>(pow2) * sizeof(double);
+    cudaFuncSetAttribute(profile_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    profile_block_kernel<<<static_cast<unsigned>(static_cast<int64_t>(heads) * n_rows), kBlockProfThreads, smem, s>>>(
+        scores, bscores, rows, h0, n_rows, n, nqb, nkb, bq, causal ? 1 : 0, pow2, grid, n_grid, mass);
+}
 
 void launch_profile_scores(const void* q_rows, const void* k, int hq, int hkv, int64_t n_rows,
                            int64_t n_k, double scale, double* scores, cudaStream_t s) {

@@ -242,6 +242,12 @@ struct shplb_ctx {
     size_t prof_aux_bytes = 0;
     void* prof_temp = nullptr;
     size_t prof_temp_bytes = 0;
+    float* prof_bscores = nullptr;  // block-selection profile: kernel 2's score matrix
+    size_t prof_bscores_bytes = 0;
+    uint16_t* prof_qrows = nullptr;  // gathered calibration rows (bf16)
+    size_t prof_qrows_bytes = 0;
+    int64_t* prof_rows = nullptr;  // their positions
+    size_t prof_rows_bytes = 0;
     // ColumnAggregateTopK workspace: score matrix + row/column statistics, kept sets.
     float* ca_ws = nullptr;
     size_t ca_ws_bytes = 0;
@@ -565,6 +571,9 @@ int shplb_ctx_destroy(shplb_ctx* ctx) {
         cudaFree(ctx->prof_mass);
         cudaFree(ctx->prof_aux);
         cudaFree(ctx->prof_temp);
+        cudaFree(ctx->prof_bscores);
+        cudaFree(ctx->prof_qrows);
+        cudaFree(ctx->prof_rows);
         if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
         if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
         if (ctx->compute) cudaStreamDestroy(ctx->compute);
@@ -1096,6 +1105,85 @@ int shplb_profile_curves(shplb_ctx* ctx, const void* q_rows, const void* k, int3
                          const int64_t* grid, int64_t n_grid, double* recovery_out, void* stream) {
     return shplb_profile_curves_kind(ctx, q_rows, k, num_q_heads, num_kv_heads, n_rows, n_k, d, grid, n_grid,
                                      SHPLB_BLOCK_TOPK, recovery_out, stream);
+}
+
+int shplb_profile_curves_block(shplb_ctx* ctx, const void* q, const void* k, int32_t num_q_heads,
+                               int32_t num_kv_heads, int64_t n, int32_t d, int32_t block_q, int32_t causal,
+                               const int64_t* rows, int64_t n_rows, const int64_t* grid, int64_t n_grid,
+                               double* recovery_out, void* stream) {
+    return guarded([&] {
+        require(ctx != nullptr, "ctx is null");
+        require(num_q_heads >= 1 && num_kv_heads >= 1 && num_q_heads % num_kv_heads == 0,
+                "num_q_heads must be a positive multiple of num_kv_heads");
+        require(n_rows >= 1 && n >= 1, "profile needs at least one row and key");
+        require(grid != nullptr && rows != nullptr && recovery_out != nullptr, "grid / rows / recovery_out is null");
+        if (n_grid < 1) throw InvalidArgument("budget grid is empty");
+        for (int64_t i = 0; i < n_grid; ++i) {  // build_profiles' grid checks (profiler.cpp:165-177)
+            if (grid[i] < 0 || grid[i] > n) {
+                throw InvalidArgument("budget grid entry " + std::to_string(grid[i]) + " out of [0, " +
+                                      std::to_string(n) + "]");
+            }
+            if (i > 0 && grid[i] <= grid[i - 1]) throw InvalidArgument("budget grid must be strictly increasing");
+        }
+        if (grid[n_grid - 1] != n) throw InvalidArgument("budget grid must include the full context length");
+        for (int64_t r = 0; r < n_rows; ++r) {
+            if (rows[r] < 0 || rows[r] >= n || (r > 0 && rows[r] <= rows[r - 1]))
+                throw InvalidArgument("calibration rows must be strictly increasing positions in [0, n)");
+        }
+        shplb_layer_shape sh{};
+        sh.num_q_heads = num_q_heads;
+        sh.num_kv_heads = num_kv_heads;
+        sh.seq_len = n;
+        sh.head_dim = d;
+        sh.block_q = block_q;
+        sh.block_k = kern::kBlock;
+        sh.causal = causal;
+        sh.kind = SHPLB_BLOCK_TOPK;
+        check_shape(&sh);
+        check_ptr(q, "q");
+        check_ptr(k, "k");
+        DeviceGuard dg(ctx->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int64_t nqb = cdiv(n, block_q), nkb = cdiv(n, kern::kBlock);
+        // Kernel 1 + kernel 2's scores (the very ranking the layer call uses).
+        grow(ctx->prof_bscores, ctx->prof_bscores_bytes, sizeof(float) * num_q_heads * nqb * nkb);
+        kern::HeadTable ht{};
+        fill_kv_map(&sh, ht);
+        pool_and_score(ctx, &sh, q, k, ht, 1, ctx->prof_bscores, false, nullptr, nullptr, st);
+        // Calibration rows and fp64 token scores, kv batches bounded as in shplb_profile_curves_kind.
+        grow(ctx->prof_rows, ctx->prof_rows_bytes, sizeof(int64_t) * n_rows);
+        grow(ctx->prof_qrows, ctx->prof_qrows_bytes, sizeof(uint16_t) * num_q_heads * n_rows * d);
+        const int32_t group = num_q_heads / num_kv_heads;
+        const int64_t units_per_kv = int64_t(group) * n_rows, units_total = int64_t(num_q_heads) * n_rows;
+        int64_t kv_batch = std::max<int64_t>(1, (int64_t(1) << 32) / (8 * units_per_kv * n));
+        kv_batch = std::min<int64_t>(kv_batch, num_kv_heads);
+        grow(ctx->prof_scores, ctx->prof_scores_bytes, sizeof(double) * kv_batch * units_per_kv * n);
+        grow(ctx->prof_mass, ctx->prof_mass_bytes,
+             sizeof(double) * (units_total * n_grid + int64_t(num_q_heads) * n_grid));
+        grow(ctx->prof_aux, ctx->prof_aux_bytes, sizeof(int64_t) * n_grid);
+        int64_t* grid_dev = ctx->prof_aux;
+        double* recovery_dev = ctx->prof_mass + units_total * n_grid;
+        SHPLB_CUDA(cudaMemcpyAsync(grid_dev, grid, sizeof(int64_t) * n_grid, cudaMemcpyHostToDevice, st));
+        SHPLB_CUDA(cudaMemcpyAsync(ctx->prof_rows, rows, sizeof(int64_t) * n_rows, cudaMemcpyHostToDevice, st));
+        kern::launch_gather_rows(q, ctx->prof_rows, num_q_heads, n, n_rows, ctx->prof_qrows, st);
+        check_launch(ctx);
+        const double scale = 1.0 / std::sqrt(static_cast<double>(d));
+        for (int64_t g0 = 0; g0 < num_kv_heads; g0 += kv_batch) {
+            const int64_t nb = std::min<int64_t>(kv_batch, num_kv_heads - g0);
+            kern::launch_profile_scores(ctx->prof_qrows + g0 * units_per_kv * d,
+                                        static_cast<const uint16_t*>(k) + g0 * n * d, static_cast<int>(nb * group),
+                                        static_cast<int>(nb), n_rows, n, scale, ctx->prof_scores, st);
+            kern::launch_profile_block(ctx->prof_scores, ctx->prof_bscores, ctx->prof_rows,
+                                       static_cast<int>(g0 * group), static_cast<int>(nb * group), n_rows, n,
+                                       block_q, causal != 0, grid_dev, n_grid, ctx->prof_mass, st);
+            check_launch(ctx, 2);
+        }
+        kern::launch_profile_rows(ctx->prof_mass, num_q_heads, n_rows, grid_dev, n_grid, recovery_dev, st);
+        check_launch(ctx);
+        SHPLB_CUDA(cudaMemcpyAsync(recovery_out, recovery_dev, sizeof(double) * num_q_heads * n_grid,
+                                   cudaMemcpyDeviceToHost, st));
+        SHPLB_CUDA(cudaStreamSynchronize(st));
+    });
 }
 
 // IPC handle layout (SHPLB_IPC_HANDLE_BYTES = 72): the CUDA IPC handle of the

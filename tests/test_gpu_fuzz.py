@@ -10,7 +10,7 @@ import torch
 
 from oracle import oracle as O
 from paper_2603_10353_b200.workload import LayerSpec, bf16_bits, make_layer
-from test_gpu_parity import MAX_ABS, MEAN_REL
+from tolerance import check_output
 
 pytestmark = pytest.mark.gpu
 
@@ -67,7 +67,4 @@ def test_random_layer(cuda_ctx, seed):
         mask[h, lo * bq:min(hi * bq, n)] = True
     assert np.all(g[~mask] == SENTINEL), "rows outside the query-block range were written"
     if mask.any():
-        diff = np.abs(g[mask] - out_o[mask])
-        mx = float(diff.max())
-        rel = float(diff.sum() / max(np.abs(out_o[mask]).sum(), 1e-300))
-        assert mx <= MAX_ABS and rel <= MEAN_REL, (c, mx, rel)
+        check_output(g[mask], out_o[mask], str(c))

@@ -4,11 +4,10 @@
   BIT-EXACT with the C restatement (oracle/shplb_oracle.c) — integer decisions
   on fp32 scores computed in the same fixed order on both sides.
 * Kernel 3 outputs must match the fp64 oracle on the same kept sets within
-  the bf16 tolerance below (north_star: "max-abs 2e-2, mean-rel 1e-3"-style):
-      max |gpu - ref|               <= 2e-2
-      sum |gpu - ref| / sum |ref|   <= MEAN_REL
-  where MEAN_REL allows for the output's own bf16 rounding (~2^-9 relative per
-  element, mean ~1e-3) plus bf16 P in the P.V product.
+  the bf16 tolerance of tests/tolerance.py: max-abs <= 2e-2 and mean-rel <=
+  1.6 x the bf16 rounding floor of the compared reference rows (the floor is
+  ~1.4e-3, so the north_star's 1e-3 example is below what any bf16 output can
+  reach; the gate is derived per comparison instead).
 """
 import numpy as np
 import pytest
@@ -20,14 +19,7 @@ from paper_2603_10353_b200.workload import LayerSpec, bf16_bits, make_layer
 
 pytestmark = pytest.mark.gpu
 
-MAX_ABS = 2e-2
-MEAN_REL = 4e-3
-
-
-def _errors(gpu_bf16: torch.Tensor, ref: np.ndarray):
-    g = gpu_bf16.float().cpu().numpy().astype(np.float64)
-    diff = np.abs(g - ref)
-    return float(diff.max()), float(diff.sum() / max(np.abs(ref).sum(), 1e-300))
+from tolerance import check_output  # noqa: E402
 
 
 def _scores_equal(a: np.ndarray, b: np.ndarray) -> bool:
@@ -57,8 +49,7 @@ def run_case(ctx, spec: LayerSpec, k_blocks, causal=True, bq=256):
 
     out = ctx.block_sparse_attention(qd, kd, vd, idx, cnt, causal=causal, block_q=bq)
     torch.cuda.synchronize()
-    mx, rel = _errors(out, out_o)
-    assert mx <= MAX_ABS and rel <= MEAN_REL, f"kernel 3: max-abs {mx:.3e}, mean-rel {rel:.3e}"
+    mx, rel, _ = check_output(out, out_o, "kernel 3")
 
     budgets = np.minimum(k_blocks * 128, spec.seq_len)
     out2 = ctx.sparse_attention_layer(qd, kd, vd, budgets, causal=causal, block_q=bq)
@@ -111,8 +102,7 @@ def test_full_budget_equals_dense(cuda_ctx):
             s[np.triu_indices(512, 1)] = -np.inf
             w = np.exp(s - s.max(1, keepdims=True))
             ref = (w / w.sum(1, keepdims=True)) @ V
-        mx, rel = _errors(out[h], ref)
-        assert mx <= MAX_ABS and rel <= MEAN_REL, (h, mx, rel)
+        check_output(out[h], ref, f"head {h}")
 
 
 @pytest.mark.parametrize("bq", [256, 128])
@@ -218,40 +208,61 @@ def test_c1_shape_two_heads_full_oracle(cuda_ctx, bq):
     run_case(cuda_ctx, spec, [4, 24], causal=True, bq=bq)
 
 
+# BASELINE.json configs at full size: (q heads, kv heads, n, requests stacked on the head axis).
+AT_SIZE = {
+    "C3": (32, 8, 131072, 1),    # Llama-3-8B layer at 128K
+    "C4": (28, 4, 65536, 1),     # Qwen2.5-7B layer at 64K (GQA 7)
+    "C5x2": (64, 8, 131072, 2),  # Llama-3-70B layer at 128K, two requests batched (128 q / 16 kv heads)
+}
+
+
+def at_size_layer(cfg: str, device="cuda"):
+    hq, hkv, n, reqs = AT_SIZE[cfg]
+    parts = [make_layer(LayerSpec(num_q_heads=hq, num_kv_heads=hkv, seq_len=n, seed=2603 + 101 * r), device)
+             for r in range(reqs)]
+    return tuple(torch.cat([p[i] for p in parts]) if reqs > 1 else parts[0][i] for i in range(3))
+
+
 @pytest.mark.slow
-def test_c3_size_sampled_rows(cuda_ctx):
-    """Full 128K Llama-3-8B layer (32 q / 8 kv heads): size-independent checks
-    on every tile (counts, ascending in-range indices) and bit-exact selection
-    plus fp64 outputs on sampled (head, query block) rows."""
-    n = 131072
-    spec = LayerSpec(num_q_heads=32, num_kv_heads=8, seq_len=n, seed=2603)
-    q, k, v = make_layer(spec, "cuda")
-    rng = np.random.default_rng(0)
-    budgets = rng.choice([128, 1024, 8192, 32768], size=32).astype(np.int64)
-    out = cuda_ctx.sparse_attention_layer(q, k, v, budgets, causal=True)
+@pytest.mark.parametrize("cfg,bq", [("C3", 256), ("C3", 128), ("C4", 256), ("C4", 128), ("C5x2", 256)])
+def test_at_size_sampled_rows(cuda_ctx, cfg, bq):
+    """A whole BASELINE config layer at full size through the layer call:
+    size-independent checks on every (head, query block) row (count = min(k_h,
+    visible), ascending in-range indices), then bit-exact selection against the
+    C restatement and fp64 outputs (bf16-floor gate) on sampled (head, query
+    block) rows, in the style of the reference's oracle comparison
+    (test_attention.cpp:143-177)."""
+    q, k, v = at_size_layer(cfg)
+    hq, n, _ = q.shape
+    group = hq // k.shape[0]
+    rng = np.random.default_rng(hash(cfg) % 2**32 + bq)
+    budgets = rng.choice([128, 1024, 8192, n // 4], size=hq).astype(np.int64)
+    out = cuda_ctx.sparse_attention_layer(q, k, v, budgets, causal=True, block_q=bq)
     torch.cuda.synchronize()
-    idx, cnt = cuda_ctx.last_selection(32, n)
+    idx, cnt = cuda_ctx.last_selection(hq, n)
     idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
-    nqb = n // 256
-    vis = 2 * np.arange(1, nqb + 1)  # a 256-row block sees 2 more key blocks per step
+    nqb = n // bq
+    vis = (bq // 128) * np.arange(1, nqb + 1)
     kb = (budgets + 127) // 128
     assert np.array_equal(cnt, np.minimum(kb[:, None], vis[None, :]))
-    for h in rng.choice(32, 4, replace=False):
-        g = h // 4
+    live = np.arange(idx.shape[2])[None, None, :] < cnt[:, :, None]  # every row at once
+    assert (idx[~live] == -1).all(), "padding past the count must be -1"
+    assert (idx[live] >= 0).all() and (idx < vis[None, :, None])[live].all(), "index outside the causal range"
+    assert (idx[:, :, 1:] > idx[:, :, :-1])[live[:, :, 1:]].all(), "selection not strictly ascending"
+    for h in sorted(rng.choice(hq, 4, replace=False).tolist()):
+        g = h // group
         qbits, kbits, vbits = bf16_bits(q[h]), bf16_bits(k[g]), bf16_bits(v[g])
         kp = O.pool_blocks(kbits, 128)
-        qbs = sorted(set(rng.choice(nqb, 3, replace=False).tolist() + [nqb - 1]))
-        sc = O.pooled_scores_rows(qbits, kp, qbs, bq=256)
+        qbs = sorted(set(rng.choice(nqb, 3, replace=False).tolist() + [0, nqb - 1]))
+        sc = O.pooled_scores_rows(qbits, kp, qbs, bq=bq)
         for r, qbk in enumerate(qbs):
             c = cnt[h, qbk]
             sel = idx[h, qbk, :c]
-            assert (np.diff(sel) > 0).all() and sel.min() >= 0 and sel.max() <= 2 * qbk + 1
-            want = np.sort(O.topk_row(sc[r, :2 * qbk + 2].astype(np.float64), c))
-            assert np.array_equal(sel, want), (h, qbk)
-            rows = [qbk * 256, qbk * 256 + 77, qbk * 256 + 128, qbk * 256 + 255]
+            want = np.sort(O.topk_row(sc[r, :vis[qbk]].astype(np.float64), c))
+            assert np.array_equal(sel, want), (cfg, h, qbk)
+            rows = sorted({qbk * bq, qbk * bq + 77, qbk * bq + bq // 2, qbk * bq + bq - 1})
             ref = O.sparse_rows(qbits, kbits, vbits, rows, sel.tolist())
-            mx, rel = _errors(out[h, rows], ref)
-            assert mx <= MAX_ABS and rel <= MEAN_REL, (h, qbk, mx, rel)
+            check_output(out[h, rows], ref, f"{cfg} bq {bq} head {h} qb {qbk}")
 
 
 @pytest.mark.parametrize("bq", [256, 128])
@@ -417,8 +428,7 @@ def test_zero_q_gives_uniform_weights_over_kept_keys(cuda_ctx):
     for i in range(n):
         last = min(i, kblk * 128 - 1)  # kept blocks 0..kblk-1, causal
         ref[i] = vf[: last + 1].mean(0)
-    mx, rel = _errors(out[0], ref)
-    assert mx <= MAX_ABS and rel <= MEAN_REL, (mx, rel)
+    check_output(out[0], ref, "zero q")
 
 
 def test_cta_pair_kernel_variant():

@@ -86,3 +86,45 @@ def test_gpu_profile_errors(cuda_ctx):
     with pytest.raises(P.InvalidArgument, match="multiple of num_kv_heads"):
         cuda_ctx.profile_curves(torch.zeros((3, 2, 128), dtype=torch.bfloat16, device="cuda"),
                                 torch.zeros((2, 64, 128), dtype=torch.bfloat16, device="cuda"), [0, 64])
+
+
+@pytest.mark.parametrize("hq,hkv,n,bq,causal,nrows", [(4, 2, 1000, 128, True, 7), (4, 2, 1000, 256, True, 5),
+                                                      (2, 1, 300, 256, False, 3), (8, 2, 4096, 256, True, 16),
+                                                      (3, 3, 129, 128, True, 2)])
+def test_block_selection_profile_matches_oracle(cuda_ctx, hq, hkv, n, bq, causal, nrows):
+    """shplb_profile_curves_block against the numpy/C restatement
+    (oracle.block_selection_profile): same kept blocks (kernel 2's fp32 ranking),
+    fp64 masses to rounding."""
+    q, k, _ = make_layer(LayerSpec(num_q_heads=hq, num_kv_heads=hkv, seq_len=n, seed=n + bq), "cpu")
+    rows = np.unique(np.linspace(0, n - 1, nrows).round().astype(np.int64))
+    grid = P.default_budget_grid(n, 128)
+    gpu = cuda_ctx.profile_curves_block(q.cuda(), k.cuda(), rows, grid, block_q=bq, causal=causal)
+    want = O.block_selection_profile(bf16_bits(q), bf16_bits(k), rows, grid, bq=bq, causal=causal)
+    for h in range(hq):
+        assert np.abs(gpu[h].recovery - want[h]).max() < TOL, f"head {h}"
+        assert gpu[h].recovery[0] == 0.0 and abs(gpu[h].recovery[-1] - 1.0) < 1e-9
+        assert (np.diff(gpu[h].recovery) >= 0).all()
+
+
+def test_block_selection_profile_is_the_layers_kept_mass(cuda_ctx):
+    """At a budget b the curve equals the softmax mass (fp64) of the calibration
+    rows inside the blocks the LAYER CALL actually selected with every head at b
+    — the profile describes the kernels' own selection, not a restatement of it."""
+    hq, hkv, n, bq = 4, 2, 2048, 256
+    q, k, v = make_layer(LayerSpec(num_q_heads=hq, num_kv_heads=hkv, seq_len=n, seed=5), "cpu")
+    rows = np.array([100, 700, 1300, 2047], np.int64)
+    grid = P.default_budget_grid(n, 128)
+    curves = cuda_ctx.profile_curves_block(q.cuda(), k.cuda(), rows, grid, block_q=bq)
+    for b in (128, 384, 1024):
+        cuda_ctx.sparse_attention_layer(q.cuda(), k.cuda(), v.cuda(), np.full(hq, b), block_q=bq)
+        idx, cnt = (t.cpu().numpy() for t in cuda_ctx.last_selection(hq, n))
+        for h in range(hq):
+            K = k[h // (hq // hkv)].double().numpy()
+            got = 0.0
+            for p in rows:
+                s = q[h, p].double().numpy() @ K[: p + 1].T / np.sqrt(128)
+                w = np.exp(s - s.max())
+                w /= w.sum()
+                sel = idx[h, p // bq, : cnt[h, p // bq]]
+                got += sum(w[blk * 128:(blk + 1) * 128].sum() for blk in sel)
+            assert abs(curves[h].recovery_at(b) - got / rows.size) < 1e-12, (b, h)
