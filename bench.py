@@ -87,12 +87,13 @@ def parse_args():
                    help="--impl reference: time the whole C1 layer (8K) this many times, best reported "
                         "(0 = skip)")
     p.add_argument("--gather", choices=["nccl", "p2p"], default="p2p",
-                   help="N>1 output reassembly: NCCL all-gather + reorder on a comm stream, or the "
+                   help="N>1 output reassembly: the C ABI's NCCL gather (shplb_gather_segments, one "
+                        "broadcast per output segment, no padding or reorder) on a comm stream, or the "
                         "fused gather (kernel 3 stores rows into every rank's buffer over NVLink)")
     p.add_argument("--policy", choices=["per_query_topk", "column_aggregate_topk"], default="per_query_topk",
                    help="selection policy (SelectionKind) of the profile and the layer: per (head, query "
                         "block) top-k blocks, or one kept block set per head (block granularity)")
-    p.add_argument("--placement", choices=["greedy", "split"], default="split",
+    p.add_argument("--placement", choices=["greedy", "split"], default="greedy",
                    help="N>1 headline plan: 'greedy' = the reference's whole-head greedy_assign (LPT on "
                         "budgets, bit-exact); 'split' = the sub-head balancer (shplb_plan_split). "
                         "All plans are timed and reported either way")
@@ -218,6 +219,23 @@ def init_single_rank_group(local):
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
 
 
+def make_hp_comm(world, rank, local):
+    """The library's NCCL communicator (shplb_nccl_comm_init) for the layer-output
+    gathers and barriers; its unique id travels over the torch.distributed
+    group (plumbing only). None in the one-device gloo debug mode."""
+    import torch
+    import paper_2603_10353_b200 as P
+    if DEBUG_GLOO:
+        return None
+    uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(P.NcclComm.unique_id()), dtype=torch.uint8))
+    if world > 1:
+        import torch.distributed as dist
+        dist.broadcast(uid, 0)
+    return P.NcclComm(local, world, rank, bytes(uid.cpu().numpy().tobytes()))
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -335,43 +353,36 @@ def time_stack(ctx, shards, steps, warmup, world, stream):
     return ms, st, launches, out
 
 
-def time_stack_gathered(ctx, shards, plans, steps, warmup, world, stream):
-    """The stack with every layer's outputs reassembled on every rank: layer l's
-    all-gather (NCCL over NVLink) + head reorder run on a communication stream
+def time_stack_gathered(ctx, shards, plans, hq, steps, warmup, world, stream, hp_comm):
+    """The stack with every layer's outputs reassembled on every rank through the
+    C ABI's NCCL gather (shplb_gather_segments: one ncclBroadcast per output
+    segment from its owner straight into every rank's [Hq, n, d] buffer, one
+    NCCL group per layer; no padding, no reorder) on a communication stream
     while layer l+1 computes; two output buffer sets alternate, the compute of
     layer l+2 waits for layer l's gather. Returns ms per layer (max over
     ranks) of the whole pipeline."""
     import torch
-    import torch.distributed as dist
 
     import paper_2603_10353_b200 as P
-    from paper_2603_10353_b200.head_parallel import apply_gather, gather_map
     n_l = len(shards)
     ref = next(ls.q for ls in shards if ls.heads)
     tail = tuple(ref.shape[1:])
-    maps = [gather_map(plans[l], world, tail[0], P.BLOCK_Q) for l in range(n_l)]
-    H = max(gm.hmax for gm in maps)
-    hq = max(gm.num_heads for gm in maps)
-    send = [torch.zeros((H,) + tail, dtype=ref.dtype, device=ref.device) for _ in range(2)]
-    recv = [torch.empty((world * H,) + tail, dtype=ref.dtype, device=ref.device) for _ in range(2)]
+    segs = [P.plan_segments(plans[l], world, hq, tail[0]) for l in range(n_l)]
+    hmax = max(max(len(ls.heads) for ls in shards), 1)
+    local = [torch.zeros((hmax,) + tail, dtype=ref.dtype, device=ref.device) for _ in range(2)]
     full = [torch.empty((hq,) + tail, dtype=ref.dtype, device=ref.device) for _ in range(2)]
     comm = torch.cuda.Stream()
     done = [torch.cuda.Event() for _ in range(2)]
     computed = [torch.cuda.Event() for _ in range(2)]
-    idx = [(torch.as_tensor(gm.src_slots, device=ref.device), torch.as_tensor(gm.dst_heads, device=ref.device))
-           for gm in maps]
 
     def one_step():
         for l, ls in enumerate(shards):
             b = l % 2
-            stream.wait_event(done[b])  # layer l-2's gather has released send/recv/full[b]
-            run_layer(ctx, ls, send[b][:len(ls.heads)], stream)
+            stream.wait_event(done[b])  # layer l-2's gather has released local/full[b]
+            run_layer(ctx, ls, local[b][:len(ls.heads)], stream)
             computed[b].record(stream)
             comm.wait_event(computed[b])
-            with torch.cuda.stream(comm):
-                hm = maps[l].hmax
-                dist.all_gather_into_tensor(recv[b][:world * hm], send[b][:hm])
-                apply_gather(recv[b][:world * hm], full[b], maps[l], *idx[l])
+            hp_comm.gather_segments(ctx, full[b], local[b], segs[l], stream=comm)
             done[b].record(comm)
         stream.wait_stream(comm)
 
@@ -392,13 +403,13 @@ def time_stack_gathered(ctx, shards, plans, steps, warmup, world, stream):
     return max(allgather_float(e0.elapsed_time(e1) / (steps * n_l), world))
 
 
-def time_stack_p2p(ctx, shards, hq, steps, warmup, world, rank, stream):
+def time_stack_p2p(ctx, shards, hq, steps, warmup, world, rank, stream, hp_comm=None):
     """The stack with the fused gather: kernel 3 of every rank stores each output
     row straight into every rank's full [Hq, n, d] buffer (CUDA IPC peer
     pointers over NVLink), so a layer needs no all-gather or reorder — only a
-    cross-rank barrier (a 1-element NCCL all-reduce on a communication stream)
-    before its buffer set is reused two layers later. ms per layer, max over
-    ranks."""
+    cross-rank barrier (shplb_comm_barrier: a 1-element all-reduce on the
+    library's NCCL communicator, on a communication stream) before its buffer
+    set is reused two layers later. ms per layer, max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -406,7 +417,6 @@ def time_stack_p2p(ctx, shards, hq, steps, warmup, world, rank, stream):
     ref = next(ls.q for ls in shards if ls.heads)
     po = PeerOutputs(hq, ref.shape[1], ref.shape[2], world, rank, ref.device, sets=2)
     comm = torch.cuda.Stream()
-    flag = torch.zeros(1, device=ref.device)
     done = [torch.cuda.Event() for _ in range(2)]
     computed = [torch.cuda.Event() for _ in range(2)]
 
@@ -424,9 +434,8 @@ def time_stack_p2p(ctx, shards, hq, steps, warmup, world, rank, stream):
                 continue
             computed[b].record(stream)
             comm.wait_event(computed[b])
-            with torch.cuda.stream(comm):
-                if world > 1:
-                    dist.all_reduce(flag)
+            if world > 1:
+                hp_comm.barrier(stream=comm)
             done[b].record(comm)
         stream.wait_stream(comm)
 
@@ -750,7 +759,9 @@ def budgets_desc(args):
 
 
 PLACEMENTS = {
-    "greedy": "greedy (LPT) whole-head plan (greedy_assign, bit-exact with the reference)",
+    "greedy": ("greedy (LPT) whole-head plan (greedy_assign, bit-exact with the reference); even head "
+               "parallelism (naive_even_hp), greedy on tile cost (greedy_tile_cost) and the sub-head "
+               "balancer (split_subhead) are timed alongside"),
     "split": ("sub-head balancer (shplb_plan_split): heads in index order with exact tile costs, cut "
               "McNaughton-style at query-block boundaries, at most D-1 heads split; the reference's "
               "whole-head greedy plan is timed alongside (greedy_whole_head)"),
@@ -817,8 +828,10 @@ def main():
             raise SystemExit(f"{args.assignment_json}: plan for {la.devices} devices / "
                              f"{la.device_of_head.size} heads, run has {world} / {args.q_heads}")
         plans_l["greedy"] = [la.device_of_head.astype(np.int32)] * L
+    hp_comm = make_hp_comm(world, rank, local) if (world > 1 or args.force_gather) else None
     if world > 1:
         plans_l["naive"] = [P.naive_assign(b, world) for b in budgets_l]
+        plans_l["greedy_tiles"] = [P.greedy_assign(P.tile_costs(b, n), world) for b in budgets_l]
         plans_l["split"] = [P.split_assign(b, world, n) for b in budgets_l]
     headline = args.placement if world > 1 else "greedy"  # at N = 1 every plan is the whole layer
     results = {}
@@ -851,17 +864,17 @@ def main():
             if args.gather == "p2p":
                 try:
                     res["ms_with_gather"] = time_stack_p2p(ctx, shards, hq, max(2, args.steps // 2), 1, world,
-                                                           rank, stream)
+                                                           rank, stream, hp_comm)
                     res["gather_kind"] = "p2p"
                 except P.ShplbError as e:  # IPC / peer access unavailable: NCCL all-gather instead
                     torch.cuda.synchronize()
                     res["gather_kind"] = f"nccl (fused p2p unavailable: {e})"
-                    res["ms_with_gather"] = time_stack_gathered(ctx, shards, plans, max(2, args.steps // 2),
-                                                                1, world, stream)
+                    res["ms_with_gather"] = time_stack_gathered(ctx, shards, plans, hq, max(2, args.steps // 2),
+                                                                1, world, stream, hp_comm)
             else:
                 res["gather_kind"] = "nccl"
-                res["ms_with_gather"] = time_stack_gathered(ctx, shards, plans, max(2, args.steps // 2),
-                                                            1, world, stream)
+                res["ms_with_gather"] = time_stack_gathered(ctx, shards, plans, hq, max(2, args.steps // 2),
+                                                            1, world, stream, hp_comm)
         if name == headline and not args.no_e2e:
             n_e2e = e2e_layer_budget(shards, args.e2e_layers or L, local_ranks=world)
             e2e_ms, h2d, d2h = time_e2e(ctx, shards[:n_e2e], max(2, args.steps // 2), 1, world, stream)
@@ -982,11 +995,19 @@ def main():
                                  "speedup_vs_even_hp": round(_vg(nv) / _vg(spl), 4),
                                  "plan": "sub-head balancer (shplb_plan_split), an extension "
                                          "beyond the reference's whole-head greedy_assign"}
-        line["gather"] = ("every layer's [Hq, n, d] output all-gathered (NCCL) and head-reordered on a "
+        gt = results["greedy_tiles"]
+        line["greedy_tile_cost"] = {"ms": round(_vg(gt), 3), "compute_only_ms": round(gt["ms"], 3),
+                                    "bubble": round(gt["bubble"], 4),
+                                    "per_rank_ms": [round(x, 3) for x in gt["per_rank_ms"]],
+                                    "speedup_vs_even_hp": round(_vg(nv) / _vg(gt), 4),
+                                    "plan": "greedy_assign on kernel 3's causal tile cost per head "
+                                            "(api.tile_costs) instead of budgets (SURVEY a11 extension)"}
+        line["gather"] = ("every layer's [Hq, n, d] output reassembled on every rank by shplb_gather_segments "
+                          "(one NCCL broadcast per output segment from its owner, one group per layer) on a "
                           "communication stream, overlapped with the next layer's compute"
                           if g.get("gather_kind", "nccl").startswith("nccl") else
                           "fused: kernel 3 stores every output row into every rank's [Hq, n, d] buffer over "
-                          "NVLink (CUDA IPC peer pointers); one NCCL barrier per layer on a comm stream")
+                          "NVLink (CUDA IPC peer pointers); one shplb_comm_barrier per layer on a comm stream")
         line["gather_kind"] = g.get("gather_kind")
         line["load_imbalance"] = round(g["load_imbalance"], 4)
     if dense_ms is not None:
@@ -996,7 +1017,7 @@ def main():
         line["per_rank_projection"] = {
             "what": ("layer 0: every rank's shard timed in turn on this GPU (CUDA events, median of 3); "
                      "barrier = max over ranks, bubble = 1 - mean/max (simulator.cpp:40-44); "
-                     "naive = even head parallelism, greedy = S-HPLB greedy_assign, split = sub-head "
+                     "naive = even head parallelism, greedy = S-HPLB greedy_assign, greedy_tiles = greedy_assign on tile cost, split = sub-head "
                      "balancer; gathers excluded"),
             "degrees": projection}
     line["cpu_baseline"] = cpu

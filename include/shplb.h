@@ -32,7 +32,8 @@ typedef enum {
     SHPLB_RUNTIME_ERROR = 2,    /* reference: std::runtime_error    */
     SHPLB_LOGIC_ERROR = 3,      /* reference: std::logic_error      */
     SHPLB_CUDA_ERROR = 4,       /* CUDA runtime / driver failure    */
-    SHPLB_NOT_SUPPORTED = 5     /* shape or policy the kernels do not implement */
+    SHPLB_NOT_SUPPORTED = 5,    /* shape or policy the kernels do not implement */
+    SHPLB_NCCL_ERROR = 6        /* NCCL failure (or libnccl.so.2 not loadable) */
 } shplb_status;
 
 /* Opaque per-device context (owns device workspace); see shplb_ctx_create. */
@@ -384,6 +385,64 @@ int shplb_layer_work(const shplb_layer_shape* shape, const int64_t* budgets_toke
  * block) tiles kernel 3 computed, counted from the selection (copies it to the
  * host; synchronises the device). FLOPs = 4*d*128*128*tiles. */
 int shplb_last_selection_work(const shplb_ctx* ctx, int64_t* tiles_out, double* flops_out);
+
+/* ======================================================================
+ * Head parallelism across ranks (one process per GPU)
+ *   reference: the paper's per-head outputs reassembled after the head-to-GPU
+ *   plan (Assignment::device_of_head, partitioner.hpp:15-21) over the per-head
+ *   fan-out of sparse_attention_all (attention.cpp:204-223)
+ * NCCL is resolved at run time (libnccl.so.2); failures -> SHPLB_NCCL_ERROR.
+ * A communicator handle (void*) wraps an ncclComm_t bound to one device.
+ * ====================================================================== */
+
+#define SHPLB_NCCL_UNIQUE_ID_BYTES 128
+
+/* ncclGetUniqueId on rank 0; the caller ships the bytes to every rank. */
+int shplb_nccl_get_unique_id(void* id_out, size_t id_bytes);
+/* ncclCommInitRank on `device` (collective over all nranks). */
+int shplb_nccl_comm_init(int device, int32_t nranks, int32_t rank, const void* id, size_t id_bytes,
+                         void** comm_out);
+int shplb_nccl_comm_destroy(void* comm);
+int shplb_nccl_comm_size(void* comm, int32_t* nranks, int32_t* rank);
+
+/* One output segment: rows [row_begin, row_end) of global q head `head`,
+ * computed by rank `owner` into its local output at local head `local_head`
+ * (the owner's layer-call output [h_owner][n][d]). */
+typedef struct {
+    int32_t head;
+    int32_t owner;
+    int32_t local_head;
+    int32_t reserved;
+    int64_t row_begin;
+    int64_t row_end;
+} shplb_out_segment;
+
+/* Reassemble a head-parallel layer on every rank: out [num_q_heads][n][d] bf16
+ * (device) receives every segment from its owner's `local` buffer (one
+ * ncclBroadcast per segment rooted at the owner, all in one NCCL group, async
+ * on `stream`; no staging, no reorder). Every rank passes the same segment
+ * list; together the segments must cover every (head, row) exactly once
+ * (InvalidArgument otherwise). A rank's own segments are copied from local to
+ * out (in place when local aliases out at those rows). Sub-head (split) plans
+ * pass one segment per (head, query-row range). */
+int shplb_gather_segments(shplb_ctx* ctx, void* comm, const shplb_out_segment* segments, int32_t n_segments,
+                          int32_t num_q_heads, int64_t seq_len, int32_t head_dim, const void* local, void* out,
+                          void* stream);
+
+/* The whole-head plan form: device_of_head [num_q_heads] (greedy_assign /
+ * naive_assign output, devices = ranks of the communicator, checked as
+ * Assignment::validate with its messages); rank r's local output holds its
+ * heads in ascending head order (shplb_sparse_attention_layer over the rank's
+ * heads with a kv map), so segment h = (h, device_of_head[h], index of h among
+ * that rank's heads, rows [0, n)). */
+int shplb_gather_heads(shplb_ctx* ctx, void* comm, int32_t num_q_heads, int64_t seq_len, int32_t head_dim,
+                       const int32_t* device_of_head, const void* local, void* out, void* stream);
+
+/* Cross-rank barrier on `stream` (a one-element ncclAllReduce): when it
+ * completes on a rank's stream, every rank's work queued before it has
+ * completed — the fence of the fused output gather (shape.out_peers), after
+ * which every peer's stores into this rank's output buffer are visible. */
+int shplb_comm_barrier(void* comm, void* stream);
 
 #ifdef __cplusplus
 }

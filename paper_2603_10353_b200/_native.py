@@ -30,6 +30,8 @@ EXPORTS = (
     "shplb_last_selection", "shplb_copy_last_selection",
     "shplb_layer_work", "shplb_last_selection_work",
     "shplb_ipc_handle", "shplb_ipc_open", "shplb_ipc_close",
+    "shplb_nccl_get_unique_id", "shplb_nccl_comm_init", "shplb_nccl_comm_destroy", "shplb_nccl_comm_size",
+    "shplb_gather_segments", "shplb_gather_heads", "shplb_comm_barrier",
 )
 
 SHPLB_OK = 0
@@ -38,6 +40,7 @@ SHPLB_RUNTIME_ERROR = 2
 SHPLB_LOGIC_ERROR = 3
 SHPLB_CUDA_ERROR = 4
 SHPLB_NOT_SUPPORTED = 5
+SHPLB_NCCL_ERROR = 6
 
 
 class ShplbError(RuntimeError):
@@ -64,12 +67,17 @@ class NotSupported(ShplbError, NotImplementedError):
     """A shape or policy the sm_100a kernels do not implement."""
 
 
+class NcclError(ShplbError):
+    """An NCCL failure (or libnccl.so.2 not loadable) in a multi-rank call."""
+
+
 _ERRORS = {
     SHPLB_INVALID_ARGUMENT: InvalidArgument,
     SHPLB_RUNTIME_ERROR: ShplbRuntimeError,
     SHPLB_LOGIC_ERROR: LogicError,
     SHPLB_CUDA_ERROR: CudaError,
     SHPLB_NOT_SUPPORTED: NotSupported,
+    SHPLB_NCCL_ERROR: NcclError,
 }
 
 
@@ -165,6 +173,13 @@ def lib() -> C.CDLL:
     L.shplb_ipc_handle.argtypes = [vp, vp, C.c_size_t]
     L.shplb_ipc_open.argtypes = [C.c_int, vp, C.c_size_t, P(vp)]
     L.shplb_ipc_close.argtypes = [C.c_int, vp]
+    L.shplb_nccl_get_unique_id.argtypes = [vp, C.c_size_t]
+    L.shplb_nccl_comm_init.argtypes = [C.c_int, i32, i32, vp, C.c_size_t, P(vp)]
+    L.shplb_nccl_comm_destroy.argtypes = [vp]
+    L.shplb_nccl_comm_size.argtypes = [vp, P(i32), P(i32)]
+    L.shplb_gather_segments.argtypes = [vp, vp, vp, i32, i32, i64, i32, vp, vp, vp]
+    L.shplb_gather_heads.argtypes = [vp, vp, i32, i64, i32, vp, vp, vp, vp]
+    L.shplb_comm_barrier.argtypes = [vp, vp]
     L.shplb_last_selection.argtypes = [vp, P(vp), P(vp), P(i64)]
     L.shplb_copy_last_selection.argtypes = [vp, vp, i64, vp, i64, vp]
     L.shplb_layer_work.argtypes = [P(LayerShape), vp, P(i64), P(f64)]

@@ -222,6 +222,23 @@ def split_assign(budgets, devices: int, seq_len: int, block_q: int = BLOCK_Q,
     return SplitPlan(dev[:k].copy(), hd[:k].copy(), qb0[:k].copy(), qb1[:k].copy(), loads)
 
 
+def tile_costs(budgets, seq_len: int, block_q: int = BLOCK_Q, causal: bool = True) -> np.ndarray:
+    """Per-head cost in kernel 3's 128x128 tiles: sum over query blocks of
+    min(ceil(b_h/128), visible key blocks) x query halves holding rows — the
+    work the layer call does for the head (shplb_layer_work per head). Passed to
+    greedy_assign instead of the budgets it is the documented extension of
+    SURVEY a11 (the same LPT, weighted by causal tile cost rather than tokens)."""
+    b = np.asarray(budgets, np.int64)
+    nkb = (seq_len + BLOCK - 1) // BLOCK
+    nqb = (seq_len + block_q - 1) // block_q
+    qb = np.arange(nqb)
+    last = np.minimum((qb + 1) * block_q, seq_len) - 1
+    vis = np.minimum(last // BLOCK + 1, nkb) if causal else np.full(nqb, nkb)
+    halves = np.array([sum(1 for hf in range(block_q // BLOCK) if q * block_q + hf * BLOCK < seq_len) for q in qb])
+    kb = np.minimum((b + BLOCK - 1) // BLOCK, nkb)
+    return (np.minimum(kb[:, None], vis[None, :]) * halves[None, :]).sum(1).astype(np.int64)
+
+
 @dataclass
 class SimulationResult:
     """simulator.hpp:20-25."""
@@ -537,3 +554,92 @@ def layer_work(num_q_heads, num_kv_heads, seq_len, budgets_tokens, causal=True, 
     t, f = C.c_int64(), C.c_double()
     check(lib().shplb_layer_work(C.byref(sh), _ptr(b), C.byref(t), C.byref(f)))
     return int(t.value), float(f.value)
+
+
+# ---------------------------------------------------------------------------
+# Head parallelism across ranks: NCCL communicator + output reassembly
+# (shplb_nccl_*, shplb_gather_segments / shplb_gather_heads, shplb_comm_barrier)
+# ---------------------------------------------------------------------------
+
+class OutSegment(C.Structure):
+    """shplb_out_segment: rows [row_begin, row_end) of global head `head`, computed
+    by rank `owner` at its local head index `local_head`."""
+    _fields_ = [("head", C.c_int32), ("owner", C.c_int32), ("local_head", C.c_int32),
+                ("reserved", C.c_int32), ("row_begin", C.c_int64), ("row_end", C.c_int64)]
+
+
+def plan_segments(plan, world: int, num_heads: int, seq_len: int, block_q: int = BLOCK_Q):
+    """Output segments of a whole-head plan (device_of_head) or a sub-head plan
+    (split_assign result): every rank's heads in ascending order (its local
+    layout), each with the rows it computes."""
+    segs = []
+    if isinstance(plan, SplitPlan):  # sub-head plan
+        for r in range(world):
+            sel = [i for i in range(len(plan.device)) if int(plan.device[i]) == r]
+            sel.sort(key=lambda i: int(plan.head[i]))
+            for li, i in enumerate(sel):
+                r0 = int(plan.qb_begin[i]) * block_q
+                r1 = min(int(plan.qb_end[i]) * block_q, seq_len)
+                if r1 > r0:
+                    segs.append((int(plan.head[i]), r, li, r0, r1))
+    else:
+        dev = np.asarray(plan)
+        for r in range(world):
+            for li, h in enumerate(np.nonzero(dev == r)[0].tolist()):
+                segs.append((h, r, li, 0, seq_len))
+    arr = (OutSegment * len(segs))()
+    for i, (h, o, li, r0, r1) in enumerate(segs):
+        arr[i] = OutSegment(h, o, li, 0, r0, r1)
+    return arr
+
+
+class NcclComm:
+    """An NCCL communicator of the library (shplb_nccl_comm_init) for the
+    head-parallel reassembly and barrier. Rank 0 makes the unique id
+    (NcclComm.unique_id()) and the host ships it to every rank."""
+
+    def __init__(self, device: int, nranks: int, rank: int, unique_id: bytes):
+        self.device, self.nranks, self.rank = device, nranks, rank
+        self._h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        check(lib().shplb_nccl_comm_init(device, nranks, rank, buf, 128, C.byref(self._h)))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().shplb_nccl_get_unique_id(buf, 128))
+        return buf.raw
+
+    def gather_segments(self, ctx, out, local, segments, stream=None):
+        """out [Hq, n, d] bf16 on every rank <- every segment from its owner's local buffer."""
+        hq, n, d = out.shape
+        check(lib().shplb_gather_segments(ctx._h, self._h, segments, len(segments), hq, n, d,
+                                          C.c_void_p(local.data_ptr() if local is not None else 0),
+                                          C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
+    def gather_heads(self, ctx, out, local, device_of_head, stream=None):
+        """Whole-head plan form (shplb_gather_heads)."""
+        hq, n, d = out.shape
+        dev = np.ascontiguousarray(device_of_head, np.int32)
+        if dev.size != hq:
+            from ._native import InvalidArgument
+            raise InvalidArgument(f"assignment covers {dev.size} heads but {hq} budgets were given")
+        check(lib().shplb_gather_heads(ctx._h, self._h, hq, n, d, _ptr(dev),
+                                       C.c_void_p(local.data_ptr() if local is not None else 0),
+                                       C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
+    def barrier(self, stream=None):
+        check(lib().shplb_comm_barrier(self._h, _stream_ptr(stream)))
+
+    def close(self):
+        if self._h:
+            check(lib().shplb_nccl_comm_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -24,6 +24,9 @@ struct CudaError : std::runtime_error {
 struct NotSupported : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+struct NcclError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 
 void set_last_error(const std::string& msg);
 void clear_last_error();
@@ -44,6 +47,9 @@ int guarded(F&& f) {
     } catch (const CudaError& e) {
         set_last_error(e.what());
         return SHPLB_CUDA_ERROR;
+    } catch (const NcclError& e) {
+        set_last_error(e.what());
+        return SHPLB_NCCL_ERROR;
     } catch (const std::invalid_argument& e) {
         set_last_error(e.what());
         return SHPLB_INVALID_ARGUMENT;

@@ -123,6 +123,13 @@ def measured_sweep(ctx, layers: dict, degrees, allocator: str = "maxmin", steps:
                                  res_g.bubble_fraction, imb_g,
                                  1.0 if res_g.barrier_latency == 0 else res_n.barrier_latency / res_g.barrier_latency,
                                  per_g))
+            # greedy_assign weighted by kernel 3's causal tile cost (api.tile_costs)
+            gt = api.greedy_assign(api.tile_costs(budgets, q.shape[1]), degree)
+            per_t, res_t = measured_barrier(ctx, q, k, v, budgets, gt, degree, steps)
+            rows.append(SweepRow(degree, length, allocator, "greedy_tiles", res_t.barrier_latency,
+                                 res_t.bubble_fraction, api.imbalance(budgets, gt, degree).imbalance,
+                                 1.0 if res_t.barrier_latency == 0 else res_n.barrier_latency / res_t.barrier_latency,
+                                 per_t))
             if include_split:
                 per_s, res_s, sp = measured_split_barrier(ctx, q, k, v, budgets, degree, steps)
                 rows.append(SweepRow(degree, length, allocator, "split", res_s.barrier_latency,

@@ -112,3 +112,32 @@ def test_fused_gather_setup_failure_is_collective():
     for r in range(2):
         assert results[r] == ([True, False], ["rank 1: open failed"])
         assert results[("sum", r)] == 3.0
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_plan_segments_match_rank_shards(world):
+    """The segment list handed to shplb_gather_segments / shplb_gather_heads
+    (api.plan_segments) names, for every rank, exactly the heads and rows that
+    rank's shard computes, at the local index its layer-call output holds them."""
+    import paper_2603_10353_b200 as P
+    from paper_2603_10353_b200.head_parallel import rank_segments, rank_shard
+    rng = np.random.default_rng(world)
+    hq, n, group = 28, 5000, 7
+    budgets = rng.choice([128, 1024, 2048, 5000], size=hq).astype(np.int64)
+    for plan in (P.greedy_assign(budgets, world), P.naive_assign(budgets, world), P.split_assign(budgets, world, n)):
+        segs = list(P.plan_segments(plan, world, hq, n))
+        rows = np.zeros((hq, n), np.int32)
+        for s in segs:
+            rows[s.head, s.row_begin:s.row_end] += 1
+        assert (rows == 1).all(), "every output row exactly once"
+        for r in range(world):
+            mine = [s for s in segs if s.owner == r]
+            if isinstance(plan, P.api.SplitPlan):
+                sh = rank_segments(plan, r, group, budgets)
+                want = [(h, i, min(int(a) * 256, n), min(int(b) * 256, n))
+                        for i, (h, (a, b)) in enumerate(zip(sh.heads, sh.q_block_range))]
+                want = [w for w in want if w[3] > w[2]]
+            else:
+                sh = rank_shard(plan, r, group, budgets)
+                want = [(h, i, 0, n) for i, h in enumerate(sh.heads)]
+            assert [(s.head, s.local_head, s.row_begin, s.row_end) for s in mine] == want
