@@ -524,33 +524,42 @@ def time_e2e(ctx, shards, steps, warmup, world, stream):
 # reference CPU path (oracle/_ref = the reference library, unmodified)
 # ---------------------------------------------------------------------------
 
-def cpu_reference_sample(q, k, v, budgets, group, target_s, rng_seed=0):
+class RefKV:
+    """fp64 K / V of every kv head (the reference's HeadData holds fp64), built
+    once and shared by every sample step (the bf16 -> fp64 conversion is
+    harness work, not the reference's)."""
+
+    def __init__(self, k, v):
+        from paper_2603_10353_b200.workload import bf16_bits
+        self.k = [_ref_f64(bf16_bits(k[g])) for g in range(k.shape[0])]
+        self.v = [_ref_f64(bf16_bits(v[g])) for g in range(v.shape[0])]
+
+
+def cpu_reference_sample(q, k, v, budgets, group, target_s, rng_seed=0, kv=None, rows_per_call=None):
     """Time headbal::sparse_attention (PerQueryTopK, fp64, OpenMP over rows) on
     a bounded sample of (head, query-row) pairs and extrapolate to ms/layer.
     Per-row cost is O(n_k*d) whatever the budget or causal mask (scores are
     computed before masking, attention.cpp:22-30), so the sample rows are run
-    without the mask and the time scales linearly with the row count."""
+    without the mask and the time scales linearly with the row count. Each
+    call takes 16 rows per thread so OpenMP's fixed cost per call stays small
+    against the rows (checked against a whole measured C1 layer in the
+    reference arm's c1_full_layer)."""
     from oracle import oracle as O
     from paper_2603_10353_b200.workload import bf16_bits
     hq, n, d = q.shape
     threads = O.ref.max_threads()
-    rows_per_call = 4 * max(threads, 4)
+    rows_per_call = rows_per_call or min(n, 16 * max(threads, 4))
+    kv = kv or RefKV(k, v)
     rng = np.random.default_rng(rng_seed)
     heads = list(rng.permutation(hq))
-    kv_cache = {}
     per_row = []  # seconds per (head,row) for each call
     spent = 0.0
     calls = 0
     for h in heads:
         g = h // group
-        if g not in kv_cache:
-            kv_cache.clear()
-            kv_cache[g] = (bf16_bits(k[g]).astype(np.uint32) << 16,
-                           bf16_bits(v[g]).astype(np.uint32) << 16)
-        kk, vv = (a.view(np.float32).astype(np.float64) for a in kv_cache[g])
         rows = np.sort(rng.choice(n, rows_per_call, replace=False))
-        qq = (bf16_bits(q[h][rows]).astype(np.uint32) << 16).view(np.float32).astype(np.float64)
-        _, sec = O.ref.sparse_attention_timed(qq, kk, vv, int(budgets[h]), causal=False)
+        qq = _ref_f64(bf16_bits(q[h][rows]))
+        _, sec = O.ref.sparse_attention_timed(qq, kv.k[g], kv.v[g], int(budgets[h]), causal=False)
         per_row.append(sec / rows_per_call)
         spent += sec
         calls += 1
@@ -719,9 +728,10 @@ def run_reference(args):
     per_step = max(1.0, args.cpu_seconds / max(1, args.steps))
     vals, walls = [], []
     threads, sample = 1, ""
+    kv = RefKV(k, v)
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        ms, threads, sample = cpu_reference_sample(q, k, v, budgets, group, per_step, rng_seed=i)
+        ms, threads, sample = cpu_reference_sample(q, k, v, budgets, group, per_step, rng_seed=i, kv=kv)
         if i >= args.warmup:
             vals.append(ms)
             walls.append((time.perf_counter() - t0) * 1e3)

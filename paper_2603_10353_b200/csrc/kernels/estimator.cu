@@ -15,6 +15,9 @@
 // is a warp-level radix (bisection) select on the order-preserving uint32
 // image of each score; both work out of shared memory / L2.
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -308,8 +311,7 @@ void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int6
                          cudaStream_t s) {
     const int64_t nqb = (n + bq - 1) / bq, nkb = (n + kBlock - 1) / kBlock;
     const size_t smem = score_select_smem(nkb);
-    cudaFuncSetAttribute(score_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    set_max_dynamic_smem(reinterpret_cast<const void*>(score_select_kernel), static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>((nqb + kRowsPerCta - 1) / kRowsPerCta), hq);
     score_select_kernel<<<grid, kSelThreads, smem, s>>>(qp, kp, hq, hkv, n, nqb, nkb, bq, causal ? 1 : 0,
                                                         scale, ht, kmax, scores_out, select ? 1 : 0,
@@ -468,6 +470,17 @@ void launch_dense_selection(int32_t* idx, int32_t* cnt, int hq, int64_t n, int b
 
 void launch_check_finite(const void* x, int64_t count, int32_t* flag, cudaStream_t s) {
     check_finite_kernel<<<148 * 8, 256, 0, s>>>(static_cast<const uint16_t*>(x), count, flag);
+}
+
+void set_max_dynamic_smem(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> set_to;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    int& cur = set_to[{func, dev}];
+    if (bytes > cur && cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess)
+        cur = bytes;
 }
 
 }  // namespace shplb::kern

@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
 }  // namespace
 
 cudaError_t launch_fa_pair(const FaParams& p, int num_tiles, cudaStream_t s) {
-    cudaFuncSetAttribute(fa_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPSmemTotal));
+    set_max_dynamic_smem(reinterpret_cast<const void*>(fa_pair_kernel), static_cast<int>(kPSmemTotal));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * static_cast<unsigned>(num_tiles));
     cfg.blockDim = dim3(kPThreads);

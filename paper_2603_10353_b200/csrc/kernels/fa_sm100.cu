@@ -548,15 +548,11 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
 }  // namespace
 
 void launch_fa(const FaParams& p, int num_tiles, bool dual, cudaStream_t s) {
-    // Per launch (not cached in a static): the attribute belongs to the current
-    // device's context, and the call costs microseconds against a long kernel.
     if (dual) {
-        cudaFuncSetAttribute(fa_sparse_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kSmemTotal));
+        set_max_dynamic_smem(reinterpret_cast<const void*>(fa_sparse_kernel<true>), static_cast<int>(kSmemTotal));
         fa_sparse_kernel<true><<<num_tiles, kThreads, kSmemTotal, s>>>(p);
     } else {
-        cudaFuncSetAttribute(fa_sparse_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kSmemTotal));
+        set_max_dynamic_smem(reinterpret_cast<const void*>(fa_sparse_kernel<false>), static_cast<int>(kSmemTotal));
         fa_sparse_kernel<false><<<num_tiles, kThreads, kSmemTotal, s>>>(p);
     }
 }

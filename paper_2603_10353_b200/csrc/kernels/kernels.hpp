@@ -111,6 +111,11 @@ size_t colagg_work_floats(int hq, int64_t n, int bq);
 // (tail -1), cnt [hq][nqb] = visible count.
 void launch_dense_selection(int32_t* idx, int32_t* cnt, int hq, int64_t n, int bq, bool causal, cudaStream_t s);
 
+// cudaFuncSetAttribute(func, MaxDynamicSharedMemorySize, bytes) once per
+// (kernel, device, larger size): the attribute belongs to the device's context,
+// so it is set the first time a kernel runs on a device (or needs more).
+void set_max_dynamic_smem(const void* func, int bytes);
+
 // Validation: sets *flag to 1 if any element of x (count elements, bf16) is not finite.
 void launch_check_finite(const void* x, int64_t count, int32_t* flag, cudaStream_t s);
 

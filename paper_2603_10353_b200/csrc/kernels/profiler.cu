@@ -396,7 +396,7 @@ void launch_profile_block(const double* scores, const float* bscores, const int6
     pow2 = max(pow2, 2);
     const size_t smem = static_cast<size_t>(std::max(pow2, kBlockProfThreads)) * sizeof(uint64_t) +
                         static_cast<size_t>(pow2) * sizeof(double);
-    cudaFuncSetAttribute(profile_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    set_max_dynamic_smem(reinterpret_cast<const void*>(profile_block_kernel), static_cast<int>(smem));
     profile_block_kernel<<<static_cast<unsigned>(static_cast<int64_t>(heads) * n_rows), kBlockProfThreads, smem, s>>>(
         scores, bscores, rows, h0, n_rows, n, nqb, nkb, bq, causal ? 1 : 0, pow2, grid, n_grid, mass);
 }
@@ -404,9 +404,7 @@ void launch_profile_block(const double* scores, const float* bscores, const int6
 void launch_profile_scores(const void* q_rows, const void* k, int hq, int hkv, int64_t n_rows,
                            int64_t n_k, double scale, double* scores, cudaStream_t s) {
     constexpr size_t smem = sizeof(double) * (kHeadDim * (kProfKeys + 1) + kProfRows * kHeadDim);
-    // Per launch (not cached in a static): the attribute belongs to the current
-    // device's context, and the call costs microseconds against a long kernel.
-    cudaFuncSetAttribute(profile_scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    set_max_dynamic_smem(reinterpret_cast<const void*>(profile_scores_kernel), static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>((n_k + kProfKeys - 1) / kProfKeys), static_cast<unsigned>(hkv));
     profile_scores_kernel<<<grid, kProfThreads, smem, s>>>(static_cast<const __nv_bfloat16*>(q_rows),
                                                         static_cast<const __nv_bfloat16*>(k), hq, hkv, n_rows,

@@ -19,6 +19,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "common.hpp"
 #include "kernels/kernels.hpp"
@@ -104,6 +105,16 @@ CUtensorMap make_tmap(const void* base, int64_t heads, int64_t n, uint32_t box_r
 }
 
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// NVTX range over a host-side stage (enqueue of K1 / K2 / K3, a host-buffer
+// chunk, a profile): visible in nsys / ncu --nvtx timelines. NVTX v3 is
+// header-only and a no-op without an attached tool.
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
 
 // Key blocks (of 128 keys) visible to query block qb of bq rows.
 int64_t visible_blocks(int64_t qb, int64_t n, int64_t bq, bool causal) {
@@ -257,14 +268,26 @@ struct shplb_ctx {
     int64_t last_rows = 0;  // Hq * nqb of the last layer call
     int64_t last_n = 0, last_nqb = 0;
     int32_t last_bq = 0, last_causal = 0;
-    // Kernel-3 work lists, one per (seq_len, causal, blocks-per-head) seen.
-    // Never overwritten, so an in-flight launch never sees its list change.
+    // Kernel-3 work lists, one per (seq_len, causal, blocks-per-head, ranges,
+    // kv map) seen, least recently used evicted past work_list_cap. Device
+    // memory comes from the stream-ordered allocator: a list is uploaded on
+    // the stream of the call that builds it and freed on the stream of the call
+    // that evicts it after that stream waited for the list's last launch
+    // (last_use), so neither side synchronises the host and an in-flight
+    // launch never sees its list change or disappear.
     struct WorkList {
-        int32_t* tiles = nullptr;
+        int32_t* tiles = nullptr;        // device (stream-ordered allocation)
+        int32_t* host = nullptr;         // pinned source of the upload
         int num_tiles = 0;
+        uint64_t stamp = 0;              // LRU clock of the last call that used it
+        cudaEvent_t last_use = nullptr;  // recorded after that call's kernel-3 launch
     };
     std::map<std::vector<int64_t>, WorkList> work_lists;
-    const WorkList* current = nullptr;
+    // Pinned sources of evicted lists, freed once their last launch completed.
+    std::vector<std::pair<int32_t*, cudaEvent_t>> host_graveyard;
+    WorkList* current = nullptr;
+    uint64_t lru_clock = 0;
+    size_t work_list_cap = 256;
     // Stage timing: 4 events per recorded layer call (before k1, after k1,
     // after k2, after k3); `timed_calls` sets in use since the last read.
     bool timing = false;
@@ -349,9 +372,13 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
     grow(ctx->qp, ctx->qp_bytes, sizeof(float) * s->num_q_heads * nqb * kern::kHeadDim);
     grow(ctx->kp, ctx->kp_bytes, sizeof(float) * s->num_kv_heads * nkb * kern::kHeadDim);
     if (select) mark(ctx, 0, st);
-    kern::launch_pool(q, s->num_q_heads, s->seq_len, s->block_q, ctx->qp, st);
-    kern::launch_pool(k, s->num_kv_heads, s->seq_len, kern::kBlock, ctx->kp, st);
+    {
+        Nvtx r("shplb.k1_pool");
+        kern::launch_pool(q, s->num_q_heads, s->seq_len, s->block_q, ctx->qp, st);
+        kern::launch_pool(k, s->num_kv_heads, s->seq_len, kern::kBlock, ctx->kp, st);
+    }
     if (select) mark(ctx, 1, st);
+    Nvtx r2("shplb.k2_score_select");
     const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(s->head_dim)));
     if (select && s->kind == SHPLB_COLUMN_AGGREGATE_TOPK) {
         // One kept set per head from the full score matrix (attention.cpp:136-148).
@@ -410,7 +437,8 @@ int tile_order_mode() {
 // heaviest first inside a group (tile_order_mode), so the hardware block
 // scheduler hands out long tiles before short ones while the CTAs in flight
 // share K/V in L2.
-void build_tiles(shplb_ctx* ctx, const shplb_layer_shape* s, const std::vector<int32_t>& kblocks) {
+void build_tiles(shplb_ctx* ctx, const shplb_layer_shape* s, const std::vector<int32_t>& kblocks,
+                 cudaStream_t st) {
     const int64_t nqb = cdiv(s->seq_len, s->block_q);
     const bool dual = dual_mode(s);
     std::vector<int64_t> key = {s->seq_len, s->causal, s->block_q, s->num_q_heads, dual ? 1 : 0};
@@ -420,7 +448,33 @@ void build_tiles(shplb_ctx* ctx, const shplb_layer_shape* s, const std::vector<i
     auto it = ctx->work_lists.find(key);
     if (it != ctx->work_lists.end()) {
         ctx->current = &it->second;
+        ctx->current->stamp = ++ctx->lru_clock;
         return;
+    }
+    // Reap pinned sources whose lists' last launches have completed.
+    for (size_t i = 0; i < ctx->host_graveyard.size();) {
+        auto& gy = ctx->host_graveyard[i];
+        if (cudaEventQuery(gy.second) == cudaSuccess) {
+            cudaFreeHost(gy.first);
+            cudaEventDestroy(gy.second);
+            gy = ctx->host_graveyard.back();
+            ctx->host_graveyard.pop_back();
+        } else {
+            ++i;
+        }
+    }
+    // Evict the least recently used list (stream-ordered after its last launch).
+    while (ctx->work_lists.size() >= ctx->work_list_cap) {
+        auto lru = ctx->work_lists.begin();
+        for (auto e = ctx->work_lists.begin(); e != ctx->work_lists.end(); ++e)
+            if (e->second.stamp < lru->second.stamp) lru = e;
+        SHPLB_CUDA(cudaStreamWaitEvent(st, lru->second.last_use, 0));
+        if (lru->second.tiles) SHPLB_CUDA(cudaFreeAsync(lru->second.tiles, st));
+        if (lru->second.host)
+            ctx->host_graveyard.push_back({lru->second.host, lru->second.last_use});
+        else
+            SHPLB_CUDA(cudaEventDestroy(lru->second.last_use));
+        ctx->work_lists.erase(lru);
     }
     std::vector<int32_t> tiles;
     std::vector<int32_t> work;
@@ -475,9 +529,16 @@ void build_tiles(shplb_ctx* ctx, const shplb_layer_shape* s, const std::vector<i
     std::vector<int32_t> sorted(tiles.size());
     for (size_t i = 0; i < order.size(); ++i) sorted[i] = tiles[order[i]];
     shplb_ctx::WorkList wl;
-    SHPLB_CUDA(cudaMalloc(&wl.tiles, sizeof(int32_t) * sorted.size()));
-    SHPLB_CUDA(cudaMemcpy(wl.tiles, sorted.data(), sizeof(int32_t) * sorted.size(), cudaMemcpyHostToDevice));
     wl.num_tiles = static_cast<int>(sorted.size());
+    SHPLB_CUDA(cudaEventCreateWithFlags(&wl.last_use, cudaEventDisableTiming));
+    if (!sorted.empty()) {
+        const size_t bytes = sizeof(int32_t) * sorted.size();
+        SHPLB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&wl.host), bytes));
+        std::memcpy(wl.host, sorted.data(), bytes);
+        SHPLB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&wl.tiles), bytes, st));
+        SHPLB_CUDA(cudaMemcpyAsync(wl.tiles, wl.host, bytes, cudaMemcpyHostToDevice, st));  // pinned: truly async
+    }
+    wl.stamp = ++ctx->lru_clock;
     ctx->current = &(ctx->work_lists[key] = wl);
 }
 
@@ -486,6 +547,7 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
             cudaStream_t st) {
     if (kmax > kern::kMaxSelected)
         throw NotSupported("more than " + std::to_string(kern::kMaxSelected) + " key blocks per query block");
+    Nvtx r("shplb.k3_sparse_fa");
     kern::FaParams p;
     std::memset(&p, 0, sizeof p);
     p.tm_q = make_tmap(q, s->num_q_heads, s->seq_len);
@@ -518,6 +580,7 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
             kern::launch_fa(p, ctx->current->num_tiles, dual_mode(s), st);
     }
     check_launch(ctx);
+    SHPLB_CUDA(cudaEventRecord(ctx->current->last_use, st));
 }
 
 }  // namespace
@@ -545,6 +608,7 @@ int shplb_ctx_create(int device, shplb_ctx** ctx_out) {
         DeviceGuard g(device);
         auto* ctx = new shplb_ctx();
         ctx->device = device;
+        if (const char* e = std::getenv("SHPLB_WORKLIST_CACHE")) ctx->work_list_cap = std::max(1, std::atoi(e));
         SHPLB_CUDA(cudaMalloc(&ctx->flag, 4 * sizeof(int32_t)));
         *ctx_out = ctx;
     });
@@ -558,7 +622,16 @@ int shplb_ctx_destroy(shplb_ctx* ctx) {
         cudaFree(ctx->kp);
         cudaFree(ctx->idx);
         cudaFree(ctx->cnt);
-        for (auto& kv : ctx->work_lists) cudaFree(kv.second.tiles);
+        cudaDeviceSynchronize();  // stream-ordered frees below must not overtake in-flight launches
+        for (auto& kv : ctx->work_lists) {
+            if (kv.second.tiles) cudaFree(kv.second.tiles);
+            if (kv.second.host) cudaFreeHost(kv.second.host);
+            if (kv.second.last_use) cudaEventDestroy(kv.second.last_use);
+        }
+        for (auto& gy : ctx->host_graveyard) {
+            cudaFreeHost(gy.first);
+            cudaEventDestroy(gy.second);
+        }
         for (cudaEvent_t e : ctx->events) cudaEventDestroy(e);
         cudaFree(ctx->flag);
         cudaFree(ctx->host_io);
@@ -682,7 +755,7 @@ int shplb_block_sparse_attention(shplb_ctx* ctx, const shplb_layer_shape* shape,
         if (shape->validate) validate_inputs(ctx, shape, q, k, v, st);
         // Without budgets the work list orders tiles by causal visibility only.
         std::vector<int32_t> kbl(static_cast<size_t>(shape->num_q_heads), static_cast<int32_t>(kmax));
-        build_tiles(ctx, shape, kbl);
+        build_tiles(ctx, shape, kbl, st);
         run_fa(ctx, shape, q, k, v, idx, cnt, kmax, out, st);
     });
 }
@@ -696,6 +769,7 @@ void sparse_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
                   const void* v, const int64_t* budgets_tokens, void* out, cudaStream_t st,
                   int64_t head_off, int64_t kmax_stride) {
     require(ctx != nullptr, "ctx is null");
+    Nvtx r("shplb.sparse_attention_layer");
     check_shape(shape);
     check_ptr(q, "q");
     check_ptr(k, "k");
@@ -718,7 +792,7 @@ void sparse_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const void* q,
     }
     int32_t* idx = ctx->idx + head_off * nqb * kmax;
     int32_t* cnt = ctx->cnt + head_off * nqb;
-    build_tiles(ctx, shape, kbl);
+    build_tiles(ctx, shape, kbl, st);
     pool_and_score(ctx, shape, q, k, kb, kmax, nullptr, true, idx, cnt, st);
     run_fa(ctx, shape, q, k, v, idx, cnt, kmax, out, st);
     mark(ctx, 3, st);
@@ -764,7 +838,7 @@ int shplb_dense_attention_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, 
             ctx->dense_key = key;
         }
         build_tiles(ctx, shape, std::vector<int32_t>(static_cast<size_t>(shape->num_q_heads),
-                                                     static_cast<int32_t>(nkb)));
+                                                     static_cast<int32_t>(nkb)), st);
         mark(ctx, 0, st);
         mark(ctx, 1, st);
         mark(ctx, 2, st);
@@ -890,6 +964,7 @@ int host_layer(shplb_ctx* ctx, const shplb_layer_shape* shape, const uint16_t* q
             const int32_t g0 = monotone ? hkv * c / chunks : 0, g1 = monotone ? hkv * (c + 1) / chunks : hkv;
             const int32_t h0 = monotone ? q_begin(g0) : 0, h1 = monotone ? q_begin(g1) : hq;
             if (h1 == h0) continue;  // kv heads no q head reads: nothing to compute or copy
+            Nvtx rc("shplb.host_chunk");
             std::vector<int32_t> sub(static_cast<size_t>(h1 - h0));
             for (int32_t h = h0; h < h1; ++h) sub[h - h0] = map.kv[h] - g0;
             cudaEvent_t in_done = ctx->chunk_events[1 + 3 * c], comp_done = ctx->chunk_events[2 + 3 * c];

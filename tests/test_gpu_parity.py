@@ -5,7 +5,7 @@
   on fp32 scores computed in the same fixed order on both sides.
 * Kernel 3 outputs must match the fp64 oracle on the same kept sets within
   the bf16 tolerance of tests/tolerance.py: max-abs <= 2e-2 and mean-rel <=
-  1.6 x the bf16 rounding floor of the compared reference rows (the floor is
+  2 x the bf16 rounding floor of the compared reference rows (the floor is
   ~1.4e-3, so the north_star's 1e-3 example is below what any bf16 output can
   reach; the gate is derived per comparison instead).
 """
@@ -443,3 +443,27 @@ def test_cta_pair_kernel_variant():
                        cwd=root, env=dict(os.environ, SHPLB_K3="pair"), capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_work_list_cache_eviction(monkeypatch):
+    """Kernel-3 work lists are LRU-evicted (SHPLB_WORKLIST_CACHE entries) with
+    stream-ordered frees: cycling more distinct budget tables than the cache
+    holds, asynchronously on one stream, gives the same outputs as a context
+    that never evicts."""
+    monkeypatch.setenv("SHPLB_WORKLIST_CACHE", "2")
+    small = P.Context(0)
+    monkeypatch.delenv("SHPLB_WORKLIST_CACHE")
+    big = P.Context(0)
+    q, k, v = (t.cuda() for t in make_layer(LayerSpec(num_q_heads=4, num_kv_heads=2, seq_len=1536, seed=8), "cpu"))
+    tables = [np.array([128 * (1 + (i + h) % 5) for h in range(4)], np.int64) for i in range(7)]
+    stream = torch.cuda.Stream()
+    want = [big.sparse_attention_layer(q, k, v, b).clone() for b in tables]
+    outs = []
+    for rep in range(3):
+        for b in tables:
+            outs.append(small.sparse_attention_layer(q, k, v, b, stream=stream))
+    stream.synchronize()
+    for i, o in enumerate(outs):
+        assert torch.equal(o, want[i % len(tables)]), i
+    small.close()
+    big.close()
