@@ -179,9 +179,13 @@ __global__ void __launch_bounds__(kSelThreads)
     float* S = Ks + kChunk * kPad;        // [16 rows][nkb_pad]
     const int64_t nkb_pad = (nkb + 3) & ~int64_t(3);
 
-    const int h = blockIdx.y;
+    // Grid (heads, row chunks): the hardware hands out CTAs head-fastest, and
+    // chunk y = 0 is the LAST chunk of query blocks, so under the causal mask
+    // the heaviest chunks (most visible key blocks) of every head go first and
+    // the launch tail is made of the lightest ones (LPT order).
+    const int h = blockIdx.x;
     const int g = ht.kv[h];
-    const int64_t qb0 = static_cast<int64_t>(blockIdx.x) * kRowsPerCta;
+    const int64_t qb0 = static_cast<int64_t>(gridDim.y - 1 - blockIdx.y) * kRowsPerCta;
     const int rows = static_cast<int>(min(static_cast<int64_t>(kRowsPerCta), nqb - qb0));
     const int tid = threadIdx.x;
 
@@ -312,7 +316,7 @@ void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int6
     const int64_t nqb = (n + bq - 1) / bq, nkb = (n + kBlock - 1) / kBlock;
     const size_t smem = score_select_smem(nkb);
     set_max_dynamic_smem(reinterpret_cast<const void*>(score_select_kernel), static_cast<int>(smem));
-    const dim3 grid(static_cast<unsigned>((nqb + kRowsPerCta - 1) / kRowsPerCta), hq);
+    const dim3 grid(static_cast<unsigned>(hq), static_cast<unsigned>((nqb + kRowsPerCta - 1) / kRowsPerCta));
     score_select_kernel<<<grid, kSelThreads, smem, s>>>(qp, kp, hq, hkv, n, nqb, nkb, bq, causal ? 1 : 0,
                                                         scale, ht, kmax, scores_out, select ? 1 : 0,
                                                         idx, cnt);

@@ -404,16 +404,6 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
 //       under plain LPT, 1.4% faster;
 //   0 = LPT over all tiles (heaviest first);
 //   2 = LPT over power-of-two work buckets, kv-grouped inside a bucket.
-// Kernel-3 variant (SHPLB_K3): 0 = single-CTA two-half kernel (fa_sm100.cu,
-// default), 1 = "pair", the CTA-pair kernel (fa_pair_sm100.cu) for block_q = 256.
-int k3_variant() {
-    static const int v = [] {
-        const char* e = std::getenv("SHPLB_K3");
-        return (e && std::string(e) == "pair") ? 1 : 0;
-    }();
-    return v;
-}
-
 // block_q = 128: two query blocks per kernel-3 CTA (each with its own selection
 // and K / V stream, fa_sm100.cu kDual). SHPLB_DUAL=0 (diagnostic) restores one
 // block per CTA.
@@ -553,8 +543,6 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     p.tm_q = make_tmap(q, s->num_q_heads, s->seq_len);
     p.tm_k = make_tmap(k, s->num_kv_heads, s->seq_len);
     p.tm_v = make_tmap(v, s->num_kv_heads, s->seq_len);
-    const bool pair = s->block_q == 256 && k3_variant() == 1;
-    if (pair) p.tm_k_half = make_tmap(k, s->num_kv_heads, s->seq_len, 64);
     p.out = out;
     p.idx = idx;
     p.cnt = cnt;
@@ -574,10 +562,7 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     }
     p.scale_log2 = static_cast<float>((1.0 / std::sqrt(static_cast<double>(s->head_dim))) * 1.4426950408889634);
     if (ctx->current->num_tiles > 0) {
-        if (pair)
-            SHPLB_CUDA(kern::launch_fa_pair(p, ctx->current->num_tiles, st));
-        else
-            kern::launch_fa(p, ctx->current->num_tiles, dual_mode(s), st);
+        kern::launch_fa(p, ctx->current->num_tiles, dual_mode(s), st);
     }
     check_launch(ctx);
     SHPLB_CUDA(cudaEventRecord(ctx->current->last_use, st));

@@ -431,20 +431,6 @@ def test_zero_q_gives_uniform_weights_over_kept_keys(cuda_ctx):
     check_output(out[0], ref, "zero q")
 
 
-def test_cta_pair_kernel_variant():
-    """The experimental CTA-pair kernel 3 (SHPLB_K3=pair, fa_pair_sm100.cu) on the
-    parity cases of this file, in a subprocess (the variant is read once per process)."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-q", "-x",
-                        "-k", "small_gqa_layer or ragged_lengths or mha_and_wide or kv_map or zero_q"],
-                       cwd=root, env=dict(os.environ, SHPLB_K3="pair"), capture_output=True, text=True,
-                       timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-
-
 def test_work_list_cache_eviction(monkeypatch):
     """Kernel-3 work lists are LRU-evicted (SHPLB_WORKLIST_CACHE entries) with
     stream-ordered frees: cycling more distinct budget tables than the cache

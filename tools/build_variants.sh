@@ -11,7 +11,7 @@ while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   (nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC \
       -I../../include -I/usr/local/cuda/include $flags -c kernels/fa_sm100.cu -o "$OUT/fa_$name.o" &&
-   g++ -shared -o "$OUT/libshplb_$name.so" ../lib/obj/kernels/estimator.o ../lib/obj/kernels/profiler.o ../lib/obj/kernels/fa_pair_sm100.o "$OUT/fa_$name.o" \
+   g++ -shared -o "$OUT/libshplb_$name.so" ../lib/obj/kernels/estimator.o ../lib/obj/kernels/profiler.o "$OUT/fa_$name.o" \
       ../lib/obj/shplb_api.o ../lib/obj/host/*.o -L/usr/local/cuda/lib64 -lcudart_static -lrt \
       -ldl -lpthread -fopenmp && echo "built $name") &
   pids+=($!)
