@@ -778,6 +778,69 @@ PLACEMENTS = {
 }
 
 
+def k3_traffic():
+    """DRAM bytes (read + write) of one kernel-3 launch from the newest ncu
+    --set full capture of the bench's layer 0 committed under profiles/
+    (profiles/rNN/ncu_k3_summary.json), and where the number comes from."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_k3_summary.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+            return d["dram_bytes_per_launch"], (f"{os.path.relpath(path, ROOT)}: {d.get('what', '')}").strip()
+        except Exception:
+            continue
+    return None, "no ncu capture committed"
+
+
+def measure_fp32_peak():
+    """FFMA throughput of this GPU, measured now (tools/bin/fp32_peak), or None."""
+    exe = os.path.join(ROOT, "tools", "bin", "fp32_peak")
+    if not os.path.exists(exe):
+        return None
+    try:
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=60)
+        return json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else None
+    except Exception:
+        return None
+
+
+def stage_rooflines(layers, plans, rank, group, n, stages, peaks, fp32_peak, split):
+    """Kernel 1 against HBM bandwidth (algorithmic bytes: Q and K read once,
+    pooled means written) and kernel 2 against FP32 FFMA throughput
+    (algorithmic FLOPs: 2*d per visible (query block, key block) pair of the
+    rank's heads), per layer averaged over the stack, with this run's stage
+    times."""
+    from paper_2603_10353_b200.head_parallel import rank_segments, rank_shard
+    d, bq = 128, 256
+    nqb, nkb = n // bq, n // 128
+    vis = np.minimum(((np.arange(nqb) + 1) * bq - 1) // 128 + 1, nkb)
+    k1_bytes, k2_flops = [], []
+    for (q, k, v), plan, b in zip(layers, plans, [None] * len(layers)):
+        sh = rank_segments(plan, rank, group, np.zeros(q.shape[0], np.int64)) if split else \
+            rank_shard(plan, rank, group, np.zeros(q.shape[0], np.int64))
+        hq_r, hkv_r = len(sh.heads), len(sh.kv_heads)
+        k1_bytes.append(2.0 * n * d * (hq_r + hkv_r) + 4.0 * d * (nqb * hq_r + nkb * hkv_r))
+        k2_flops.append(2.0 * d * hq_r * float(vis.sum()))
+    k1_ms, k2_ms = float(stages[0]), float(stages[1])
+    out = {}
+    if k1_ms > 0:
+        gbs = np.mean(k1_bytes) / (k1_ms * 1e-3) / 1e9
+        out["k1_pool"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": peaks.get("hbm_gbs"),
+                          "unit": "GB/s", "frac": round(gbs / float(peaks.get("hbm_gbs", 1)), 4),
+                          "bytes_per_layer": float(np.mean(k1_bytes)),
+                          "bytes_formula": "2*n*d*(Hq+Hkv) bf16 read + 4*d*(nqb*Hq + nkb*Hkv) fp32 written"}
+    if k2_ms > 0 and fp32_peak:
+        tf = np.mean(k2_flops) / (k2_ms * 1e-3) / 1e12
+        out["k2_score_select"] = {"bound": "fp32", "achieved": round(tf, 2),
+                                  "peak": fp32_peak["fp32_tflops_burst"], "unit": "TFLOP/s",
+                                  "frac": round(tf / fp32_peak["fp32_tflops_burst"], 4),
+                                  "flops_per_layer": float(np.mean(k2_flops)),
+                                  "flops_formula": "2*d per visible (query block, key block) pair (fp32 FFMA "
+                                                   "pooled product; the selection's bisection not counted)",
+                                  "peak_source": f"tools/bin/fp32_peak measured in this run ({fp32_peak})"}
+    return out
+
+
 def config_dict(args, budgets_desc, headline="greedy"):
     return {
         "workload": (f"C3: Llama-3-8B-shaped {args.layers}-layer attention stack ({args.q_heads} Q / "
@@ -814,6 +877,7 @@ def main():
     if args.force_gather and world == 1:
         init_single_rank_group(local)
     peaks, peaks_src = load_peaks()
+    fp32_peak = measure_fp32_peak() if rank == 0 else None
     hq, n, group = args.q_heads, args.seq_len, args.q_heads // args.kv_heads
     L = max(1, args.layers)
     layers, budgets_l, binfo = [], [], {}
@@ -935,13 +999,9 @@ def main():
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
     k3_ms = float(g["stages"][2])
     k3_tflops = g["flops_local"] / (k3_ms * 1e-3) / 1e12
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("fa_dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic, traffic_src = k3_traffic()
+    stage_roofs = stage_rooflines(layers, plans_l[headline], rank, group, n, g["stages"], peaks, fp32_peak,
+                                  headline == "split")
     # Headline: per-layer time of the stack. At N > 1 it includes every
     # layer's output all-gather (overlapped with the next layer's compute).
     value = g.get("ms_with_gather", g["ms"])
@@ -973,7 +1033,8 @@ def main():
                      "flops_per_launch": g["flops_local"],
                      "flops_formula": "4*d*128*128*computed (query half, key block) tiles, counted "
                                       "from the selection (diagonal tiles counted in full)",
-                     "traffic": traffic},
+                     "traffic": traffic, "traffic_source": traffic_src},
+        "stage_rooflines": stage_roofs,
         "gpu_launches": g["launches"],
         "clocks": g["clocks"],
     }

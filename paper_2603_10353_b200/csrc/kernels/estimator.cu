@@ -15,6 +15,7 @@
 // is a warp-level radix (bisection) select on the order-preserving uint32
 // image of each score; both work out of shared memory / L2.
 #include <cstdint>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -101,6 +102,11 @@ __device__ __forceinline__ uint32_t order_key(float s) {
 template <typename KeyAt>
 __device__ void warp_select_row(KeyAt key_at, int vis, int kk, int64_t kmax, int32_t* __restrict__ idx_row) {
     const int lane = threadIdx.x & 31;
+    if (kk >= vis) {  // every visible block is kept: no ranking needed
+        for (int j = lane; j < vis; j += 32) idx_row[j] = j;
+        for (int64_t p = vis + lane; p < kmax; p += 32) idx_row[p] = -1;
+        return;
+    }
     constexpr int kRegKeys = 32;  // rows of up to 1024 candidates (128K tokens) run from registers
     uint32_t kr[kRegKeys];
     const bool in_regs = vis <= 32 * kRegKeys;
@@ -121,10 +127,17 @@ __device__ void warp_select_row(KeyAt key_at, int vis, int kk, int64_t kmax, int
         }
         return __reduce_add_sync(0xffffffffu, c);
     };
+    // T = the largest threshold with count(keys >= T) >= kk. Stop early when a
+    // trial isolates exactly kk keys: they are then the unique top kk (no tie
+    // straddles the boundary), the set the full bisection would keep.
     uint32_t T = 0;
     for (int bit = 31; bit >= 0; --bit) {
         const uint32_t trial = T | (1u << bit);
-        if (count_ge(trial) >= kk) T = trial;
+        const int c = count_ge(trial);
+        if (c >= kk) {
+            T = trial;
+            if (c == kk) break;
+        }
     }
     const int gt = T == 0xFFFFFFFFu ? 0 : count_ge(T + 1);  // keys > T
     const int need = kk - gt;
@@ -159,23 +172,29 @@ __device__ void warp_select_row(KeyAt key_at, int vis, int kk, int64_t kmax, int
 
 constexpr int kSelThreads = 256;  // 8 warps
 constexpr int kRowsPerCta = 16;   // query blocks per CTA
-constexpr int kChunk = 64;        // key blocks per shared-memory chunk
 constexpr int kPad = kHeadDim + 4;  // row stride (floats) of the Q / K tiles: 16-byte rows, no bank conflicts
 
 // One CTA: head h, query blocks [qb0, qb0+16). Scores for all visible key
-// blocks are built in shared memory with an FFMA micro-tile (2 rows x 2 key
-// blocks per thread, strided 8 rows / 32 blocks apart; per 4 columns two
-// float4 loads of Q, two of K, 16 FFMAs; every dot product is one fmaf chain
-// over c = 0..127 in order), then
-// converted once to order keys, then each warp selects two rows.
+// blocks are built in shared memory with an FFMA register tile of kRT rows x
+// kKT key blocks per thread (rows strided 16/kRT apart, key blocks kChunk/kKT
+// apart; per 4 columns kRT + kKT float4 loads feed kRT*kKT*4 FFMAs; every dot
+// product is one fmaf chain over c = 0..127 in order, so the tile shape never
+// changes a score), then converted once to order keys, then each warp selects
+// two rows. Two shapes: 4 x 4 over 256-block chunks (8 FFMA per float loaded
+// from shared memory; needs the 135 KB chunk, so rows of up to 1390 key
+// blocks), and 2 x 2 over 64-block chunks for longer rows.
+template <int kRT, int kKT, int kChunk>
 __global__ void __launch_bounds__(kSelThreads)
     score_select_kernel(const float* __restrict__ qp, const float* __restrict__ kp, int hq,
                         int hkv, int64_t n, int64_t nqb, int64_t nkb, int bq, int causal, float scale,
                         HeadTable ht, int64_t kmax, float* __restrict__ scores_out, int select,
                         int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
+    static_assert((kRowsPerCta / kRT) * (kChunk / kKT) == kSelThreads, "one thread per register tile");
+    constexpr int kRowStep = kRowsPerCta / kRT;  // threads along rows
+    constexpr int kKbStep = kChunk / kKT;        // threads along key blocks
     extern __shared__ __align__(16) float smem[];
     float* Qs = smem;                     // [16 rows][kPad]
-    float* Ks = Qs + kRowsPerCta * kPad;  // [64 key blocks][kPad]
+    float* Ks = Qs + kRowsPerCta * kPad;  // [kChunk key blocks][kPad]
     float* S = Ks + kChunk * kPad;        // [16 rows][nkb_pad]
     const int64_t nkb_pad = (nkb + 3) & ~int64_t(3);
 
@@ -198,46 +217,53 @@ __global__ void __launch_bounds__(kSelThreads)
     }
     const int64_t vis_max = visible_blocks(qb0 + rows - 1, n, nkb, bq, causal != 0);
 
-    // Thread (rp, kq) computes rows {rp, rp+8} x key blocks {kq, kq+32} of the
-    // chunk: a warp's 8 row / 4 key-block float4 loads then hit distinct bank
-    // quads (row stride 132 floats = 4 banks).
-    const int rp = tid & 7;
-    const int kq = tid >> 3;
+    // Thread (rp, kq): rows rp + kRowStep*i, key blocks kq + kKbStep*j. A warp
+    // spans 32/kRowStep consecutive kq, whose K rows (stride 132 floats = 4
+    // banks) are conflict-free, and kRowStep rows of Q (broadcast).
+    const int rp = tid % kRowStep;
+    const int kq = tid / kRowStep;
     for (int64_t kc = 0; kc < vis_max; kc += kChunk) {
         __syncthreads();  // previous chunk fully consumed (and Q tile visible)
+        const int64_t kc_end = min(static_cast<int64_t>(kChunk), vis_max - kc);  // rows worth loading
         for (int f = tid; f < kChunk * (kHeadDim / 4); f += kSelThreads) {
             const int kb = f / (kHeadDim / 4), c4 = f % (kHeadDim / 4);
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (kc + kb < nkb) v = *reinterpret_cast<const float4*>(kp + ((int64_t)g * nkb + kc + kb) * kHeadDim + c4 * 4);
+            if (kb < kc_end) v = *reinterpret_cast<const float4*>(kp + ((int64_t)g * nkb + kc + kb) * kHeadDim + c4 * 4);
             *reinterpret_cast<float4*>(Ks + kb * kPad + c4 * 4) = v;
         }
         __syncthreads();
-        float a00 = 0.f, a01 = 0.f, a10 = 0.f, a11 = 0.f;
+        if (kq >= kc_end) continue;  // none of this thread's key blocks is visible (kq is the smallest)
+        float a[kRT][kKT];
+#pragma unroll
+        for (int i = 0; i < kRT; ++i)
+#pragma unroll
+            for (int j = 0; j < kKT; ++j) a[i][j] = 0.f;
         const float* q0p = Qs + rp * kPad;
         const float* k0p = Ks + kq * kPad;
-#pragma unroll 4
+#pragma unroll 2
         for (int c4 = 0; c4 < kHeadDim / 4; ++c4) {
-            const float4 q0 = *reinterpret_cast<const float4*>(q0p + c4 * 4);
-            const float4 q1 = *reinterpret_cast<const float4*>(q0p + 8 * kPad + c4 * 4);
-            const float4 k0 = *reinterpret_cast<const float4*>(k0p + c4 * 4);
-            const float4 k1 = *reinterpret_cast<const float4*>(k0p + 32 * kPad + c4 * 4);
-            a00 = __fmaf_rn(q0.x, k0.x, a00); a01 = __fmaf_rn(q0.x, k1.x, a01);
-            a10 = __fmaf_rn(q1.x, k0.x, a10); a11 = __fmaf_rn(q1.x, k1.x, a11);
-            a00 = __fmaf_rn(q0.y, k0.y, a00); a01 = __fmaf_rn(q0.y, k1.y, a01);
-            a10 = __fmaf_rn(q1.y, k0.y, a10); a11 = __fmaf_rn(q1.y, k1.y, a11);
-            a00 = __fmaf_rn(q0.z, k0.z, a00); a01 = __fmaf_rn(q0.z, k1.z, a01);
-            a10 = __fmaf_rn(q1.z, k0.z, a10); a11 = __fmaf_rn(q1.z, k1.z, a11);
-            a00 = __fmaf_rn(q0.w, k0.w, a00); a01 = __fmaf_rn(q0.w, k1.w, a01);
-            a10 = __fmaf_rn(q1.w, k0.w, a10); a11 = __fmaf_rn(q1.w, k1.w, a11);
-        }
-        const float a[2][2] = {{a00, a01}, {a10, a11}};
+            float4 qv[kRT], kv[kKT];
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-            const int r = rp + 8 * i;
+            for (int i = 0; i < kRT; ++i) qv[i] = *reinterpret_cast<const float4*>(q0p + i * kRowStep * kPad + c4 * 4);
+#pragma unroll
+            for (int j = 0; j < kKT; ++j) kv[j] = *reinterpret_cast<const float4*>(k0p + j * kKbStep * kPad + c4 * 4);
+#pragma unroll
+            for (int i = 0; i < kRT; ++i)
+#pragma unroll
+                for (int j = 0; j < kKT; ++j) {
+                    a[i][j] = __fmaf_rn(qv[i].x, kv[j].x, a[i][j]);
+                    a[i][j] = __fmaf_rn(qv[i].y, kv[j].y, a[i][j]);
+                    a[i][j] = __fmaf_rn(qv[i].z, kv[j].z, a[i][j]);
+                    a[i][j] = __fmaf_rn(qv[i].w, kv[j].w, a[i][j]);
+                }
+        }
+#pragma unroll
+        for (int i = 0; i < kRT; ++i) {
+            const int r = rp + kRowStep * i;
             const int64_t vis = visible_blocks(qb0 + r, n, nkb, bq, causal != 0);
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int64_t kb = kc + kq + 32 * j;
+            for (int j = 0; j < kKT; ++j) {
+                const int64_t kb = kc + kq + kKbStep * j;
                 if (kb < nkb) S[r * nkb_pad + kb] = kb < vis ? __fmul_rn(a[i][j], scale) : -INFINITY;
             }
         }
@@ -304,22 +330,32 @@ void launch_pool(const void* x, int heads, int64_t n, int rows, float* out, cuda
         pool_kernel<128><<<grid, kPoolThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(x), n, out);
 }
 
-static size_t score_select_smem(int64_t nkb) {
+static size_t score_select_smem(int64_t nkb, int chunk) {
     const int64_t nkb_pad = (nkb + 3) & ~int64_t(3);
-    return sizeof(float) * (kPad * kRowsPerCta + kPad * kChunk + kRowsPerCta * nkb_pad);
+    return sizeof(float) * (kPad * kRowsPerCta + kPad * chunk + kRowsPerCta * nkb_pad);
 }
+constexpr size_t kSmemOptIn = 227 * 1024;
 
 void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n, int bq,
                          bool causal, float scale, const HeadTable& ht, int64_t kmax,
                          float* scores_out, bool select, int32_t* idx, int32_t* cnt,
                          cudaStream_t s) {
     const int64_t nqb = (n + bq - 1) / bq, nkb = (n + kBlock - 1) / kBlock;
-    const size_t smem = score_select_smem(nkb);
-    set_max_dynamic_smem(reinterpret_cast<const void*>(score_select_kernel), static_cast<int>(smem));
     const dim3 grid(static_cast<unsigned>(hq), static_cast<unsigned>((nqb + kRowsPerCta - 1) / kRowsPerCta));
-    score_select_kernel<<<grid, kSelThreads, smem, s>>>(qp, kp, hq, hkv, n, nqb, nkb, bq, causal ? 1 : 0,
-                                                        scale, ht, kmax, scores_out, select ? 1 : 0,
-                                                        idx, cnt);
+    const size_t wide = score_select_smem(nkb, 256);
+    static const bool force_narrow = std::getenv("SHPLB_K2_NARROW") != nullptr;  // tests: exercise the 2 x 2 shape
+    if (wide <= kSmemOptIn && !force_narrow) {  // 4 x 4 register tile over 256-block chunks
+        auto* k = score_select_kernel<4, 4, 256>;
+        set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(wide));
+        k<<<grid, kSelThreads, wide, s>>>(qp, kp, hq, hkv, n, nqb, nkb, bq, causal ? 1 : 0, scale, ht, kmax,
+                                         scores_out, select ? 1 : 0, idx, cnt);
+    } else {  // long rows: 2 x 2 over 64-block chunks leaves room for the score rows
+        const size_t smem = score_select_smem(nkb, 64);
+        auto* k = score_select_kernel<2, 2, 64>;
+        set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
+        k<<<grid, kSelThreads, smem, s>>>(qp, kp, hq, hkv, n, nqb, nkb, bq, causal ? 1 : 0, scale, ht, kmax,
+                                         scores_out, select ? 1 : 0, idx, cnt);
+    }
 }
 
 void launch_select_from_scores(const float* scores, int hq, int64_t n, int bq, bool causal,

@@ -470,15 +470,75 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
 
         // -------------------------------------------------------- epilogue
         // Row i of this half: O_hf / l (zero when no kept key was visible),
-        // stored to `out`, or — fused gather — to every listed output buffer
+        // written to `out`, or — fused gather — to every listed output buffer
         // at the head's global index (peer buffers are written over NVLink).
         // (The head / row are re-derived from the work list here rather than kept
         // live across the block loop, which is register-bound.)
         const int32_t tile_e = p.tiles[blockIdx.x];
         const int h_e = tile_e >> 20;
-        const int64_t qrow_e = (kDual ? static_cast<int64_t>((tile_e >> 2) & 0x3FFFF) * (2 * kBlock)
-                                      : static_cast<int64_t>(tile_e & 0xFFFFF) * p.bq) + hf * kBlock + r;
-        const bool live = hf < halves && qrow_e < p.n && (!kDual || ((tile_e >> hf) & 1));
+        const int64_t row0_e = (kDual ? static_cast<int64_t>((tile_e >> 2) & 0x3FFFF) * (2 * kBlock)
+                                      : static_cast<int64_t>(tile_e & 0xFFFFF) * p.bq) + hf * kBlock;
+        const bool live_half = hf < halves && row0_e < p.n && (!kDual || ((tile_e >> hf) & 1));
+        const float inv = l > 0.0f ? 1.0f / l : 0.0f;
+        if (it > 0) {
+            mbar_wait(&bar->pv_done[hf], (it - 1) & 1);
+            tc_fence_after();
+        }
+#ifndef SHPLB_STG_EPILOGUE
+        // TMA-store epilogue: each thread writes its row, scaled and rounded to
+        // bf16, into this half's Q tile in shared memory (free: the half's
+        // last S MMA completed before its last P.V), in the 128B-swizzled
+        // layout the Q loads use (16-byte chunk c of row r at c ^ (r mod 8));
+        // then one thread stores the 128 x 128 tile with two bulk tensor copies
+        // per destination — whole 128-byte row segments instead of one 16-byte
+        // store per thread per row, and rows past n clipped by the tensor map.
+        if (live_half) {
+            const uint32_t tile_s = sQ + static_cast<uint32_t>(hf) * kTileBytes;
+            // A half that computed nothing must still let the Q load (issued
+            // whenever the tile has any block) land before reusing its buffer.
+            if (it == 0 && nsel > 0) mbar_wait(&bar->q_full, 0);
+#pragma unroll 1
+            for (int c = 0; c < kHeadDim / 32; ++c) {
+                uint32_t v[32];
+                if (it > 0) {
+                    tmem_ld32(o_addr + c * 32, v);
+                    tmem_wait_ld();
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = 0u;
+                }
+                const uint32_t row_s = tile_s + static_cast<uint32_t>(c >> 1) * kChunkBytes + static_cast<uint32_t>(r) * 128u;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t chunk = static_cast<uint32_t>((c & 1) * 4 + u) ^ static_cast<uint32_t>(r & 7);
+                    sts128(row_s + chunk * 16u,
+                           pack_bf16x2(__uint_as_float(v[u * 8 + 0]) * inv, __uint_as_float(v[u * 8 + 1]) * inv),
+                           pack_bf16x2(__uint_as_float(v[u * 8 + 2]) * inv, __uint_as_float(v[u * 8 + 3]) * inv),
+                           pack_bf16x2(__uint_as_float(v[u * 8 + 4]) * inv, __uint_as_float(v[u * 8 + 5]) * inv),
+                           pack_bf16x2(__uint_as_float(v[u * 8 + 6]) * inv, __uint_as_float(v[u * 8 + 7]) * inv));
+                }
+            }
+            fence_proxy_async_smem();
+            named_bar_sync(1 + hf, 128);  // the half's 4 warps wrote their rows
+            if (r == 0) {
+                const int ndst = p.n_out_peers > 0 ? p.n_out_peers : 1;
+                const int plane = p.n_out_peers > 0 ? p.heads.k[h_e] : h_e;
+                for (int i = 0; i < ndst; ++i) tma_store_tile(&p.tm_out[i], tile_s, static_cast<int32_t>(row0_e), plane);
+                bulk_commit_group();
+                // Peer stores must be performed (not just read out of shared
+                // memory) before the system fence the cross-rank barrier relies on.
+                if (p.n_out_peers > 1) {
+                    bulk_wait_group0();
+                    __threadfence_system();
+                } else {
+                    bulk_wait_group_read0();  // shared memory stays valid until read
+                }
+            }
+        }
+#else
+        // Per-thread stores (dev-only A/B baseline of the TMA-store epilogue).
+        const int64_t qrow_e = row0_e + r;
+        const bool live = live_half && qrow_e < p.n;
         const int ndst = p.n_out_peers > 0 ? p.n_out_peers : 1;
         auto dst_row = [&](int i) -> __nv_bfloat16* {
             if (p.n_out_peers == 0)
@@ -486,43 +546,35 @@ __global__ void __launch_bounds__(kThreads, 1) fa_sparse_kernel(const __grid_con
             return static_cast<__nv_bfloat16*>(p.out_peers[i]) +
                    (static_cast<int64_t>(p.heads.k[h_e]) * p.n + qrow_e) * kHeadDim;
         };
-        if (it > 0) {
-            mbar_wait(&bar->pv_done[hf], (it - 1) & 1);
-            tc_fence_after();
-            const float inv = l > 0.0f ? 1.0f / l : 0.0f;
 #pragma unroll 1
-            for (int c = 0; c < kHeadDim / 32; ++c) {
-                uint32_t v[32];
+        for (int c = 0; c < kHeadDim / 32; ++c) {
+            uint32_t v[32];
+            if (it > 0) {
                 tmem_ld32(o_addr + c * 32, v);
                 tmem_wait_ld();
-                if (live) {
-                    uint4 w[4];
+            } else {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        w[u].x = pack_bf16x2(__uint_as_float(v[u * 8 + 0]) * inv, __uint_as_float(v[u * 8 + 1]) * inv);
-                        w[u].y = pack_bf16x2(__uint_as_float(v[u * 8 + 2]) * inv, __uint_as_float(v[u * 8 + 3]) * inv);
-                        w[u].z = pack_bf16x2(__uint_as_float(v[u * 8 + 4]) * inv, __uint_as_float(v[u * 8 + 5]) * inv);
-                        w[u].w = pack_bf16x2(__uint_as_float(v[u * 8 + 6]) * inv, __uint_as_float(v[u * 8 + 7]) * inv);
-                    }
+                for (int e = 0; e < 32; ++e) v[e] = 0u;
+            }
+            if (live) {
+                uint4 w[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    w[u].x = pack_bf16x2(__uint_as_float(v[u * 8 + 0]) * inv, __uint_as_float(v[u * 8 + 1]) * inv);
+                    w[u].y = pack_bf16x2(__uint_as_float(v[u * 8 + 2]) * inv, __uint_as_float(v[u * 8 + 3]) * inv);
+                    w[u].z = pack_bf16x2(__uint_as_float(v[u * 8 + 4]) * inv, __uint_as_float(v[u * 8 + 5]) * inv);
+                    w[u].w = pack_bf16x2(__uint_as_float(v[u * 8 + 6]) * inv, __uint_as_float(v[u * 8 + 7]) * inv);
+                }
 #pragma unroll 1
-                    for (int i = 0; i < ndst; ++i) {
-                        __nv_bfloat16* out = dst_row(i);
+                for (int i = 0; i < ndst; ++i) {
+                    __nv_bfloat16* out = dst_row(i);
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(out + c * 32 + u * 8) = w[u];
-                    }
+                    for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(out + c * 32 + u * 8) = w[u];
                 }
             }
-        } else if (live) {
-#pragma unroll 1
-            for (int i = 0; i < ndst; ++i) {
-                __nv_bfloat16* out = dst_row(i);
-#pragma unroll
-                for (int u = 0; u < kHeadDim / 8; ++u) *reinterpret_cast<uint4*>(out + u * 8) = make_uint4(0, 0, 0, 0);
-            }
         }
-        // Peer stores: make them visible system-wide before the kernel retires
-        // (the caller's cross-rank barrier follows the kernel on its stream).
         if (p.n_out_peers > 1) __threadfence_system();
+#endif
     }
 
     tc_fence_before();

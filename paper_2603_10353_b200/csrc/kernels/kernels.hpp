@@ -63,6 +63,10 @@ struct FaParams {
     // GPU's full output and its peers' over NVLink) instead of to `out`.
     void* out_peers[kMaxPeers];
     int32_t n_out_peers;
+    // Output tensor maps of the TMA-store epilogue ([heads][n][128] bf16, box
+    // {64,128,1}, 128B swizzle): tm_out[0] over `out` (heads = hq), or with the
+    // fused gather tm_out[i] over out_peers[i] (heads = the global head count).
+    CUtensorMap tm_out[kMaxPeers];
 };
 // dual: block_q = 128 with two query blocks per CTA (tiles packed as pairs, see
 // fa_sm100.cu); otherwise one tile per query block.

@@ -116,6 +116,30 @@ __device__ __forceinline__ void tma_load_tile_noarm_warp(void* dst, const CUtens
         : "memory");
 }
 
+// TMA store of a 128-row x 128-col bf16 tile (two 64-column chunks, 16 KB
+// apart in shared memory, 128B-swizzled as the loads leave them) to
+// (row, plane) of a 3-D tensor map; rows past the tensor's extent are clipped.
+// Tracked by this thread's bulk async-group.
+__device__ __forceinline__ void tma_store_tile(const CUtensorMap* m, uint32_t src, int32_t row, int32_t plane) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {0, %2, %3}], [%1];\n\t"
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {64, %2, %3}], [%4];"
+        ::"l"(reinterpret_cast<uint64_t>(m)), "r"(src), "r"(row), "r"(plane), "r"(src + 16384)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Wait until the bulk stores of this thread have finished READING shared memory.
+__device__ __forceinline__ void bulk_wait_group_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// Wait until they have completed (writes performed).
+__device__ __forceinline__ void bulk_wait_group0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+
 // Make this thread's generic-proxy shared-memory writes visible to the async
 // proxy (tensor core operand reads).
 __device__ __forceinline__ void fence_proxy_async_smem() {

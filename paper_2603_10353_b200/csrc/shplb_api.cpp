@@ -556,9 +556,14 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     p.causal = s->causal;
     fill_kv_map(s, p.heads);
     if (fused_gather(s)) {  // validated by check_shape
-        for (int i = 0; i < s->n_out_peers; ++i) p.out_peers[i] = s->out_peers[i];
+        for (int i = 0; i < s->n_out_peers; ++i) {
+            p.out_peers[i] = s->out_peers[i];
+            p.tm_out[i] = make_tmap(s->out_peers[i], s->out_heads_total, s->seq_len);
+        }
         for (int h = 0; h < s->num_q_heads; ++h) p.heads.k[h] = s->out_head_of_q[h];
         p.n_out_peers = s->n_out_peers;
+    } else {
+        p.tm_out[0] = make_tmap(out, s->num_q_heads, s->seq_len);
     }
     p.scale_log2 = static_cast<float>((1.0 / std::sqrt(static_cast<double>(s->head_dim))) * 1.4426950408889634);
     if (ctx->current->num_tiles > 0) {
