@@ -222,16 +222,33 @@ __global__ void __launch_bounds__(kSelThreads)
     // banks) are conflict-free, and kRowStep rows of Q (broadcast).
     const int rp = tid % kRowStep;
     const int kq = tid / kRowStep;
+    // The next chunk's pooled K rows are fetched into registers while the
+    // current chunk is multiplied (one CTA per SM leaves few warps to hide the
+    // L2 latency of a synchronous load), then stored to shared memory.
+    constexpr int kLoads = kChunk * (kHeadDim / 4) / kSelThreads;  // float4 per thread per chunk
+    float4 pre[kLoads];
+    auto fetch = [&](int64_t kc) {
+        const int64_t kc_end = min(static_cast<int64_t>(kChunk), vis_max - kc);
+#pragma unroll
+        for (int u = 0; u < kLoads; ++u) {
+            const int f = tid + u * kSelThreads;
+            const int kb = f / (kHeadDim / 4), c4 = f % (kHeadDim / 4);
+            pre[u] = kb < kc_end ? __ldg(reinterpret_cast<const float4*>(kp + ((int64_t)g * nkb + kc + kb) * kHeadDim + c4 * 4))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    if (vis_max > 0) fetch(0);
     for (int64_t kc = 0; kc < vis_max; kc += kChunk) {
         __syncthreads();  // previous chunk fully consumed (and Q tile visible)
         const int64_t kc_end = min(static_cast<int64_t>(kChunk), vis_max - kc);  // rows worth loading
-        for (int f = tid; f < kChunk * (kHeadDim / 4); f += kSelThreads) {
+#pragma unroll
+        for (int u = 0; u < kLoads; ++u) {
+            const int f = tid + u * kSelThreads;
             const int kb = f / (kHeadDim / 4), c4 = f % (kHeadDim / 4);
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (kb < kc_end) v = *reinterpret_cast<const float4*>(kp + ((int64_t)g * nkb + kc + kb) * kHeadDim + c4 * 4);
-            *reinterpret_cast<float4*>(Ks + kb * kPad + c4 * 4) = v;
+            *reinterpret_cast<float4*>(Ks + kb * kPad + c4 * 4) = pre[u];
         }
         __syncthreads();
+        if (kc + kChunk < vis_max) fetch(kc + kChunk);
         if (kq >= kc_end) continue;  // none of this thread's key blocks is visible (kq is the smallest)
         float a[kRT][kKT];
 #pragma unroll

@@ -46,7 +46,7 @@ int main(int argc, char** argv) {
         const int repeats = argc > 3 ? std::atoi(argv[3]) : 3;
         const int hq = argc > 4 ? std::atoi(argv[4]) : 32;
         const int hkv = argc > 5 ? std::atoi(argv[5]) : 8;
-        const int d = 128, calib = 16;
+        const int d = 128, calib = 128;
         const double fraction = 0.25;
         std::printf("%s\n", shplb_version());
 
@@ -89,11 +89,15 @@ int main(int argc, char** argv) {
             dev_in[3 * l] = q;
             dev_in[3 * l + 1] = k;
             dev_in[3 * l + 2] = v;
-            // calibration rows = the last `calib` query rows of every head
+            // calibration rows: `calib` rows evenly spaced through the sequence
+            // (round(linspace(0, n-1, calib)), as calibrate.calibration_rows)
             for (int h = 0; h < hq; ++h)
-                cuda(cudaMemcpy(dcal + static_cast<size_t>(h) * calib * d,
-                                q + (static_cast<size_t>(h) * n + (n - calib)) * d, calib * d * 2,
-                                cudaMemcpyDeviceToDevice), "calib");
+                for (int r = 0; r < calib; ++r) {
+                    const int64_t pos = calib > 1 ? std::llround(static_cast<double>(r) * (n - 1) / (calib - 1)) : n - 1;
+                    cuda(cudaMemcpy(dcal + (static_cast<size_t>(h) * calib + r) * d,
+                                    q + (static_cast<size_t>(h) * n + pos) * d, d * 2, cudaMemcpyDeviceToDevice),
+                         "calib");
+                }
             std::vector<double> rec(static_cast<size_t>(hq) * grid.size());
             check(shplb_profile_curves(ctx, dcal, k, hq, hkv, calib, n, d, grid.data(),
                                        static_cast<int64_t>(grid.size()), rec.data(), st),

@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--profile-kind", choices=["token", "block"], default="token")
     ap.add_argument("--targets", choices=["per_query", "per_head"], default="per_query",
                     help="synthetic generator: per-query random targets, or per-head hot key blocks")
+    ap.add_argument("--floor", type=int, default=128, help="AllocatorConfig.floor (tokens) of both tables")
     ap.add_argument("--fractions", type=float, nargs="+", default=[0.25, 0.5, 0.75, 1.0],
                     help="skyline total budgets as fractions of Hq*n")
     ap.add_argument("--skyline-devices", type=int, default=8)
@@ -51,7 +52,7 @@ def main():
         q, k, v = make_layer(LayerSpec(num_q_heads=hq, num_kv_heads=hkv, seq_len=n, seed=2603 + 104729 * r,
                                        targets=a.targets), "cuda")
         curves, _ = calibrate.profile_layer(q, k, kind=a.profile_kind, rows=a.calib_rows, ctx=ctx)
-        bs.append(P.maxmin_allocate(curves, int(round(0.25 * hq * n)), quantum=128, floor=128).budgets)
+        bs.append(P.maxmin_allocate(curves, int(round(0.25 * hq * n)), quantum=128, floor=a.floor).budgets)
         qs.append(q), ks.append(k), vs.append(v), cs.extend(curves)
     if a.requests > 1:
         q, k, v = torch.cat(qs), torch.cat(ks), torch.cat(vs)
@@ -59,6 +60,7 @@ def main():
     budgets = np.concatenate(bs)
     tag = a.config if a.requests == 1 else f"{a.config}x{a.requests}"
     tag += ("" if a.profile_kind == "token" else "_block") + ("" if a.targets == "per_query" else "_perhead")
+    tag += "" if a.floor == 128 else f"_floor{a.floor}"
     os.makedirs(a.out, exist_ok=True)
     rows = X.measured_sweep(ctx, {n: (q, k, v, budgets)}, a.degrees, steps=a.steps)
     X.write_sweep_csv(os.path.join(a.out, f"sweep_{tag}.csv"), rows)
@@ -69,10 +71,11 @@ def main():
         return
     curves = cs
     totals = [int(round(f * q.shape[0] * n)) for f in a.fractions]
-    pts = X.measured_skyline(ctx, q, k, v, curves, devices=a.skyline_devices, steps=a.steps, totals=totals)
+    pts = X.measured_skyline(ctx, q, k, v, curves, devices=a.skyline_devices, steps=a.steps, totals=totals,
+                             floor=a.floor)
     X.write_skyline_csv(os.path.join(a.out, f"skyline_{tag}.csv"), pts)
     for p in pts:
-        print(json.dumps({"kind": "skyline", "config": tag, "profile_kind": a.profile_kind,
+        print(json.dumps({"kind": "skyline", "config": tag, "profile_kind": a.profile_kind, "floor": a.floor,
                           "targets": a.targets, "fraction": p.total_budget / (q.shape[0] * n),
                           **p.__dict__}), flush=True)
     torch.cuda.synchronize()
