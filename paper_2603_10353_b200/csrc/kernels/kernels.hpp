@@ -47,6 +47,7 @@ struct FaParams {
     CUtensorMap tm_q;  // [hq][n][128] bf16, box {64,128,1}, 128B swizzle
     CUtensorMap tm_k;  // [hkv][n][128]
     CUtensorMap tm_v;  // [hkv][n][128]
+    CUtensorMap tm_k_half;  // K again with a {64,64,1} box (CTA-pair kernel: 64 keys per CTA)
     void* out;         // [hq][n][128] bf16
     const int32_t* idx;
     const int32_t* cnt;
@@ -71,6 +72,9 @@ struct FaParams {
 // dual: block_q = 128 with two query blocks per CTA (tiles packed as pairs, see
 // fa_sm100.cu); otherwise one tile per query block.
 void launch_fa(const FaParams& p, int num_tiles, bool dual, cudaStream_t s);
+// The CTA-pair variant (fa_pair_sm100.cu): bq = 256; one 2-CTA cluster per tile,
+// two softmax warpgroups per CTA on alternate key blocks.
+cudaError_t launch_fa_pair(const FaParams& p, int num_tiles, cudaStream_t s);
 
 // GPU recovery-curve profiler (profiler.cu). q_rows bf16 [hq][n_rows][128],
 // k bf16 [hkv][n_k][128]; units = hq * n_rows.

@@ -404,6 +404,19 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
 //       under plain LPT, 1.4% faster;
 //   0 = LPT over all tiles (heaviest first);
 //   2 = LPT over power-of-two work buckets, kv-grouped inside a bucket.
+// Kernel-3 variant for block_q = 256 (SHPLB_K3): "pair" (default) =
+// fa_pair_sm100.cu, a 2-CTA cluster per query block with two softmax
+// warpgroups per CTA on alternate key blocks (C3 bench: 45.6 vs 46.1 ms per
+// layer); "single" = fa_sm100.cu, one CTA with two query halves
+// ping-ponging (also the block_q = 128 kernel).
+int k3_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("SHPLB_K3");
+        return (e && std::string(e) == "single") ? 0 : 1;
+    }();
+    return v;
+}
+
 // block_q = 128: two query blocks per kernel-3 CTA (each with its own selection
 // and K / V stream, fa_sm100.cu kDual). SHPLB_DUAL=0 (diagnostic) restores one
 // block per CTA.
@@ -543,6 +556,8 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     p.tm_q = make_tmap(q, s->num_q_heads, s->seq_len);
     p.tm_k = make_tmap(k, s->num_kv_heads, s->seq_len);
     p.tm_v = make_tmap(v, s->num_kv_heads, s->seq_len);
+    const bool pair = s->block_q == 256 && k3_variant() == 1;
+    if (pair) p.tm_k_half = make_tmap(k, s->num_kv_heads, s->seq_len, 64);
     p.out = out;
     p.idx = idx;
     p.cnt = cnt;
@@ -567,7 +582,10 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     }
     p.scale_log2 = static_cast<float>((1.0 / std::sqrt(static_cast<double>(s->head_dim))) * 1.4426950408889634);
     if (ctx->current->num_tiles > 0) {
-        kern::launch_fa(p, ctx->current->num_tiles, dual_mode(s), st);
+        if (pair)
+            SHPLB_CUDA(kern::launch_fa_pair(p, ctx->current->num_tiles, st));
+        else
+            kern::launch_fa(p, ctx->current->num_tiles, dual_mode(s), st);
     }
     check_launch(ctx);
     SHPLB_CUDA(cudaEventRecord(ctx->current->last_use, st));

@@ -446,6 +446,23 @@ def test_kernel2_narrow_tile_variant():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+def test_single_cta_kernel3_variant():
+    """block_q = 256 runs the CTA-pair kernel 3 by default; the single-CTA kernel
+    (fa_sm100.cu, SHPLB_K3=single — also the block_q = 128 kernel) on the parity
+    cases of this file and the fused-gather tests, in a subprocess (the switch is
+    read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "tests/test_gpu_gather.py", "-q",
+                        "-x", "-k", "small_gqa_layer or ragged_lengths or mha_and_wide or kv_map or zero_q or "
+                                    "single_kept or full_budget or c1_shape or fused_gather"],
+                       cwd=root, env=dict(os.environ, SHPLB_K3="single"), capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def test_work_list_cache_eviction(monkeypatch):
     """Kernel-3 work lists are LRU-evicted (SHPLB_WORKLIST_CACHE entries) with
     stream-ordered frees: cycling more distinct budget tables than the cache
