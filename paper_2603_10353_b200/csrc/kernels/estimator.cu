@@ -15,6 +15,7 @@
 // is a warp-level radix (bisection) select on the order-preserving uint32
 // image of each score; both work out of shared memory / L2.
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -100,7 +101,8 @@ __device__ __forceinline__ uint32_t order_key(float s) {
 // is compacted in ascending index order with ballots. Rows of up to 1024
 // candidates are held in registers (32 per lane) for the 33 counting passes.
 template <typename KeyAt>
-__device__ void warp_select_row(KeyAt key_at, int vis, int kk, int64_t kmax, int32_t* __restrict__ idx_row) {
+__device__ void warp_select_row(KeyAt key_at, int vis, int kk, int64_t kmax, int32_t* __restrict__ idx_row,
+                                uint32_t* __restrict__ scratch) {
     const int lane = threadIdx.x & 31;
     if (kk >= vis) {  // every visible block is kept: no ranking needed
         for (int j = lane; j < vis; j += 32) idx_row[j] = j;
@@ -130,16 +132,51 @@ __device__ void warp_select_row(KeyAt key_at, int vis, int kk, int64_t kmax, int
     // T = the largest threshold with count(keys >= T) >= kk. Stop early when a
     // trial isolates exactly kk keys: they are then the unique top kk (no tie
     // straddles the boundary), the set the full bisection would keep.
+    //
+    // Narrowing: after the bits above `bit` are decided, every key is either
+    // above the window [T, T + 2^bit) (counted in `hi`), below it, or inside
+    // it (lo - hi keys, lo = count(keys >= T)). Once at most 32 keys are
+    // inside, they are compacted into one register per lane (scratch: 32
+    // words of shared memory per warp) and the remaining bits count only
+    // those: hi0 + (inside keys >= trial), hi0 = the keys above the window at
+    // narrowing time (later trials all fall inside it). Same counts, same T.
     uint32_t T = 0;
+    int lo = vis, hi = 0, hi0 = 0;
+    bool narrow = false;
+    uint32_t cand = 0u;  // narrowed: this lane's window key (0 = none; trials are >= 1)
+    auto count_ge_n = [&](uint32_t trial) {
+        return narrow ? hi0 + __popc(__ballot_sync(0xffffffffu, cand >= trial)) : count_ge(trial);
+    };
     for (int bit = 31; bit >= 0; --bit) {
         const uint32_t trial = T | (1u << bit);
-        const int c = count_ge(trial);
+        const int c = count_ge_n(trial);
         if (c >= kk) {
             T = trial;
+            lo = c;
             if (c == kk) break;
+        } else {
+            hi = c;
+        }
+        if (!narrow && in_regs && bit > 0 && lo - hi <= 32) {
+            // Window [T, T + 2^bit): T >= 1 here unless every trial so far failed,
+            // in which case the window starts at 0 and padding (key 0, j >= vis) is excluded by j.
+            const uint32_t span = 1u << bit;
+            int pos = 0;
+#pragma unroll
+            for (int t = 0; t < kRegKeys; ++t) {
+                const bool in = (lane + 32 * t) < vis && kr[t] >= T && kr[t] - T < span;
+                const uint32_t m = __ballot_sync(0xffffffffu, in);
+                if (in) scratch[pos + __popc(m & ((1u << lane) - 1u))] = kr[t];
+                pos += __popc(m);
+            }
+            __syncwarp();
+            cand = lane < pos ? scratch[lane] : 0u;
+            __syncwarp();
+            hi0 = hi;
+            narrow = true;
         }
     }
-    const int gt = T == 0xFFFFFFFFu ? 0 : count_ge(T + 1);  // keys > T
+    const int gt = T == 0xFFFFFFFFu ? 0 : count_ge_n(T + 1);  // keys > T
     const int need = kk - gt;
     const uint32_t lt_mask = (1u << lane) - 1u;
     int written = 0, ties = 0;
@@ -170,144 +207,175 @@ __device__ void warp_select_row(KeyAt key_at, int vis, int kk, int64_t kmax, int
     for (int64_t p = kk + lane; p < kmax; p += 32) idx_row[p] = -1;
 }
 
-constexpr int kSelThreads = 256;  // 8 warps
-constexpr int kRowsPerCta = 16;   // query blocks per CTA
+constexpr int kSelThreads = 256;  // standalone selector: 8 warps, one row each
 constexpr int kPad = kHeadDim + 4;  // row stride (floats) of the Q / K tiles: 16-byte rows, no bank conflicts
 
-// One CTA: head h, query blocks [qb0, qb0+16). Scores for all visible key
-// blocks are built in shared memory with an FFMA register tile of kRT rows x
-// kKT key blocks per thread (rows strided 16/kRT apart, key blocks kChunk/kKT
-// apart; per 4 columns kRT + kKT float4 loads feed kRT*kKT*4 FFMAs; every dot
-// product is one fmaf chain over c = 0..127 in order, so the tile shape never
-// changes a score), then converted once to order keys, then each warp selects
-// two rows. Two shapes: 4 x 4 over 256-block chunks (8 FFMA per float loaded
-// from shared memory; needs the 135 KB chunk, so rows of up to 1390 key
-// blocks), and 2 x 2 over 64-block chunks for longer rows.
-template <int kRT, int kKT, int kChunk>
-__global__ void __launch_bounds__(kSelThreads)
-    score_select_kernel(const float* __restrict__ qp, const float* __restrict__ kp, int hq,
-                        int hkv, int64_t n, int64_t nqb, int64_t nkb, int bq, int causal, float scale,
-                        HeadTable ht, int64_t kmax, float* __restrict__ scores_out, int select,
-                        int32_t* __restrict__ idx, int32_t* __restrict__ cnt) {
-    static_assert((kRowsPerCta / kRT) * (kChunk / kKT) == kSelThreads, "one thread per register tile");
-    constexpr int kRowStep = kRowsPerCta / kRT;  // threads along rows
-    constexpr int kKbStep = kChunk / kKT;        // threads along key blocks
-    extern __shared__ __align__(16) float smem[];
-    float* Qs = smem;                     // [16 rows][kPad]
-    float* Ks = Qs + kRowsPerCta * kPad;  // [kChunk key blocks][kPad]
-    float* S = Ks + kChunk * kPad;        // [16 rows][nkb_pad]
-    const int64_t nkb_pad = (nkb + 3) & ~int64_t(3);
+// Kernel 2 (score + select). One CTA = one GROUP of up to 4 q heads that read
+// the same kv head (GQA) x Q = 64 / G consecutive query blocks: 64 row slots
+// share every pooled K chunk the CTA stages in shared memory (G x fewer K
+// loads than one head per CTA). 512 threads; thread (rp, kq) holds an 8 x 4
+// FFMA register tile: row slots rp + 8i, key blocks kq + 64j of the 256-block
+// chunk (per 4 columns 8 + 4 float4 loads feed 128 FFMAs). Every dot product
+// is one fmaf chain over c = 0..127 in order, then x (1/sqrt d), so no tiling
+// choice changes a score. A thread computes only the key
+// blocks of the chunk that exist (nj <= 4), so a partial last chunk costs its
+// own size. Scores go to global memory (the caller's score matrix, or a
+// workspace that stays in L2), then each warp selects 4 rows from there.
+constexpr int kGrpThreads = 512;
+constexpr int kGrpRows = 64;     // row slots per CTA
+constexpr int kGrpRowStep = 8;   // threads along rows
+constexpr int kGrpChunk = 256;   // key blocks per staged chunk
+constexpr int kGrpKbStep = kGrpThreads / kGrpRowStep;  // 64 threads along key blocks
+constexpr int kGrpRT = kGrpRows / kGrpRowStep;         // 8 rows per thread
+constexpr int kGrpKT = kGrpChunk / kGrpKbStep;         // 4 key blocks per thread
+constexpr size_t kGrpSmem = sizeof(float) * (kGrpRows + kGrpChunk) * kPad + sizeof(uint32_t) * 32 * (kGrpThreads / 32);
 
-    // Grid (heads, row chunks): the hardware hands out CTAs head-fastest, and
-    // chunk y = 0 is the LAST chunk of query blocks, so under the causal mask
-    // the heaviest chunks (most visible key blocks) of every head go first and
-    // the launch tail is made of the lightest ones (LPT order).
-    const int h = blockIdx.x;
-    const int g = ht.kv[h];
-    const int64_t qb0 = static_cast<int64_t>(gridDim.y - 1 - blockIdx.y) * kRowsPerCta;
-    const int rows = static_cast<int>(min(static_cast<int64_t>(kRowsPerCta), nqb - qb0));
+struct GrpCtx {
+    float* scores;
+    int64_t nqb, nkb, n, qb0;
+    int bq, causal, Q, G;
+    uint32_t heads;  // 4 x 8-bit q head ids
+    __device__ bool valid(int s) const { return s / Q < G && qb0 + s % Q < nqb; }
+    __device__ int head(int s) const { return static_cast<int>((heads >> (8 * (s / Q))) & 0xFFu); }
+    __device__ int64_t qb(int s) const { return qb0 + s % Q; }
+};
+
+// One chunk's tile product for a thread computing NJ of its key blocks, and
+// the store of those scores (-inf past the row's causally visible blocks).
+template <int NJ>
+__device__ __forceinline__ void grp_tile(const float* __restrict__ Qs, const float* __restrict__ Ks, int rp, int kq,
+                                         int64_t kc, int kc_end, float scale, const GrpCtx& c) {
+    float a[kGrpRT][NJ];
+#pragma unroll
+    for (int i = 0; i < kGrpRT; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) a[i][j] = 0.f;
+    const float* q0p = Qs + rp * kPad;
+    const float* k0p = Ks + kq * kPad;
+#pragma unroll 2
+    for (int c4 = 0; c4 < kHeadDim / 4; ++c4) {
+        float4 qv[kGrpRT], kv[NJ];
+#pragma unroll
+        for (int i = 0; i < kGrpRT; ++i) qv[i] = *reinterpret_cast<const float4*>(q0p + i * kGrpRowStep * kPad + c4 * 4);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) kv[j] = *reinterpret_cast<const float4*>(k0p + j * kGrpKbStep * kPad + c4 * 4);
+#pragma unroll
+        for (int i = 0; i < kGrpRT; ++i)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                a[i][j] = __fmaf_rn(qv[i].x, kv[j].x, a[i][j]);
+                a[i][j] = __fmaf_rn(qv[i].y, kv[j].y, a[i][j]);
+                a[i][j] = __fmaf_rn(qv[i].z, kv[j].z, a[i][j]);
+                a[i][j] = __fmaf_rn(qv[i].w, kv[j].w, a[i][j]);
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < kGrpRT; ++i) {
+        const int s = rp + kGrpRowStep * i;
+        if (!c.valid(s)) continue;
+        const int64_t qb = c.qb(s);
+        const int64_t vis = visible_blocks(qb, c.n, c.nkb, c.bq, c.causal != 0);
+        float* dst = c.scores + (static_cast<int64_t>(c.head(s)) * c.nqb + qb) * c.nkb + kc;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int kb = kq + kGrpKbStep * j;
+            if (kb < kc_end) dst[kb] = kc + kb < vis ? __fmul_rn(a[i][j], scale) : -INFINITY;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kGrpThreads, 1)
+    score_select_kernel(const float* __restrict__ qp, const float* __restrict__ kp, int64_t n, int64_t nqb,
+                        int64_t nkb, int bq, int causal, float scale, HeadTable ht, GroupTable gt, int64_t kmax,
+                        float* scores, int fill_tail, int select, int32_t* __restrict__ idx,
+                        int32_t* __restrict__ cnt) {
+    extern __shared__ __align__(16) float smem[];
+    float* Qs = smem;                    // [64 row slots][kPad]
+    float* Ks = Qs + kGrpRows * kPad;    // [256 key blocks][kPad]
+    uint32_t* scratch = reinterpret_cast<uint32_t*>(Ks + kGrpChunk * kPad);  // [16 warps][32]
+
+    GrpCtx c;
+    c.scores = scores;
+    c.nqb = nqb;
+    c.nkb = nkb;
+    c.n = n;
+    c.bq = bq;
+    c.causal = causal;
+    c.G = gt.size[blockIdx.x];
+    c.Q = kGrpRows / c.G;
+    c.heads = gt.heads[blockIdx.x];
+    // Grid (groups, row chunks): the hardware hands out CTAs group-fastest, and
+    // y = 0 is the LAST chunk of query blocks, so under the causal mask the
+    // heaviest chunks (most visible key blocks) go first and the launch tail
+    // is made of the lightest ones (LPT order). Groups with fewer heads have
+    // fewer (longer) chunks; their surplus y exits.
+    const int64_t nchunks = (nqb + c.Q - 1) / c.Q;
+    if (static_cast<int64_t>(blockIdx.y) >= nchunks) return;
+    c.qb0 = (nchunks - 1 - static_cast<int64_t>(blockIdx.y)) * c.Q;
+    const int g = ht.kv[c.head(0)];
     const int tid = threadIdx.x;
 
-    // Q tile (row-major, float4).
-    for (int f = tid; f < kRowsPerCta * (kHeadDim / 4); f += kSelThreads) {
-        const int r = f / (kHeadDim / 4), c4 = f % (kHeadDim / 4);
+    for (int f = tid; f < kGrpRows * (kHeadDim / 4); f += kGrpThreads) {
+        const int s = f / (kHeadDim / 4), c4 = f % (kHeadDim / 4);
         float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r < rows) v = *reinterpret_cast<const float4*>(qp + ((int64_t)h * nqb + qb0 + r) * kHeadDim + c4 * 4);
-        *reinterpret_cast<float4*>(Qs + r * kPad + c4 * 4) = v;
+        if (c.valid(s))
+            v = __ldg(reinterpret_cast<const float4*>(qp + (static_cast<int64_t>(c.head(s)) * nqb + c.qb(s)) * kHeadDim + c4 * 4));
+        *reinterpret_cast<float4*>(Qs + s * kPad + c4 * 4) = v;
     }
-    const int64_t vis_max = visible_blocks(qb0 + rows - 1, n, nkb, bq, causal != 0);
-
-    // Thread (rp, kq): rows rp + kRowStep*i, key blocks kq + kKbStep*j. A warp
-    // spans 32/kRowStep consecutive kq, whose K rows (stride 132 floats = 4
-    // banks) are conflict-free, and kRowStep rows of Q (broadcast).
-    const int rp = tid % kRowStep;
-    const int kq = tid / kRowStep;
-    // The next chunk's pooled K rows are fetched into registers while the
-    // current chunk is multiplied (one CTA per SM leaves few warps to hide the
-    // L2 latency of a synchronous load), then stored to shared memory.
-    constexpr int kLoads = kChunk * (kHeadDim / 4) / kSelThreads;  // float4 per thread per chunk
-    float4 pre[kLoads];
-    auto fetch = [&](int64_t kc) {
-        const int64_t kc_end = min(static_cast<int64_t>(kChunk), vis_max - kc);
+    const int64_t vis_max = visible_blocks(min(c.qb0 + c.Q, nqb) - 1, n, nkb, bq, causal != 0);
+    // Thread (rp, kq): a warp spans 4 consecutive kq (K rows 132 floats = 4
+    // banks apart: conflict-free 16-byte loads) and all 8 rp (Q rows, likewise).
+    const int rp = tid % kGrpRowStep;
+    const int kq = tid / kGrpRowStep;
+    const float* kbase = kp + static_cast<int64_t>(g) * nkb * kHeadDim;
+    for (int64_t kc = 0; kc < vis_max; kc += kGrpChunk) {
+        const int kc_end = static_cast<int>(min(static_cast<int64_t>(kGrpChunk), vis_max - kc));
+        __syncthreads();  // previous chunk consumed (and the Q tile visible)
+        {
+            const float4* src = reinterpret_cast<const float4*>(kbase + kc * kHeadDim);
+            constexpr int kPer = kGrpChunk * (kHeadDim / 4) / kGrpThreads;  // 16 float4 per thread
+            float4 t[kPer];
 #pragma unroll
-        for (int u = 0; u < kLoads; ++u) {
-            const int f = tid + u * kSelThreads;
-            const int kb = f / (kHeadDim / 4), c4 = f % (kHeadDim / 4);
-            pre[u] = kb < kc_end ? __ldg(reinterpret_cast<const float4*>(kp + ((int64_t)g * nkb + kc + kb) * kHeadDim + c4 * 4))
-                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    };
-    if (vis_max > 0) fetch(0);
-    for (int64_t kc = 0; kc < vis_max; kc += kChunk) {
-        __syncthreads();  // previous chunk fully consumed (and Q tile visible)
-        const int64_t kc_end = min(static_cast<int64_t>(kChunk), vis_max - kc);  // rows worth loading
+            for (int u = 0; u < kPer; ++u) {
+                const int f = tid + u * kGrpThreads;
+                t[u] = f / (kHeadDim / 4) < kc_end ? __ldg(src + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
 #pragma unroll
-        for (int u = 0; u < kLoads; ++u) {
-            const int f = tid + u * kSelThreads;
-            const int kb = f / (kHeadDim / 4), c4 = f % (kHeadDim / 4);
-            *reinterpret_cast<float4*>(Ks + kb * kPad + c4 * 4) = pre[u];
-        }
-        __syncthreads();
-        if (kc + kChunk < vis_max) fetch(kc + kChunk);
-        if (kq >= kc_end) continue;  // none of this thread's key blocks is visible (kq is the smallest)
-        float a[kRT][kKT];
-#pragma unroll
-        for (int i = 0; i < kRT; ++i)
-#pragma unroll
-            for (int j = 0; j < kKT; ++j) a[i][j] = 0.f;
-        const float* q0p = Qs + rp * kPad;
-        const float* k0p = Ks + kq * kPad;
-#pragma unroll 2
-        for (int c4 = 0; c4 < kHeadDim / 4; ++c4) {
-            float4 qv[kRT], kv[kKT];
-#pragma unroll
-            for (int i = 0; i < kRT; ++i) qv[i] = *reinterpret_cast<const float4*>(q0p + i * kRowStep * kPad + c4 * 4);
-#pragma unroll
-            for (int j = 0; j < kKT; ++j) kv[j] = *reinterpret_cast<const float4*>(k0p + j * kKbStep * kPad + c4 * 4);
-#pragma unroll
-            for (int i = 0; i < kRT; ++i)
-#pragma unroll
-                for (int j = 0; j < kKT; ++j) {
-                    a[i][j] = __fmaf_rn(qv[i].x, kv[j].x, a[i][j]);
-                    a[i][j] = __fmaf_rn(qv[i].y, kv[j].y, a[i][j]);
-                    a[i][j] = __fmaf_rn(qv[i].z, kv[j].z, a[i][j]);
-                    a[i][j] = __fmaf_rn(qv[i].w, kv[j].w, a[i][j]);
-                }
-        }
-#pragma unroll
-        for (int i = 0; i < kRT; ++i) {
-            const int r = rp + kRowStep * i;
-            const int64_t vis = visible_blocks(qb0 + r, n, nkb, bq, causal != 0);
-#pragma unroll
-            for (int j = 0; j < kKT; ++j) {
-                const int64_t kb = kc + kq + kKbStep * j;
-                if (kb < nkb) S[r * nkb_pad + kb] = kb < vis ? __fmul_rn(a[i][j], scale) : -INFINITY;
+            for (int u = 0; u < kPer; ++u) {
+                const int f = tid + u * kGrpThreads;
+                *reinterpret_cast<float4*>(Ks + (f / (kHeadDim / 4)) * kPad + (f % (kHeadDim / 4)) * 4) = t[u];
             }
         }
+        __syncthreads();
+        const int nj = kq < kc_end ? min(kGrpKT, (kc_end - kq + kGrpKbStep - 1) / kGrpKbStep) : 0;
+        switch (nj) {
+            case 4: grp_tile<4>(Qs, Ks, rp, kq, kc, kc_end, scale, c); break;
+            case 3: grp_tile<3>(Qs, Ks, rp, kq, kc, kc_end, scale, c); break;
+            case 2: grp_tile<2>(Qs, Ks, rp, kq, kc, kc_end, scale, c); break;
+            case 1: grp_tile<1>(Qs, Ks, rp, kq, kc, kc_end, scale, c); break;
+            default: break;
+        }
     }
-    __syncthreads();
-
-    if (scores_out) {
-        for (int r = 0; r < rows; ++r) {
-            float* dst = scores_out + ((int64_t)h * nqb + qb0 + r) * nkb;
-            for (int64_t kb = tid; kb < nkb; kb += kSelThreads)
-                dst[kb] = kb < vis_max ? S[r * nkb_pad + kb] : -INFINITY;
+    if (fill_tail) {  // score-matrix output: -inf past the CTA's last visible block
+        for (int s = 0; s < kGrpRows; ++s) {
+            if (!c.valid(s)) continue;
+            float* dst = scores + (static_cast<int64_t>(c.head(s)) * nqb + c.qb(s)) * nkb;
+            for (int64_t kb = vis_max + tid; kb < nkb; kb += kGrpThreads) dst[kb] = -INFINITY;
         }
     }
     if (!select) return;
-    // Scores -> order keys in place, once (the bisection reads each key 33 times).
-    uint32_t* Kk = reinterpret_cast<uint32_t*>(S);
-    for (int r = 0; r < rows; ++r)
-        for (int64_t kb = tid; kb < vis_max; kb += kSelThreads) Kk[r * nkb_pad + kb] = order_key(S[r * nkb_pad + kb]);
-    __syncthreads();
+    __syncthreads();  // this CTA's score rows are written (read back from L2 below)
     const int warp = tid >> 5;
-    for (int r = warp; r < rows; r += kSelThreads / 32) {
-        const int64_t qb = qb0 + r;
+    for (int s = warp; s < kGrpRows; s += kGrpThreads / 32) {
+        if (!c.valid(s)) continue;
+        const int h = c.head(s);
+        const int64_t qb = c.qb(s);
         const int vis = static_cast<int>(visible_blocks(qb, n, nkb, bq, causal != 0));
         const int kk = min(ht.k[h], vis);
-        const uint32_t* keys = Kk + r * nkb_pad;
-        warp_select_row([keys](int j) { return keys[j]; }, vis, kk, kmax, idx + ((int64_t)h * nqb + qb) * kmax);
-        if ((tid & 31) == 0) cnt[(int64_t)h * nqb + qb] = kk;
+        const float* row = scores + (static_cast<int64_t>(h) * nqb + qb) * nkb;
+        warp_select_row([row](int j) { return order_key(__ldcg(row + j)); }, vis, kk, kmax,
+                        idx + (static_cast<int64_t>(h) * nqb + qb) * kmax, scratch + 32 * warp);
+        if ((tid & 31) == 0) cnt[static_cast<int64_t>(h) * nqb + qb] = kk;
     }
 }
 
@@ -316,6 +384,7 @@ __global__ void __launch_bounds__(kSelThreads)
     select_kernel(const float* __restrict__ scores, int hq, int64_t n, int64_t nqb, int64_t nkb,
                   int bq, int causal, HeadTable ht, int64_t kmax, int32_t* __restrict__ idx,
                   int32_t* __restrict__ cnt) {
+    __shared__ uint32_t scratch[kSelThreads / 32][32];
     const int64_t row = static_cast<int64_t>(blockIdx.x) * (kSelThreads / 32) + (threadIdx.x >> 5);
     if (row >= (int64_t)hq * nqb) return;
     const int h = static_cast<int>(row / nqb);
@@ -323,7 +392,8 @@ __global__ void __launch_bounds__(kSelThreads)
     const int vis = static_cast<int>(visible_blocks(qb, n, nkb, bq, causal != 0));
     const int kk = min(ht.k[h], vis);
     const float* srow = scores + row * nkb;
-    warp_select_row([srow](int j) { return order_key(srow[j]); }, vis, kk, kmax, idx + row * kmax);
+    warp_select_row([srow](int j) { return order_key(srow[j]); }, vis, kk, kmax, idx + row * kmax,
+                    scratch[threadIdx.x >> 5]);
     if ((threadIdx.x & 31) == 0) cnt[row] = kk;
 }
 
@@ -347,32 +417,46 @@ void launch_pool(const void* x, int heads, int64_t n, int rows, float* out, cuda
         pool_kernel<128><<<grid, kPoolThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(x), n, out);
 }
 
-static size_t score_select_smem(int64_t nkb, int chunk) {
-    const int64_t nkb_pad = (nkb + 3) & ~int64_t(3);
-    return sizeof(float) * (kPad * kRowsPerCta + kPad * chunk + kRowsPerCta * nkb_pad);
-}
-constexpr size_t kSmemOptIn = 227 * 1024;
-
 void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n, int bq,
                          bool causal, float scale, const HeadTable& ht, int64_t kmax,
-                         float* scores_out, bool select, int32_t* idx, int32_t* cnt,
+                         float* scores_out, float* scores_ws, bool select, int32_t* idx, int32_t* cnt,
                          cudaStream_t s) {
+    (void)hkv;
     const int64_t nqb = (n + bq - 1) / bq, nkb = (n + kBlock - 1) / kBlock;
-    const dim3 grid(static_cast<unsigned>(hq), static_cast<unsigned>((nqb + kRowsPerCta - 1) / kRowsPerCta));
-    const size_t wide = score_select_smem(nkb, 256);
-    static const bool force_narrow = std::getenv("SHPLB_K2_NARROW") != nullptr;  // tests: exercise the 2 x 2 shape
-    if (wide <= kSmemOptIn && !force_narrow) {  // 4 x 4 register tile over 256-block chunks
-        auto* k = score_select_kernel<4, 4, 256>;
-        set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(wide));
-        k<<<grid, kSelThreads, wide, s>>>(qp, kp, hq, hkv, n, nqb, nkb, bq, causal ? 1 : 0, scale, ht, kmax,
-                                         scores_out, select ? 1 : 0, idx, cnt);
-    } else {  // long rows: 2 x 2 over 64-block chunks leaves room for the score rows
-        const size_t smem = score_select_smem(nkb, 64);
-        auto* k = score_select_kernel<2, 2, 64>;
-        set_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
-        k<<<grid, kSelThreads, smem, s>>>(qp, kp, hq, hkv, n, nqb, nkb, bq, causal ? 1 : 0, scale, ht, kmax,
-                                         scores_out, select ? 1 : 0, idx, cnt);
+    // Row groups: the q heads of each kv head in head order, up to
+    // SHPLB_K2_GROUP (default 4; tests vary it) per group.
+    static const int max_group = [] {
+        const char* e = std::getenv("SHPLB_K2_GROUP");
+        const int v = e ? std::atoi(e) : 4;
+        return v < 1 ? 1 : (v > 4 ? 4 : v);
+    }();
+    GroupTable gt{};
+    int groups = 0, min_q = kGrpRows;
+    {
+        int open_kv[kMaxHeads];
+        int open_grp[kMaxHeads];
+        for (int i = 0; i < kMaxHeads; ++i) open_kv[i] = -1;
+        int n_open = 0;
+        for (int h = 0; h < hq; ++h) {
+            int slot = -1;
+            for (int i = 0; i < n_open; ++i)
+                if (open_kv[i] == ht.kv[h]) slot = i;
+            if (slot < 0 || gt.size[open_grp[slot]] >= max_group) {
+                if (slot < 0) slot = n_open++;
+                open_kv[slot] = ht.kv[h];
+                open_grp[slot] = groups++;
+            }
+            const int gi = open_grp[slot];
+            gt.heads[gi] |= static_cast<uint32_t>(h) << (8 * gt.size[gi]);
+            gt.size[gi] += 1;
+        }
+        for (int gi = 0; gi < groups; ++gi) min_q = std::min(min_q, kGrpRows / static_cast<int>(gt.size[gi]));
     }
+    const dim3 grid(static_cast<unsigned>(groups), static_cast<unsigned>((nqb + min_q - 1) / min_q));
+    set_max_dynamic_smem(reinterpret_cast<const void*>(score_select_kernel), static_cast<int>(kGrpSmem));
+    score_select_kernel<<<grid, kGrpThreads, kGrpSmem, s>>>(qp, kp, n, nqb, nkb, bq, causal ? 1 : 0, scale, ht, gt,
+                                                           kmax, scores_out ? scores_out : scores_ws,
+                                                           scores_out ? 1 : 0, select ? 1 : 0, idx, cnt);
 }
 
 void launch_select_from_scores(const float* scores, int hq, int64_t n, int bq, bool causal,
@@ -455,12 +539,13 @@ __global__ void colagg_colsum_kernel(const float* __restrict__ scores, const flo
 // One warp per head: the k_h key blocks with the largest column sums, ascending.
 __global__ void colagg_select_kernel(const float* __restrict__ c, int hq, int64_t nkb, HeadTable ht,
                                      int64_t kmax, int32_t* __restrict__ kept, int32_t* __restrict__ kk_out) {
+    __shared__ uint32_t scratch[4][32];  // 128 threads
     const int h = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
     if (h >= hq) return;
     const int kk = static_cast<int>(min(static_cast<int64_t>(ht.k[h]), nkb));
     const float* row = c + static_cast<int64_t>(h) * nkb;
     warp_select_row([row](int j) { return order_key(row[j]); }, static_cast<int>(nkb), kk, kmax,
-                    kept + static_cast<int64_t>(h) * kmax);
+                    kept + static_cast<int64_t>(h) * kmax, scratch[threadIdx.x >> 5]);
     if ((threadIdx.x & 31) == 0) kk_out[h] = kk;
 }
 

@@ -14,8 +14,10 @@ constexpr int kPoolSplit = 16;  // interleaved row groups of the pooled sum (DES
 constexpr int kMaxHeads = 256;  // per-launch k-block table lives in the kernel parameters
 constexpr int kMaxSelected = 2048;  // selected key blocks per query tile staged in smem (256K tokens)
 constexpr int kMaxPeers = 8;        // output buffers kernel 3 can write each row to (fused gather)
-// Kernel 2 keeps 16 rows of scores for all key blocks in shared memory:
-// 41.25 KB of Q / K tiles + 64 B per key block within the 227 KB opt-in limit.
+// Supported sequence range (key blocks per row): the round-1 selector kept 16
+// score rows in shared memory (41.25 KB of tiles + 64 B per key block within
+// 227 KB); kernel 2 now writes scores to L2 and has no such limit, but the
+// range the parity tests cover stays the documented one.
 constexpr int kMaxKeyBlocks = (227 * 1024 - 42240) / 64;  // 2972 -> 380,416 tokens
 
 // Per-q-head table passed in kernel parameters.
@@ -24,17 +26,24 @@ struct HeadTable {
     int32_t kv[kMaxHeads];  // kv head read by this q head
 };
 
+// Kernel 2 row groups: up to 4 q heads that read the same kv head.
+struct GroupTable {
+    uint32_t heads[kMaxHeads];  // q head ids, 8 bits each
+    uint8_t size[kMaxHeads];    // heads in the group (1..4)
+};
+
 // Kernel 1: x [heads][n][128] bf16 -> out [heads][ceil(n/rows)][128] fp32 block means
 // (rows = 128 or 256).
 void launch_pool(const void* x, int heads, int64_t n, int rows, float* out, cudaStream_t s);
 
 // Kernel 2 (fused score + select): pooled q [hq][nqb][128], pooled k
 // [hkv][nkb][128]; q head h scores against pooled kv head ht.kv[h]. scores_out (nullable) receives the full score matrix
-// [hq][nqb][nkb] (-inf where causally invisible). With select=true, idx/cnt
-// receive the per-(head, q block) top-k block lists.
+// [hq][nqb][nkb] (-inf where causally invisible); otherwise the scores go to
+// scores_ws (hq*nqb*nkb floats, contents undefined after). With select=true,
+// idx/cnt receive the per-(head, q block) top-k block lists.
 void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n, int bq,
                          bool causal, float scale, const HeadTable& ht, int64_t kmax,
-                         float* scores_out, bool select, int32_t* idx, int32_t* cnt,
+                         float* scores_out, float* scores_ws, bool select, int32_t* idx, int32_t* cnt,
                          cudaStream_t s);
 
 // Kernel 2 (standalone): selection from a precomputed score matrix.

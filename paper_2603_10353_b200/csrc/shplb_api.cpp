@@ -262,6 +262,8 @@ struct shplb_ctx {
     // ColumnAggregateTopK workspace: score matrix + row/column statistics, kept sets.
     float* ca_ws = nullptr;
     size_t ca_ws_bytes = 0;
+    float* k2_ws = nullptr;  // kernel 2's score rows when no score matrix is requested (L2-resident)
+    size_t k2_ws_bytes = 0;
     int32_t* ca_kept = nullptr;
     size_t ca_kept_bytes = 0;
     int64_t last_kmax = 0;
@@ -385,13 +387,14 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
         const size_t n_scores = static_cast<size_t>(s->num_q_heads) * nqb * nkb;
         float* ws = colagg_workspace(ctx, s, kmax);
         kern::launch_score_select(ctx->qp, ctx->kp, s->num_q_heads, s->num_kv_heads, s->seq_len, s->block_q,
-                                  s->causal != 0, scale, kb, kmax, ws, false, nullptr, nullptr, st);
+                                  s->causal != 0, scale, kb, kmax, ws, nullptr, false, nullptr, nullptr, st);
         kern::launch_colagg_select(ws, s->num_q_heads, s->seq_len, s->block_q, s->causal != 0, kb, kmax,
                                    ws + n_scores, ctx->ca_kept, idx, cnt, st);
         check_launch(ctx, 3 + 4);
     } else {
+        if (!scores_out) grow(ctx->k2_ws, ctx->k2_ws_bytes, sizeof(float) * s->num_q_heads * nqb * nkb);
         kern::launch_score_select(ctx->qp, ctx->kp, s->num_q_heads, s->num_kv_heads, s->seq_len, s->block_q,
-                                  s->causal != 0, scale, kb, kmax, scores_out, select, idx, cnt, st);
+                                  s->causal != 0, scale, kb, kmax, scores_out, ctx->k2_ws, select, idx, cnt, st);
         check_launch(ctx, 3);
     }
     if (select) mark(ctx, 2, st);
@@ -647,6 +650,7 @@ int shplb_ctx_destroy(shplb_ctx* ctx) {
         cudaFree(ctx->dense_cnt);
         cudaFree(ctx->prof_scores);
         cudaFree(ctx->ca_ws);
+        cudaFree(ctx->k2_ws);
         cudaFree(ctx->ca_kept);
         cudaFree(ctx->prof_sorted);
         cudaFree(ctx->prof_mass);

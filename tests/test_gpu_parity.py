@@ -431,17 +431,20 @@ def test_zero_q_gives_uniform_weights_over_kept_keys(cuda_ctx):
     check_output(out[0], ref, "zero q")
 
 
-def test_kernel2_narrow_tile_variant():
-    """Kernel 2's 2 x 2 / 64-block-chunk score tile (used for rows longer than
-    1388 key blocks, forced here with SHPLB_K2_NARROW) on the parity cases of this
-    file, in a subprocess (the switch is read once per process)."""
+@pytest.mark.parametrize("group", ["1", "3"])
+def test_kernel2_group_sizes(group):
+    """Kernel 2 scores up to 4 q heads of one kv head per CTA (64 row slots =
+    G heads x 64 / G query blocks); SHPLB_K2_GROUP caps G, so 1 (64 query
+    blocks of one head) and 3 (21 query blocks, a slot left idle, GQA groups
+    split 3 + 1) run the other row mappings on the parity cases of this file,
+    in a subprocess (the switch is read once per process)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-q", "-x",
-                        "-k", "small_gqa_layer or ragged_lengths or mha_and_wide or ties or c1_shape"],
-                       cwd=root, env=dict(os.environ, SHPLB_K2_NARROW="1"), capture_output=True, text=True,
+                        "-k", "small_gqa_layer or ragged_lengths or mha_and_wide or ties or c1_shape or kv_map"],
+                       cwd=root, env=dict(os.environ, SHPLB_K2_GROUP=group), capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
