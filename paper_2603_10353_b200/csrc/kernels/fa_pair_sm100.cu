@@ -21,22 +21,23 @@
 // so each 64 KB K/V tile still feeds 256 query rows (the reuse of the
 // single-CTA kernel's two halves) while each SM reads only half of it.
 //
-// Online softmax across two warpgroups (same semantics as fa_sm100.cu:
+// Online softmax per warpgroup (same semantics as fa_sm100.cu:
 // softmax_weighted_sum over the kept set, proj/src/attention.cpp:35-49; causal
-// mask :28-30; zero row when nothing is visible :40-41). The running max is a
-// chain m_j = f(m_{j-1}, block j): warpgroup (j mod 2) reads m_{j-1} from
-// shared memory (4 slots, one mbarrier each), decides m_j with the lazy rule
-// (raise only when the block max exceeds it by > 2^8), publishes it, then
-// exponentiates against it. When m rises it rescales O in TMEM after
-// P(j-1)·V(j-1) has landed and before P(j)·V(j) is issued. Each warpgroup keeps
-// its row sum relative to the last m it used; the epilogue combines the two.
+// mask :28-30; zero row when nothing is visible :40-41). Each warpgroup keeps
+// its own running max (lazy rule: raised only when a block max exceeds it by
+// > 2^8), row sum and accumulator O_w in TMEM — P(j)·V(j) accumulates into
+// O_(j mod 2) — so the two never wait on each other; when m rises the
+// warpgroup rescales its O_w after its previous P·V has landed and before its
+// next is issued. The epilogue merges (O_0, l_0, m_0) and (O_1, l_1, m_1).
+// (Round-2 history: one shared O with the max chained between the warpgroups
+// through shared memory cost every block a cross-warpgroup wait.)
 //
 // Warps (384 threads, registers rebalanced with setmaxnreg as fa_sm100.cu):
 //   0-3 softmax A (even blocks), 4-7 softmax B (odd blocks), 8 TMA producer of
 //   this CTA's halves of Q and K, 10 of V (completion bytes on the leader's
 //   barriers), 9 TMEM allocator and (leader) S issuer, 11 (leader) P·V issuer.
-// Shared memory: Q 32 KB, K 4 x 16 KB, V 4 x 16 KB, selection, barriers, m slots.
-// TMEM (512 columns allocated): S [0,128), P_A [128,192), P_B [192,256), O [256,384).
+// Shared memory: Q 32 KB, K 4 x 16 KB, V 4 x 16 KB, selection, barriers, (l, m).
+// TMEM (512 columns): S [0,128), P_A [128,192), P_B [192,256), O_A [256,384), O_B [384,512).
 #include <cstdint>
 #include <cstdio>
 #include <cuda.h>
@@ -59,7 +60,7 @@ constexpr int kQHalfBytes = 32768;  // [2 d-chunks][128 rows][128 B]
 constexpr int kKHalfBytes = 16384;  // [2 d-chunks][64 keys][128 B]
 constexpr int kVHalfBytes = 16384;  // [128 keys][64 d = 128 B]
 constexpr uint32_t kPairTmemCols = 512;
-constexpr uint32_t kColS = 0, kColP = 128, kColO = 256;  // P buffer w at kColP + 64 w
+constexpr uint32_t kColS = 0, kColP = 128, kColO = 256;  // P_w at kColP + 64 w, O_w at kColO + 128 w
 constexpr uint32_t kIdescPairS = idesc_bf16_f32(256, 128, 0, 0);   // Q K-major, K K-major
 constexpr uint32_t kIdescPairPV = idesc_bf16_f32(256, 128, 0, 1);  // P (TMEM), V MN-major
 constexpr float kPairRescaleThreshold = 8.0f;
@@ -72,7 +73,6 @@ struct __align__(8) PairBarriers {
     uint64_t s_free;      // leader: the owning warpgroups of both CTAs loaded S(j) (8 warps)
     uint64_t p_full[2][2];  // leader: CTA r's P(j) stored (and O rescaled), [r][j mod 2], 4 warps
     uint64_t pv_done[4];  // each CTA: P(j)·V(j) completed, [j mod 4] (4 slots: see the rescale wait)
-    uint64_t m_ready[4];  // this CTA: m_j published, slot j mod 4 (4 warps)
     uint32_t tmem_base;
 };
 
@@ -81,8 +81,8 @@ constexpr size_t kPSmemK = kPSmemQ + kQHalfBytes;
 constexpr size_t kPSmemV = kPSmemK + kPStages * kKHalfBytes;
 constexpr size_t kPSmemSel = kPSmemV + kPStages * kVHalfBytes;
 constexpr size_t kPSmemBar = kPSmemSel + kMaxSelected * sizeof(int32_t);
-constexpr size_t kPSmemX = kPSmemBar + ((sizeof(PairBarriers) + 15) / 16) * 16;  // m slots [4][128] + l / m [2][2][128]
-constexpr size_t kPSmemTotal = kPSmemX + (4 * 128 + 4 * 128) * sizeof(float) + 1024;
+constexpr size_t kPSmemX = kPSmemBar + ((sizeof(PairBarriers) + 15) / 16) * 16;  // l / m [2][2][128]
+constexpr size_t kPSmemTotal = kPSmemX + 4 * 128 * sizeof(float) + 1024;
 
 #ifdef SHPLB_PTRACE  // dev-only: per-block clock64 timeline of cluster SHPLB_PTRACE (leader CTA), printed at exit
 constexpr int kPTraceBlocks = 32;
@@ -103,8 +103,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
     int32_t* sel = reinterpret_cast<int32_t*>(smem + kPSmemSel);
     const uint32_t sSel = smem_u32(sel);
     auto sel_at = [&](int j) { return lds_s32(sSel + 4u * static_cast<uint32_t>(j)); };
-    float* mslot = reinterpret_cast<float*>(smem + kPSmemX);  // [4][128]
-    float* lfin = mslot + 4 * 128;                              // [2 warpgroups][2 (l, m)][128]
+    float* lfin = reinterpret_cast<float*>(smem + kPSmemX);  // [2 warpgroups][2 (l, m)][128]
 
     const uint32_t rank = cluster_ctarank();
     const int warp = warp_index_uniform();
@@ -135,7 +134,6 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
             mbar_init(&bar->p_full[i][1], 4);
         }
         for (int i = 0; i < 4; ++i) mbar_init(&bar->pv_done[i], 1);
-        for (int i = 0; i < 4; ++i) mbar_init(&bar->m_ready[i], 4);
         fence_mbar_init();
     }
     if (warp == 9) tmem_alloc_pair<kPairTmemCols>(&bar->tmem_base);
@@ -221,8 +219,9 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
                         PTRACE(j, 2, (threadIdx.x & 31) == 0);
                         mbar_wait(&bar->v_full[st], (j / kPStages) & 1);
                         tc_fence_after();
-                        mma_pair_ts(tm + kColO, tm + kColP + 64u * static_cast<uint32_t>(j & 1),
-                                    vd0 + static_cast<uint64_t>(st) * (kVHalfBytes >> 4), kIdescPairPV, j > 0 ? 1u : 0u);
+                        mma_pair_ts(tm + kColO + 128u * static_cast<uint32_t>(j & 1),
+                                    tm + kColP + 64u * static_cast<uint32_t>(j & 1),
+                                    vd0 + static_cast<uint64_t>(st) * (kVHalfBytes >> 4), kIdescPairPV, j > 1 ? 1u : 0u);
                         mma_commit_pair_warp(&bar->pv_done[j & 3]);
                         mma_commit_pair_warp(&bar->v_empty[st]);
                         PTRACE(j, 3, (threadIdx.x & 31) == 0);
@@ -237,22 +236,24 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
         tile_scalars(nsel, row0, h, g);
         (void)g;
         // ------------------------------------------------ softmax warpgroups
+        // Each warpgroup runs its own online softmax over its blocks (its own
+        // running max m, row sum l and accumulator O_wg in TMEM), so neither
+        // waits on the other; the epilogue merges the two.
         const int wg = warp >> 2;          // takes blocks j = wg, wg + 2, ...
         const int r = threadIdx.x & 127;   // row within this CTA's half == TMEM lane
         const int64_t qrow = row0 + 128 * static_cast<int64_t>(rank) + r;
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const uint32_t s_addr = tmem + lane_base + kColS;
         const uint32_t p_addr = tmem + lane_base + kColP + 64u * static_cast<uint32_t>(wg);
-        const uint32_t o_addr = tmem + lane_base + kColO;
+        const uint32_t o_addr = tmem + lane_base + kColO + 128u * static_cast<uint32_t>(wg);
         const float sl2 = p.scale_log2;
         const int64_t lim = p.causal ? min(qrow, p.n - 1) : p.n - 1;  // last visible key
         const uint32_t s_free_l = leader(&bar->s_free);
         const uint32_t p_full_l = leader(&bar->p_full[rank][wg]);
         const float2 sc2 = make_float2(sl2, sl2);
-        float m = -INFINITY;     // reference max of the last block (log2 domain)
-        float l = 0.0f;          // this warpgroup's row sum, relative to mref
-        float mref = -INFINITY;  // the reference max l is relative to
-        int mine = 0;            // blocks this warpgroup has processed
+        float m = -INFINITY;  // this warpgroup's reference max (log2 domain)
+        float l = 0.0f;       // its row sum, relative to m
+        int mine = 0;         // blocks this warpgroup has processed
         for (int j = wg; j < nsel; j += 2, ++mine) {
             const int64_t key0 = static_cast<int64_t>(sel_at(j)) * kBlock;
             const bool need_mask = key0 + kBlock - 1 > lim;
@@ -280,54 +281,19 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
             for (int c = 0; c < kBlock; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
             const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                    fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
-            // m_{j-1} from the other warpgroup (slot (j-1) mod 4), the lazy rule, publish m_j.
-            float mprev = -INFINITY;
             PTRACE(j, 5, r == 0);
-            if (j >= 1) {
-                mbar_wait(&bar->m_ready[(j - 1) & 3], ((j - 1) >> 2) & 1);
-                mprev = mslot[((j - 1) & 3) * 128 + r];
-            }
-            PTRACE(j, 6, r == 0);
-            m = mprev;
+            // Lazy rule: raise m only when the block max exceeds it by > 2^8.
+            const float mprev = m;
             if (mx > m + kPairRescaleThreshold || (m == -INFINITY && mx > -INFINITY)) m = mx;
-            mslot[(j & 3) * 128 + r] = m;
-            __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(&bar->m_ready[j & 3]);
-            // O holds P(0..j-1)·V relative to mprev: rescale it before P(j)·V(j) when m rose.
-            // (Branches, not selects: an ex2 per row per block would queue behind
-            // the other warpgroup's exponentials on the MUFU.)
             const bool rose = m != mprev && mprev != -INFINITY;
-            if (j >= 1 && __any_sync(0xffffffffu, rose)) {
-                const float alpha = rose ? ex2(mprev - m) : 1.0f;
-                // P(j-1)·V(j-1) done. pv_done has 4 slots (block j -> slot j mod 4,
-                // phase j / 4): a parity wait can only alias to P(j-5)·V(j-5),
-                // which has completed (P·V completions are in order and this
-                // warpgroup saw P(j-4)·V(j-4) complete before storing P(j-2)),
-                // or to P(j+3)·V(j+3), which cannot run before P(j).
-                mbar_wait(&bar->pv_done[(j - 1) & 3], ((j - 1) >> 2) & 1);
-                tc_fence_after();
-#pragma unroll
-                for (int c = 0; c < kHeadDim / 32; ++c) {
-                    uint32_t v[32];
-                    tmem_ld32(o_addr + c * 32, v);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
-                    tmem_st32(o_addr + c * 32, v);
-                }
-            }
-            if (m != mref) {  // bring this warpgroup's row sum to the new reference
-                l = (mref == -INFINITY) ? 0.0f : l * ex2(mref - m);
-                mref = m;
-            }
-            PTRACE(j, 7, r == 0);
             const float msub = (m == -INFINITY) ? 0.0f : m;
             const float2 nm2 = make_float2(-msub, -msub);
             float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#ifndef SHPLB_PAIR_INTERLEAVED
+            PTRACE(j, 6, r == 0);
             // All 128 exponentials first (packed bf16 pairs; the S registers die
-            // as they are consumed), then wait for the P buffer: its last
-            // reader, P(j-2)·V(j-2), runs while this block exponentiates.
+            // as they are consumed), then wait for this warpgroup's last P·V —
+            // P(j-2)·V(j-2), which read its P buffer and accumulated into its O —
+            // while this block exponentiated.
             uint32_t pk[4][16];
 #pragma unroll
             for (int e = 0; e < kBlock / 2; ++e) {
@@ -338,32 +304,29 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
                 sum2[e & 1] = fadd2(sum2[e & 1], pe);
                 pk[e >> 4][e & 15] = pack_bf16x2(pe.x, pe.y);
             }
-            if (mine >= 1) {  // this warpgroup's P buffer was last read by P(j-2)·V(j-2)
+            PTRACE(j, 7, r == 0);
+            if (mine >= 1) {
                 mbar_wait(&bar->pv_done[(j - 2) & 3], ((j - 2) >> 2) & 1);
                 tc_fence_after();
             }
+            // O_wg holds this warpgroup's P·V relative to mprev: rescale it before
+            // P(j)·V(j) accumulates when m rose (rare; branches, not selects: an
+            // ex2 per row per block would queue on the MUFU).
+            if (__any_sync(0xffffffffu, rose)) {
+                const float alpha = rose ? ex2(mprev - m) : 1.0f;
+#pragma unroll
+                for (int c = 0; c < kHeadDim / 32; ++c) {
+                    uint32_t v[32];
+                    tmem_ld32(o_addr + c * 32, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
+                    tmem_st32(o_addr + c * 32, v);
+                }
+            }
+            if (rose) l *= ex2(mprev - m);
 #pragma unroll
             for (int c = 0; c < 4; ++c) tmem_st16(p_addr + c * 16, pk[c]);
-#else
-            if (mine >= 1) {  // this warpgroup's P buffer was last read by P(j-2)·V(j-2)
-                mbar_wait(&bar->pv_done[(j - 2) & 3], ((j - 2) >> 2) & 1);
-                tc_fence_after();
-            }
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t pk[16];
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const float2 x = ffma2(make_float2(s[c * 32 + 2 * e], s[c * 32 + 2 * e + 1]), sc2, nm2);
-                    float2 pe;
-                    pe.x = ex2(x.x);
-                    pe.y = ex2(x.y);
-                    sum2[e & 1] = fadd2(sum2[e & 1], pe);
-                    pk[e] = pack_bf16x2(pe.x, pe.y);
-                }
-                tmem_st16(p_addr + c * 16, pk);
-            }
-#endif
             const float2 sum = fadd2(sum2[0], sum2[1]);
             l += sum.x + sum.y;
             tmem_wait_st();
@@ -373,22 +336,22 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
         }
 
         // -------------------------------------------------------- epilogue
-        // Row sum = both warpgroups' parts brought to the final reference max
-        // m_f (the last published one); O / l staged in this CTA's Q buffer
-        // (free once the last P·V, which follows every S, has completed) —
-        // warpgroup w writes d-chunk w — then stored with bulk tensor copies.
+        // O = (O_0 2^(m_0 - m_f) + O_1 2^(m_1 - m_f)) / (l_0 2^(m_0 - m_f) +
+        // l_1 2^(m_1 - m_f)), m_f = max(m_0, m_1); a warpgroup that had no
+        // block (nsel = 1) or only masked ones (m = -inf) contributes nothing
+        // (its O is never read). Staged in this CTA's Q buffer (free once the
+        // last P·V, which follows every S, has completed) — warpgroup w writes
+        // d-chunk w — then stored with bulk tensor copies.
         lfin[(wg * 2 + 0) * 128 + r] = l;
-        lfin[(wg * 2 + 1) * 128 + r] = mref;
+        lfin[(wg * 2 + 1) * 128 + r] = m;
         named_bar_sync(1, 256);
-        float mf = -INFINITY;
-        if (nsel > 0) mf = mslot[((nsel - 1) & 3) * 128 + r];  // m_ready of the last block: see below
-        float lt = 0.0f;
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-            const float lw = lfin[(w * 2 + 0) * 128 + r], mw = lfin[(w * 2 + 1) * 128 + r];
-            if (mw != -INFINITY) lt += lw * ex2(mw - mf);
-        }
+        const float m0 = lfin[1 * 128 + r], m1 = (nsel > 1) ? lfin[3 * 128 + r] : -INFINITY;
+        const float mf = fmaxf(m0, m1);
+        const float f0 = m0 != -INFINITY ? ex2(m0 - mf) : 0.0f;
+        const float f1 = m1 != -INFINITY ? ex2(m1 - mf) : 0.0f;
+        const float lt = lfin[0 * 128 + r] * f0 + (nsel > 1 ? lfin[2 * 128 + r] * f1 : 0.0f);
         const float inv = lt > 0.0f ? 1.0f / lt : 0.0f;
+        const float g0 = f0 * inv, g1 = f1 * inv;
         const bool live = row0 + 128 * static_cast<int64_t>(rank) < p.n;
         if (nsel > 0) {
             mbar_wait(&bar->pv_done[(nsel - 1) & 3], ((nsel - 1) >> 2) & 1);
@@ -396,26 +359,34 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
         }
         if (live) {
             const uint32_t tile_s = smem_u32(smem + kPSmemQ);
+            const uint32_t o0 = tmem + lane_base + kColO, o1 = o0 + 128u;
 #pragma unroll 1
             for (int cc = 0; cc < 2; ++cc) {
                 const int c = wg * 2 + cc;  // 32-column group of d (warpgroup w: d-chunk w)
-                uint32_t v[32];
-                if (nsel > 0) {
-                    tmem_ld32(o_addr + c * 32, v);
-                    tmem_wait_ld();
-                } else {
+                float v[32];
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) v[e] = 0u;
+                for (int e = 0; e < 32; ++e) v[e] = 0.0f;
+                if (nsel > 0 && m0 != -INFINITY) {
+                    uint32_t t[32];
+                    tmem_ld32(o0 + c * 32, t);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(t[e]) * g0;
+                }
+                if (nsel > 1 && m1 != -INFINITY) {
+                    uint32_t t[32];
+                    tmem_ld32(o1 + c * 32, t);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = fmaf(__uint_as_float(t[e]), g1, v[e]);
                 }
                 const uint32_t row_s = tile_s + static_cast<uint32_t>(wg) * 16384u + static_cast<uint32_t>(r) * 128u;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const uint32_t chunk = static_cast<uint32_t>(cc * 4 + u) ^ static_cast<uint32_t>(r & 7);
-                    sts128(row_s + chunk * 16u,
-                           pack_bf16x2(__uint_as_float(v[u * 8 + 0]) * inv, __uint_as_float(v[u * 8 + 1]) * inv),
-                           pack_bf16x2(__uint_as_float(v[u * 8 + 2]) * inv, __uint_as_float(v[u * 8 + 3]) * inv),
-                           pack_bf16x2(__uint_as_float(v[u * 8 + 4]) * inv, __uint_as_float(v[u * 8 + 5]) * inv),
-                           pack_bf16x2(__uint_as_float(v[u * 8 + 6]) * inv, __uint_as_float(v[u * 8 + 7]) * inv));
+                    sts128(row_s + chunk * 16u, pack_bf16x2(v[u * 8 + 0], v[u * 8 + 1]),
+                           pack_bf16x2(v[u * 8 + 2], v[u * 8 + 3]), pack_bf16x2(v[u * 8 + 4], v[u * 8 + 5]),
+                           pack_bf16x2(v[u * 8 + 6], v[u * 8 + 7]));
                 }
             }
             fence_proxy_async_smem();
