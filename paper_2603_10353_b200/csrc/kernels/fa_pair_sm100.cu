@@ -64,6 +64,11 @@ constexpr uint32_t kColS = 0, kColP = 128, kColO = 256;  // P_w at kColP + 64 w,
 constexpr uint32_t kIdescPairS = idesc_bf16_f32(256, 128, 0, 0);   // Q K-major, K K-major
 constexpr uint32_t kIdescPairPV = idesc_bf16_f32(256, 128, 0, 1);  // P (TMEM), V MN-major
 constexpr float kPairRescaleThreshold = 8.0f;
+// Control warp roles (warp index; SMSP = warp % 4). A warp blocked issuing
+// tcgen05.mma slows the softmax warps of its SMSP (~300 cycles per block on
+// the leader CTA, measured with SHPLB_PTRACE); moving the issuers to other
+// SMSPs only moves the lag (profiles/r02/k3_pair_tuning.txt).
+constexpr int kWarpQK = 8, kWarpS = 9, kWarpV = 10, kWarpPV = 11;
 
 struct __align__(8) PairBarriers {
     uint64_t q_full;                                // leader: both CTAs' Q landed
@@ -94,8 +99,8 @@ constexpr int kPTraceBlocks = 32;
 
 __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_constant__ FaParams p) {
 #ifdef SHPLB_PTRACE
-    __shared__ long long ptrace[kPTraceBlocks][10];
-    for (int i = threadIdx.x; i < kPTraceBlocks * 10; i += kPThreads) ptrace[i / 10][i % 10] = 0;
+    __shared__ long long ptrace[kPTraceBlocks][12];
+    for (int i = threadIdx.x; i < kPTraceBlocks * 12; i += kPThreads) ptrace[i / 12][i % 12] = 0;
 #endif
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -158,7 +163,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
         int nsel, h, g;
         int64_t row0;
         tile_scalars(nsel, row0, h, g);
-        if (warp == 8) {
+        if (warp == kWarpQK) {
             // ---------------------------------------- TMA producer: Q and K
             // (K and V have separate producers: a V load waits for the P·V four
             // blocks back, which must not hold up the K loads S runs on.)
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
                                        sel_at(j) * kBlock + 64 * static_cast<int>(rank), g, 2, 8192);
                 }
             }
-        } else if (warp == 10) {
+        } else if (warp == kWarpV) {
             // ----------------------------------------------- TMA producer: V
             for (int j = 0; j < nsel; ++j) {
                 const int st = j % kPStages;
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
                 tma_load_pair_warp(smem + kPSmemV + st * kVHalfBytes, &p.tm_v, leader(&bar->v_full[st]),
                                    64 * static_cast<int>(rank), sel_at(j) * kBlock, g, 1, 0);
             }
-        } else if (warp == 9 || warp == 11) {
+        } else if (warp == kWarpS || warp == kWarpPV) {
             // ----------------------------- MMA issuers (leader only): warp 9 issues
             // the S stream, warp 11 the P·V stream. tcgen05.mma issue blocks while
             // the tensor pipe is full, so one thread issuing both streams in a fixed
@@ -195,7 +200,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
             // barriers (a commit tracks the committing thread's MMAs).
             if (rank == 0 && nsel > 0) {
                 const uint32_t tm = __shfl_sync(0xffffffffu, static_cast<uint32_t>(lds_s32(smem_u32(&bar->tmem_base))), 0);
-                if (warp == 9) {
+                if (warp == kWarpS) {
                     const uint64_t qd = umma_desc_sw128(smem_u32(smem + kPSmemQ), 16, 1024);
                     const uint64_t kd0 = umma_desc_sw128(smem_u32(smem + kPSmemK), 16, 1024);
                     mbar_wait(&bar->q_full, 0);
@@ -330,7 +335,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
             const float2 sum = fadd2(sum2[0], sum2[1]);
             l += sum.x + sum.y;
             tmem_wait_st();
-            PTRACE(j, 8, r == 0);
+            PTRACE(j, 8 + (warp & 3), (threadIdx.x & 31) == 0);  // P stored, per warp
             tc_fence_before();
             mbar_arrive_cluster_warp(p_full_l);
         }
@@ -416,9 +421,10 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
         printf("PTRACE rank %d\n", rr);
         printf("PTRACE nsel %d\n", p.cnt[(p.tiles[blockIdx.x >> 1] >> 20) * (int64_t)p.nqb + (p.tiles[blockIdx.x >> 1] & 0xFFFFF)]);
         for (int j = 0; j < kPTraceBlocks; ++j)
-            printf("PTRACE j %d mma sfree %lld s_iss %lld pfull %lld vfull %lld | sm sfull %lld max %lld mrdy %lld exp0 %lld pst %lld\n", j,
+            printf("PTRACE j %d mma sfree %lld s_iss %lld pfull %lld vfull %lld | sm sfull %lld max %lld mdec %lld expd %lld pst %lld %lld %lld %lld\n", j,
                    ptrace[j][0] - t0, ptrace[j][1] - t0, ptrace[j][2] - t0, ptrace[j][3] - t0, ptrace[j][4] - t0,
-                   ptrace[j][5] - t0, ptrace[j][6] - t0, ptrace[j][7] - t0, ptrace[j][8] - t0);
+                   ptrace[j][5] - t0, ptrace[j][6] - t0, ptrace[j][7] - t0, ptrace[j][8] - t0,
+                   ptrace[j][9] - t0, ptrace[j][10] - t0, ptrace[j][11] - t0);
     }
     }
 #endif
