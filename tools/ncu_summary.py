@@ -1,7 +1,7 @@
 """Summarise one kernel launch of an ncu report into the JSON kept under
 profiles/ (dev tool; reads the report with `ncu -i`, no GPU needed).
 
-usage: python tools/ncu_summary.py <report.ncu-rep> <out.json> "<what>" [algorithmic_bytes]
+usage: python tools/ncu_summary.py <report.ncu-rep> <out.json> "<what>" [algorithmic_bytes] [kernel substring]
 """
 import csv
 import io
@@ -32,11 +32,14 @@ SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 def main():
     rep, out, what = sys.argv[1], sys.argv[2], sys.argv[3]
-    alg = float(sys.argv[4]) if len(sys.argv) > 4 else None
+    alg = float(sys.argv[4]) if len(sys.argv) > 4 and float(sys.argv[4]) > 0 else None
+    want = sys.argv[5] if len(sys.argv) > 5 else ""
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], check=True,
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
-    head, units, vals = rows[0], rows[1], rows[2]
+    head, units = rows[0], rows[1]
+    ik = head.index("Kernel Name")
+    vals = next(r for r in rows[2:] if want in r[ik])
     got, unit = {}, {}
     for m in METRICS:
         if m in head:
