@@ -211,7 +211,9 @@ constexpr int kSelThreads = 256;  // standalone selector: 8 warps, one row each
 constexpr int kPad = kHeadDim + 4;  // row stride (floats) of the Q / K tiles: 16-byte rows, no bank conflicts
 
 // Kernel 2 (score + select). One CTA = one GROUP of up to 4 q heads that read
-// the same kv head (GQA) x Q = 64 / G consecutive query blocks: 64 row slots
+// the same kv head (GQA) x Q = 64, 32, 16, 16 consecutive query blocks for
+// G = 1, 2, 3, 4 (powers of two: the slot -> (head, query block) map is
+// shifts and masks; a group of 3 leaves 16 of the slots idle): 64 row slots
 // share every pooled K chunk the CTA stages in shared memory (G x fewer K
 // loads than one head per CTA). 512 threads; thread (rp, kq) holds an 8 x 4
 // FFMA register tile: row slots rp + 8i, key blocks kq + 64j of the 256-block
@@ -233,11 +235,11 @@ constexpr size_t kGrpSmem = sizeof(float) * (kGrpRows + kGrpChunk) * kPad + size
 struct GrpCtx {
     float* scores;
     int64_t nqb, nkb, n, qb0;
-    int bq, causal, Q, G;
+    int bq, causal, Q, G, qshift;  // Q = 2^qshift query blocks per head
     uint32_t heads;  // 4 x 8-bit q head ids
-    __device__ bool valid(int s) const { return s / Q < G && qb0 + s % Q < nqb; }
-    __device__ int head(int s) const { return static_cast<int>((heads >> (8 * (s / Q))) & 0xFFu); }
-    __device__ int64_t qb(int s) const { return qb0 + s % Q; }
+    __device__ bool valid(int s) const { return (s >> qshift) < G && qb0 + (s & (Q - 1)) < nqb; }
+    __device__ int head(int s) const { return static_cast<int>((heads >> (8 * (s >> qshift))) & 0xFFu); }
+    __device__ int64_t qb(int s) const { return qb0 + (s & (Q - 1)); }
 };
 
 // One chunk's tile product for a thread computing NJ of its key blocks, and
@@ -302,7 +304,8 @@ __global__ void __launch_bounds__(kGrpThreads, 1)
     c.bq = bq;
     c.causal = causal;
     c.G = gt.size[blockIdx.x];
-    c.Q = kGrpRows / c.G;
+    c.qshift = c.G == 1 ? 6 : (c.G == 2 ? 5 : 4);  // a group of 3 leaves 16 slots idle
+    c.Q = 1 << c.qshift;
     c.heads = gt.heads[blockIdx.x];
     // Grid (groups, row chunks): the hardware hands out CTAs group-fastest, and
     // y = 0 is the LAST chunk of query blocks, so under the causal mask the
@@ -450,7 +453,7 @@ void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int6
             gt.heads[gi] |= static_cast<uint32_t>(h) << (8 * gt.size[gi]);
             gt.size[gi] += 1;
         }
-        for (int gi = 0; gi < groups; ++gi) min_q = std::min(min_q, kGrpRows / static_cast<int>(gt.size[gi]));
+        for (int gi = 0; gi < groups; ++gi) min_q = std::min(min_q, gt.size[gi] == 1 ? 64 : (gt.size[gi] == 2 ? 32 : 16));
     }
     const dim3 grid(static_cast<unsigned>(groups), static_cast<unsigned>((nqb + min_q - 1) / min_q));
     set_max_dynamic_smem(reinterpret_cast<const void*>(score_select_kernel), static_cast<int>(kGrpSmem));

@@ -434,9 +434,9 @@ def test_zero_q_gives_uniform_weights_over_kept_keys(cuda_ctx):
 @pytest.mark.parametrize("group", ["1", "3"])
 def test_kernel2_group_sizes(group):
     """Kernel 2 scores up to 4 q heads of one kv head per CTA (64 row slots =
-    G heads x 64 / G query blocks); SHPLB_K2_GROUP caps G, so 1 (64 query
-    blocks of one head) and 3 (21 query blocks, a slot left idle, GQA groups
-    split 3 + 1) run the other row mappings on the parity cases of this file,
+    G heads x 64 / 32 / 16 / 16 query blocks for G = 1..4); SHPLB_K2_GROUP
+    caps G, so 1 (64 query blocks of one head) and 3 (16 query blocks, 16
+    slots idle, GQA-4 groups split 3 + 1) run the other row mappings on the parity cases of this file,
     in a subprocess (the switch is read once per process)."""
     import os
     import subprocess
