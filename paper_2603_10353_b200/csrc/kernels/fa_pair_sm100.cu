@@ -89,6 +89,16 @@ constexpr size_t kPSmemBar = kPSmemSel + kMaxSelected * sizeof(int32_t);
 constexpr size_t kPSmemX = kPSmemBar + ((sizeof(PairBarriers) + 15) / 16) * 16;  // l / m [2][2][128]
 constexpr size_t kPSmemTotal = kPSmemX + 4 * 128 * sizeof(float) + 1024;
 
+#ifdef SHPLB_TILETRACE  // dev-only: per-CTA timestamps of every tile (tools/tile_trace.py)
+constexpr int kTTraceCtas = 1 << 16;
+// [cta][0 entry globaltimer, 1 smid | nsel << 32, 2 entry clock64, 3 setup done, 4 first S landed
+//       (warpgroup A), 5 last P·V landed (epilogue), 6 output stored, 7 exit clock64]
+__device__ unsigned long long g_tiletrace[kTTraceCtas][8];
+#define TTRACE(e, v) do { if (blockIdx.x < kTTraceCtas) g_tiletrace[blockIdx.x][(e)] = (v); } while (0)
+#else
+#define TTRACE(e, v) do { } while (0)
+#endif
+
 #ifdef SHPLB_PTRACE  // dev-only: per-block clock64 timeline of cluster SHPLB_PTRACE (leader CTA), printed at exit
 constexpr int kPTraceBlocks = 32;
 #define PTRACE(j, e, cond) \
@@ -101,6 +111,18 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
 #ifdef SHPLB_PTRACE
     __shared__ long long ptrace[kPTraceBlocks][12];
     for (int i = threadIdx.x; i < kPTraceBlocks * 12; i += kPThreads) ptrace[i / 12][i % 12] = 0;
+#endif
+#ifdef SHPLB_TILETRACE
+    if (threadIdx.x == 0) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        TTRACE(0, gt);
+        TTRACE(2, clock64());
+        const int32_t t = p.tiles[blockIdx.x >> 1];
+        TTRACE(1, smid | (static_cast<unsigned long long>(p.cnt[static_cast<int64_t>(t >> 20) * p.nqb + (t & 0xFFFFF)]) << 32));
+    }
 #endif
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -146,6 +168,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
     __syncthreads();
     cluster_sync_all();  // both CTAs' barriers exist before any remote arrive / TMA
     tc_fence_after();
+    if (threadIdx.x == 0) TTRACE(3, clock64());
     const uint32_t tmem = bar->tmem_base;
     auto leader = [&](const uint64_t* b) { return mapa_shared(smem_u32(b), 0); };
 
@@ -266,6 +289,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
             float* s = reinterpret_cast<float*>(sv);
             mbar_wait(&bar->s_full[wg], mine & 1);
             PTRACE(j, 4, r == 0);
+            if (j == 0 && threadIdx.x == 0) TTRACE(4, clock64());
             tc_fence_after();
             tmem_ld32(s_addr + 0, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
             tmem_ld32(s_addr + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
@@ -362,6 +386,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
             mbar_wait(&bar->pv_done[(nsel - 1) & 3], ((nsel - 1) >> 2) & 1);
             tc_fence_after();
         }
+        if (threadIdx.x == 0) TTRACE(5, clock64());
         if (live) {
             const uint32_t tile_s = smem_u32(smem + kPSmemQ);
             const uint32_t o0 = tmem + lane_base + kColO, o1 = o0 + 128u;
@@ -410,6 +435,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
                 }
             }
         }
+        if (threadIdx.x == 0) TTRACE(6, clock64());
     }
 
 #ifdef SHPLB_PTRACE
@@ -435,6 +461,7 @@ __global__ void __launch_bounds__(kPThreads, 1) fa_pair_kernel(const __grid_cons
         tc_fence_after();
         tmem_dealloc_pair<kPairTmemCols>(tmem);
     }
+    if (threadIdx.x == 0) TTRACE(7, clock64());
 }
 
 }  // namespace
@@ -457,3 +484,9 @@ cudaError_t launch_fa_pair(const FaParams& p, int num_tiles, cudaStream_t s) {
 }
 
 }  // namespace shplb::kern
+
+#ifdef SHPLB_TILETRACE
+extern "C" int shplb_debug_tiletrace(void* host, size_t bytes) {
+    return static_cast<int>(cudaMemcpyFromSymbol(host, shplb::kern::g_tiletrace, bytes));
+}
+#endif

@@ -57,33 +57,54 @@ def _time(fn, steps: int, repeats: int = 3) -> float:
     return float(np.median(times))
 
 
-def shard_latency_ms(ctx, q, k, v, shard, steps: int = 3, block_q: int = api.BLOCK_Q, kind=0) -> float:
-    """Device time of one rank's shard (its q heads, the kv heads they read,
-    optional query-block ranges)."""
+def _shard_call(ctx, q, k, v, shard, block_q: int = api.BLOCK_Q, kind=0):
+    """A closure running one rank's shard (its q heads, the kv heads they read,
+    optional query-block ranges) on its own copies of the inputs; None if empty."""
     import torch
     if not shard.heads:
-        return 0.0
+        return None
     ql = q[shard.heads].contiguous()
     kl, vl = k[shard.kv_heads].contiguous(), v[shard.kv_heads].contiguous()
     out = torch.empty_like(ql)
     ranges = getattr(shard, "q_block_range", None)
-    return _time(lambda: ctx.sparse_attention_layer(ql, kl, vl, shard.budgets, out=out, kv_map=shard.kv_map,
-                                                    q_block_range=ranges, block_q=block_q, kind=kind), steps)
+    return lambda: ctx.sparse_attention_layer(ql, kl, vl, shard.budgets, out=out, kv_map=shard.kv_map,
+                                              q_block_range=ranges, block_q=block_q, kind=kind)
+
+
+def shard_latency_ms(ctx, q, k, v, shard, steps: int = 3, block_q: int = api.BLOCK_Q, kind=0) -> float:
+    """Device time of one rank's shard."""
+    fn = _shard_call(ctx, q, k, v, shard, block_q, kind)
+    return 0.0 if fn is None else _time(fn, steps)
+
+
+def shards_latency_ms(ctx, q, k, v, shards, steps: int = 3, rounds: int = 3, block_q: int = api.BLOCK_Q,
+                      kind=0) -> list:
+    """Device time of every rank's shard, timed in turn on this GPU: `rounds`
+    passes over the ranks (each pass times every rank once), median per rank.
+    Interleaving the ranks spreads the power-capped clock's drift over all of
+    them instead of charging a slow stretch to whichever rank ran then."""
+    fns = [_shard_call(ctx, q, k, v, sh, block_q, kind) for sh in shards]
+    times = [[] for _ in fns]
+    for _ in range(rounds):
+        for r, fn in enumerate(fns):
+            if fn is not None:
+                times[r].append(_time(fn, steps, repeats=1))
+    return [float(np.median(t)) if t else 0.0 for t in times]
 
 
 def measured_barrier(ctx, q, k, v, budgets, device_of_head, devices: int, steps: int = 3, kind=0):
     """(per-rank ms, SimulationResult-like barrier/bubble) of a whole-head plan."""
     group = q.shape[0] // k.shape[0]
-    per = [shard_latency_ms(ctx, q, k, v, rank_shard(device_of_head, r, group, budgets), steps, kind=kind)
-           for r in range(devices)]
+    per = shards_latency_ms(ctx, q, k, v, [rank_shard(device_of_head, r, group, budgets) for r in range(devices)],
+                            steps, kind=kind)
     return per, api.barrier(per)
 
 
 def measured_split_barrier(ctx, q, k, v, budgets, devices: int, steps: int = 3, kind=0):
     group = q.shape[0] // k.shape[0]
     sp = api.split_assign(budgets, devices, q.shape[1])
-    per = [shard_latency_ms(ctx, q, k, v, rank_segments(sp, r, group, budgets), steps, kind=kind)
-           for r in range(devices)]
+    per = shards_latency_ms(ctx, q, k, v, [rank_segments(sp, r, group, budgets) for r in range(devices)],
+                            steps, kind=kind)
     return per, api.barrier(per), sp
 
 
