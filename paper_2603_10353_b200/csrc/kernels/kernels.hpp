@@ -61,6 +61,9 @@ struct FaParams {
     const int32_t* idx;
     const int32_t* cnt;
     const int32_t* tiles;  // work list: tile t -> (h << 20) | qb, heaviest first
+    // Persistent kernel only: tile ticket counter (zero at launch) and list length.
+    int32_t* counter;
+    int32_t num_tiles;
     int64_t kmax;
     int64_t n;
     int32_t hq, hkv, nqb;
@@ -84,6 +87,12 @@ void launch_fa(const FaParams& p, int num_tiles, bool dual, cudaStream_t s);
 // The CTA-pair variant (fa_pair_sm100.cu): bq = 256; one 2-CTA cluster per tile,
 // two softmax warpgroups per CTA on alternate key blocks.
 cudaError_t launch_fa_pair(const FaParams& p, int num_tiles, cudaStream_t s);
+// The persistent CTA-pair variant (fa_persist_sm100.cu): num_clusters resident
+// clusters taking tiles of p.tiles in order through the ticket counter p.counter.
+cudaError_t launch_fa_persist(const FaParams& p, int num_clusters, cudaStream_t s);
+// Clusters of the persistent kernel that fit on the device at once (0 if the
+// occupancy query fails).
+int fa_persist_max_clusters();
 
 // GPU recovery-curve profiler (profiler.cu). q_rows bf16 [hq][n_rows][128],
 // k bf16 [hkv][n_k][128]; units = hq * n_rows.

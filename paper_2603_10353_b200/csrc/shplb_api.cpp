@@ -14,6 +14,7 @@
 #include <map>
 #include <mutex>
 #include <numeric>
+#include <queue>
 #include <string>
 #include <vector>
 
@@ -289,6 +290,8 @@ struct shplb_ctx {
     std::vector<std::pair<int32_t*, cudaEvent_t>> host_graveyard;
     WorkList* current = nullptr;
     uint64_t lru_clock = 0;
+    int32_t* tickets = nullptr;  // persistent kernel 3's ticket counters (kTicketRing)
+    uint64_t ticket_seq = 0;
     size_t work_list_cap = 256;
     // Stage timing: 4 events per recorded layer call (before k1, after k1,
     // after k2, after k3); `timed_calls` sets in use since the last read.
@@ -412,13 +415,22 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
 // warpgroups per CTA on alternate key blocks (C3 bench: 45.6 vs 46.1 ms per
 // layer); "single" = fa_sm100.cu, one CTA with two query halves
 // ping-ponging (also the block_q = 128 kernel).
+// "persist" = fa_persist_sm100.cu, the CTA-pair kernel as one resident
+// cluster per SM pair walking a host-built (LPT) tile list.
 int k3_variant() {
     static const int v = [] {
         const char* e = std::getenv("SHPLB_K3");
-        return (e && std::string(e) == "single") ? 0 : 1;
+        if (e && std::string(e) == "single") return 0;
+        if (e && std::string(e) == "persist") return 2;
+        return 1;
     }();
     return v;
 }
+
+// Tile-ticket counters of the persistent kernel 3: one per launch from a ring,
+// zeroed on the launch's stream, so launches of one context in flight on
+// different streams never share a counter.
+constexpr int kTicketRing = 64;
 
 // block_q = 128: two query blocks per kernel-3 CTA (each with its own selection
 // and K / V stream, fa_sm100.cu kDual). SHPLB_DUAL=0 (diagnostic) restores one
@@ -536,6 +548,7 @@ void build_tiles(shplb_ctx* ctx, const shplb_layer_shape* s, const std::vector<i
     for (size_t i = 0; i < order.size(); ++i) sorted[i] = tiles[order[i]];
     shplb_ctx::WorkList wl;
     wl.num_tiles = static_cast<int>(sorted.size());
+
     SHPLB_CUDA(cudaEventCreateWithFlags(&wl.last_use, cudaEventDisableTiming));
     if (!sorted.empty()) {
         const size_t bytes = sizeof(int32_t) * sorted.size();
@@ -559,7 +572,8 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     p.tm_q = make_tmap(q, s->num_q_heads, s->seq_len);
     p.tm_k = make_tmap(k, s->num_kv_heads, s->seq_len);
     p.tm_v = make_tmap(v, s->num_kv_heads, s->seq_len);
-    const bool pair = s->block_q == 256 && k3_variant() == 1;
+    const bool pair = s->block_q == 256 && k3_variant() >= 1;
+    const bool persist = s->block_q == 256 && k3_variant() == 2;
     if (pair) p.tm_k_half = make_tmap(k, s->num_kv_heads, s->seq_len, 64);
     p.out = out;
     p.idx = idx;
@@ -585,7 +599,17 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     }
     p.scale_log2 = static_cast<float>((1.0 / std::sqrt(static_cast<double>(s->head_dim))) * 1.4426950408889634);
     if (ctx->current->num_tiles > 0) {
-        if (pair)
+        if (persist) {
+            const int maxc = kern::fa_persist_max_clusters();
+            if (maxc < 1) throw CudaError("kernel 3 (persistent): no cluster fits on the device");
+            if (!ctx->tickets) SHPLB_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->tickets), kTicketRing * sizeof(int32_t)));
+            p.counter = ctx->tickets + (ctx->ticket_seq++ % kTicketRing);
+            p.num_tiles = ctx->current->num_tiles;
+            SHPLB_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st));
+            SHPLB_CUDA(kern::launch_fa_persist(p, std::min(maxc, p.num_tiles), st));
+        } else if (pair)
+            SHPLB_CUDA(kern::launch_fa_pair(p, ctx->current->num_tiles, st));
+        else if (pair)
             SHPLB_CUDA(kern::launch_fa_pair(p, ctx->current->num_tiles, st));
         else
             kern::launch_fa(p, ctx->current->num_tiles, dual_mode(s), st);
@@ -648,6 +672,7 @@ int shplb_ctx_destroy(shplb_ctx* ctx) {
         cudaFree(ctx->host_io);
         cudaFree(ctx->dense_idx);
         cudaFree(ctx->dense_cnt);
+        cudaFree(ctx->tickets);
         cudaFree(ctx->prof_scores);
         cudaFree(ctx->ca_ws);
         cudaFree(ctx->k2_ws);

@@ -2,6 +2,8 @@
 
 usage: SHPLB_LIB=<SHPLB_TILETRACE build of the pair kernel> python tools/tile_trace.py [out.json]
 (build: K3=pair tools/build_variants.sh tt "-DSHPLB_TILETRACE")
+   or: SHPLB_K3=persist SHPLB_LIB=<trace build of the persistent kernel> python tools/tile_trace.py --persist [out.json]
+(build: K3=persist tools/build_variants.sh ttp "-DSHPLB_TILETRACE")
 
 Runs the C3 128K layer (the bench's layer-0 inputs and max-min table), reads the per-CTA
 timestamps the trace build records (entry, setup done, first S landed, last P.V landed,
@@ -27,6 +29,9 @@ from paper_2603_10353_b200 import _native  # noqa: E402
 from paper_2603_10353_b200.calibrate import layer_budgets  # noqa: E402
 from paper_2603_10353_b200.workload import LayerSpec, make_layer  # noqa: E402
 
+persist = "--persist" in sys.argv
+if persist:
+    sys.argv.remove("--persist")
 n = int(os.environ.get("TUNE_N", "131072"))
 q, k, v = make_layer(LayerSpec(seq_len=n, seed=2603), "cuda")
 ctx = P.Context(0)
@@ -35,6 +40,8 @@ out = torch.empty_like(q)
 for _ in range(3):
     ctx.sparse_attention_layer(q, k, v, budgets, out=out)
 torch.cuda.synchronize()
+if persist:
+    assert C.CDLL(_native.LIB_PATH).shplb_debug_tiletrace_persist_clear() == 0
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
 e0.record()
 ctx.sparse_attention_layer(q, k, v, budgets, out=out)
@@ -43,6 +50,47 @@ torch.cuda.synchronize()
 layer_ms = e0.elapsed_time(e1)
 
 lib = C.CDLL(_native.LIB_PATH)
+if persist:
+    # per tile (schedule order): first S landed, last P.V landed, epilogue done, smid | nsel << 32
+    buf = np.zeros((1 << 16, 12), dtype=np.uint64)  # [cluster * 512 + tile of the cluster]
+    assert lib.shplb_debug_tiletrace_persist(buf.ctypes.data_as(C.c_void_p), C.c_size_t(buf.nbytes)) == 0
+    t = buf[buf[:, 3] != 0].astype(np.int64)
+    ntile = len(t)
+    s0, pv, ep = t[:, 0], t[:, 1], t[:, 2]
+    smid, nsel = t[:, 3] & 0xFFFFFFFF, t[:, 3] >> 32
+    steady = pv - s0
+    A = np.stack([np.ones(ntile), nsel], 1).astype(np.float64)
+    coef, *_ = np.linalg.lstsq(A, steady.astype(np.float64), rcond=None)
+    bound, spans, parts = [], [], []
+    for sm in np.unique(smid):
+        o = np.where(smid == sm)[0]
+        o = o[np.argsort(s0[o])]
+        bound.extend((s0[o[1:]] - pv[o[:-1]]).tolist())  # last P.V of a tile -> first S of the next seen
+        spans.append(ep[o[-1]] - s0[o[0]])
+        a, b = o[:-1], o[1:]  # previous tile, next tile; times relative to the previous tile's last P.V
+        parts.append(np.stack([t[a, 2] - pv[a], t[a, 4] - pv[a], t[b, 7] - pv[a], t[b, 5] - pv[a],
+                               t[b, 6] - pv[a], s0[b] - pv[a], t[b, 8] - pv[a], t[b, 9] - pv[a],
+                               t[b, 10] - pv[a], t[a, 11] - pv[a]], 1))
+    parts = np.concatenate(parts)
+    boundary_detail = dict(zip(["staged", "stored", "next_q_issued", "next_q_seen_by_s_issuer",
+                                "next_s0_issued", "next_s0_seen_by_softmax", "next_s0_past_s_free",
+                                "next_s0_past_k_full", "next_k0_issued", "last_s_issued"],
+                               [float(np.median(parts[:, i])) for i in range(parts.shape[1])]))
+    res = {"layer_ms": layer_ms, "tiles": int(ntile), "leader_sms": int(len(spans)),
+           "fit_steady_cycles": {"per_tile": float(coef[0]), "per_block": float(coef[1])},
+           "mean_cycles_per_tile": {"steady": float(steady.mean()), "epilogue": float((ep - pv).mean()),
+                                    "boundary_last_pv_to_next_first_s": float(np.mean(bound))},
+           "boundary_median_cycles_after_last_pv": boundary_detail,
+           "share_of_span": {"steady": float(steady.sum() / np.sum(spans)),
+                             "boundaries": float(np.sum(bound) / np.sum(spans))},
+           "span_cycles": {"mean": float(np.mean(spans)), "min": float(np.min(spans)), "max": float(np.max(spans))},
+           "steady_cycles_per_block_total": float(steady.sum() / nsel.sum())}
+    print(json.dumps(res, indent=1))
+    if len(sys.argv) > 1:
+        with open(sys.argv[1], "w") as f:
+            json.dump(res, f, indent=1)
+        np.save(sys.argv[1].replace(".json", ".npy"), t)
+    sys.exit(0)
 ncta = 2 * int(np.ceil(n / 256)) * 32
 buf = np.zeros((1 << 16, 8), dtype=np.uint64)
 rc = lib.shplb_debug_tiletrace(buf.ctypes.data_as(C.c_void_p), C.c_size_t(buf.nbytes))
