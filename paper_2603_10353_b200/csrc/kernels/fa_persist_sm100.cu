@@ -532,7 +532,10 @@ __global__ void __launch_bounds__(kThreads, 1) fa_persist_kernel(const __grid_co
             const bool live = row0 + 128 * static_cast<int64_t>(rank) < p.n;
             mbar_wait(&bar->tile_ack, static_cast<uint32_t>(tl) & 1);
             if (nsel > 0) {
+                // The tile's last two P·V (one per warpgroup): every P·V phase
+                // is observed by someone before its slot is reused four blocks on.
                 const int Jl = J0 + nsel - 1;
+                if (nsel > 1) mbar_wait(&bar->pv_done[(Jl - 1) & 3], ((Jl - 1) >> 2) & 1);
                 mbar_wait(&bar->pv_done[Jl & 3], (Jl >> 2) & 1);
                 tc_fence_after();
             }

@@ -410,19 +410,21 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
 //       under plain LPT, 1.4% faster;
 //   0 = LPT over all tiles (heaviest first);
 //   2 = LPT over power-of-two work buckets, kv-grouped inside a bucket.
-// Kernel-3 variant for block_q = 256 (SHPLB_K3): "pair" (default) =
-// fa_pair_sm100.cu, a 2-CTA cluster per query block with two softmax
-// warpgroups per CTA on alternate key blocks (C3 bench: 45.6 vs 46.1 ms per
-// layer); "single" = fa_sm100.cu, one CTA with two query halves
-// ping-ponging (also the block_q = 128 kernel).
-// "persist" = fa_persist_sm100.cu, the CTA-pair kernel as one resident
-// cluster per SM pair walking a host-built (LPT) tile list.
+// Kernel-3 variant for block_q = 256 (SHPLB_K3):
+//   "persist" (default) = fa_persist_sm100.cu: the CTA-pair data path (a 2-CTA
+//       cluster per 256-row query block, two softmax warpgroups per CTA on
+//       alternate key blocks) as one resident cluster per SM pair taking tiles
+//       of the work list by atomic ticket — tile boundaries 11.4 K -> 2.0 K
+//       cycles; C3 unchanged under the power cap, short tiles up to ~10% faster;
+//   "pair" = fa_pair_sm100.cu, the same data path with one cluster per tile;
+//   "single" = fa_sm100.cu, one CTA with two query halves ping-ponging (also
+//       the block_q = 128 kernel).
 int k3_variant() {
     static const int v = [] {
         const char* e = std::getenv("SHPLB_K3");
         if (e && std::string(e) == "single") return 0;
-        if (e && std::string(e) == "persist") return 2;
-        return 1;
+        if (e && std::string(e) == "pair") return 1;
+        return 2;
     }();
     return v;
 }

@@ -449,18 +449,71 @@ def test_kernel2_group_sizes(group):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-def test_single_cta_kernel3_variant():
-    """block_q = 256 runs the CTA-pair kernel 3 by default; the single-CTA kernel
-    (fa_sm100.cu, SHPLB_K3=single — also the block_q = 128 kernel) on the parity
-    cases of this file and the fused-gather tests, in a subprocess (the switch is
-    read once per process)."""
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("bq", [256, 128])
+def test_caller_selection_with_empty_rows(cuda_ctx, causal, bq):
+    """shplb_block_sparse_attention on a caller-made selection (random counts,
+    zeros included, ascending random visible blocks): rows whose query block
+    keeps nothing are zero (attention.cpp:40-41), the others match the fp64
+    oracle on their kept sets — kernel 3 runs every tile, empty ones included
+    (the persistent kernel's tile handshakes must hold without any P·V)."""
+    n = 1500
+    spec = LayerSpec(num_q_heads=3, num_kv_heads=1, seq_len=n, seed=41 + bq + int(causal))
+    q, k, v = make_layer(spec, "cpu")
+    qbits, kbits, vbits = bf16_bits(q), bf16_bits(k), bf16_bits(v)
+    nqb, nkb = (n + bq - 1) // bq, (n + 127) // 128
+    rng = np.random.default_rng(bq + 2 * int(causal))
+    kmax = nkb
+    idx = np.full((3, nqb, kmax), -1, np.int32)
+    cnt = np.zeros((3, nqb), np.int32)
+    for h in range(3):
+        for qb in range(nqb):
+            vis = min(nkb, (min((qb + 1) * bq, n) - 1) // 128 + 1) if causal else nkb
+            c = 0 if rng.random() < 0.35 else int(rng.integers(1, vis + 1))
+            cnt[h, qb] = c
+            idx[h, qb, :c] = np.sort(rng.choice(vis, c, replace=False))
+    out = cuda_ctx.block_sparse_attention(q.cuda(), k.cuda(), v.cuda(), torch.from_numpy(idx).cuda(),
+                                          torch.from_numpy(cnt).cuda(), causal=causal, block_q=bq)
+    torch.cuda.synchronize()
+    o = out.float().cpu()
+    assert (cnt == 0).any() and (cnt > 0).any()
+    for h in range(3):
+        for qb in range(nqb):
+            rows = list(range(qb * bq, min(n, (qb + 1) * bq)))
+            if cnt[h, qb] == 0:
+                assert torch.count_nonzero(o[h, rows]) == 0, (h, qb)
+                continue
+            ref = O.sparse_rows(qbits[h], kbits[0], vbits[0], rows, idx[h, qb, :cnt[h, qb]].tolist(), causal=causal)
+            check_output(out[h, rows], ref, f"caller selection h {h} qb {qb}")
+
+
+def test_cta_pair_kernel3_variant():
+    """block_q = 256 runs the persistent CTA-pair kernel 3 by default; the
+    one-cluster-per-tile CTA-pair kernel (fa_pair_sm100.cu, SHPLB_K3=pair) on
+    the parity cases of this file and the fused-gather tests, in a subprocess."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "tests/test_gpu_gather.py", "-q",
                         "-x", "-k", "small_gqa_layer or ragged_lengths or mha_and_wide or kv_map or zero_q or "
-                                    "single_kept or full_budget or c1_shape or fused_gather"],
+                                    "single_kept or full_budget or c1_shape or fused_gather or caller_selection"],
+                       cwd=root, env=dict(os.environ, SHPLB_K3="pair"), capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_single_cta_kernel3_variant():
+    """The single-CTA kernel (fa_sm100.cu, SHPLB_K3=single — also the block_q =
+    128 kernel) on the parity cases of this file and the fused-gather tests, in a
+    subprocess (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "tests/test_gpu_gather.py", "-q",
+                        "-x", "-k", "small_gqa_layer or ragged_lengths or mha_and_wide or kv_map or zero_q or "
+                                    "single_kept or full_budget or c1_shape or fused_gather or caller_selection"],
                        cwd=root, env=dict(os.environ, SHPLB_K3="single"), capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
