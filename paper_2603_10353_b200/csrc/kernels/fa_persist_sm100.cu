@@ -456,6 +456,26 @@ __global__ void __launch_bounds__(kThreads, 1) fa_persist_kernel(const __grid_co
                 tmem_wait_ld();
                 tc_fence_before();
                 mbar_arrive_cluster_warp(s_free_l);  // the leader may now compute the next S over it
+#ifdef SHPLB_DIAG_NOSOFTMAX  // dev-only diagnostic (wrong results): S loaded, P stored, no softmax math
+                {
+                    uint32_t pk[4][16];
+#pragma unroll
+                    for (int e = 0; e < kBlock / 2; ++e) pk[e >> 4][e & 15] = sv[2 * e] ^ sv[2 * e + 1];
+                    if (mine >= 1) {
+                        mbar_wait(&bar->pv_done[(J - 2) & 3], ((J - 2) >> 2) & 1);
+                        tc_fence_after();
+                    }
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) tmem_st16(p_addr + c * 16, pk[c]);
+                    tmem_wait_st();
+                    tc_fence_before();
+                    mbar_arrive_cluster_warp(p_full_l);
+                    m = 0.0f;
+                    l = 1.0f;
+                    (void)need_mask;
+                    continue;
+                }
+#endif
                 if (need_mask) {
 #pragma unroll
                     for (int c = 0; c < kBlock; ++c)
@@ -480,8 +500,12 @@ __global__ void __launch_bounds__(kThreads, 1) fa_persist_kernel(const __grid_co
                 for (int e = 0; e < kBlock / 2; ++e) {
                     const float2 x = ffma2(make_float2(s[2 * e], s[2 * e + 1]), sc2, nm2);
                     float2 pe;
+#ifdef SHPLB_DIAG_NOEXP  // dev-only energy/timing diagnostic (wrong results): no MUFU
+                    pe = x;
+#else
                     pe.x = ex2(x.x);
                     pe.y = ex2(x.y);
+#endif
                     sum2[e & 1] = fadd2(sum2[e & 1], pe);
                     pk[e >> 4][e & 15] = pack_bf16x2(pe.x, pe.y);
                 }

@@ -2,7 +2,8 @@
 
 usage: python tools/tune_fa.py lib1.so[:block_q] lib2.so ...   (each a full libshplb variant)
 Each variant runs in a fresh subprocess (SHPLB_LIB=<path>) on the C3 128K layer with
-the bench's max-min budget table; prints ms per layer and per-stage ms.
+the bench's max-min budget table; prints ms per layer, per-stage ms, SM clock, and the
+board energy per layer from the NVML energy counter (at the power cap, time follows energy).
 """
 import json
 import os
@@ -36,11 +37,19 @@ import subprocess
 smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw", "--format=csv,noheader,nounits",
                         "-lms", "100"], stdout=subprocess.PIPE, text=True)
 e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+try:
+    import pynvml
+    pynvml.nvmlInit()
+    nvh = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    mj0 = pynvml.nvmlDeviceGetTotalEnergyConsumption(nvh)
+except Exception:
+    nvh = None
 e0.record()
 for _ in range(%(steps)d):
     ctx.sparse_attention_layer(q, k, v, budgets, out=out, **kw)
 e1.record()
 torch.cuda.synchronize()
+joules = (pynvml.nvmlDeviceGetTotalEnergyConsumption(nvh) - mj0) / 1e3 / %(steps)d if nvh is not None else None
 smi.terminate()
 vals = [l.split(",") for l in smi.communicate()[0].strip().splitlines() if "," in l]
 clk = sorted(float(a) for a, b in vals) if vals else [0.0]
@@ -50,7 +59,8 @@ tiles, flops = P.layer_work(32, 8, n, budgets)
 print(json.dumps({"ms": e0.elapsed_time(e1) / %(steps)d, "k3_ms": st[2], "k2_ms": st[1],
                   "k1_ms": st[0], "k3_tflops": flops / st[2] / 1e9,
                   "sm_mhz": clk[len(clk) // 2], "power_w": pw[len(pw) // 2],
-                  "k3_mcycles": st[2] * clk[len(clk) // 2] / 1e3}))
+                  "k3_mcycles": st[2] * clk[len(clk) // 2] / 1e3, "joules_per_layer": joules,
+                  "avg_power_w": joules / (e0.elapsed_time(e1) / %(steps)d / 1e3) if joules else None}))
 """
 
 
