@@ -93,9 +93,10 @@ def parse_args():
     p.add_argument("--policy", choices=["per_query_topk", "column_aggregate_topk"], default="per_query_topk",
                    help="selection policy (SelectionKind) of the profile and the layer: per (head, query "
                         "block) top-k blocks, or one kept block set per head (block granularity)")
-    p.add_argument("--placement", choices=["greedy", "split"], default="greedy",
+    p.add_argument("--placement", choices=["greedy", "greedy_refined", "split"], default="greedy",
                    help="N>1 headline plan: 'greedy' = the reference's whole-head greedy_assign (LPT on "
-                        "budgets, bit-exact); 'split' = the sub-head balancer (shplb_plan_split). "
+                        "budgets, bit-exact); 'greedy_refined' = greedy on tile cost + whole-head local "
+                        "search (shplb_plan_refine); 'split' = the sub-head balancer (shplb_plan_split). "
                         "All plans are timed and reported either way")
     p.add_argument("--force-gather", action="store_true",
                    help="validation: run the overlapped all-gather pipeline even at N=1 (1-rank NCCL group)")
@@ -770,8 +771,11 @@ def budgets_desc(args):
 
 PLACEMENTS = {
     "greedy": ("greedy (LPT) whole-head plan (greedy_assign, bit-exact with the reference); even head "
-               "parallelism (naive_even_hp), greedy on tile cost (greedy_tile_cost) and the sub-head "
-               "balancer (split_subhead) are timed alongside"),
+               "parallelism (naive_even_hp), greedy on tile cost (greedy_tile_cost), its whole-head "
+               "refinement (greedy_refined) and the sub-head balancer (split_subhead) are timed alongside"),
+    "greedy_refined": ("whole-head plan: greedy_assign on kernel 3's tile cost per head, refined by moves / "
+                       "swaps of heads off the most loaded rank (shplb_plan_refine); the reference's greedy plan, "
+                       "even head parallelism and the sub-head balancer are timed alongside"),
     "split": ("sub-head balancer (shplb_plan_split): heads in index order with exact tile costs, cut "
               "McNaughton-style at query-block boundaries, at most D-1 heads split; the reference's "
               "whole-head greedy plan is timed alongside (greedy_whole_head)"),
@@ -906,6 +910,8 @@ def main():
     if world > 1:
         plans_l["naive"] = [P.naive_assign(b, world) for b in budgets_l]
         plans_l["greedy_tiles"] = [P.greedy_assign(P.tile_costs(b, n), world) for b in budgets_l]
+        plans_l["greedy_refined"] = [P.refine_assign(P.tile_costs(b, n), world, g)
+                                     for b, g in zip(budgets_l, plans_l["greedy_tiles"])]
         plans_l["split"] = [P.split_assign(b, world, n) for b in budgets_l]
     headline = args.placement if world > 1 else "greedy"  # at N = 1 every plan is the whole layer
     results = {}
@@ -1073,6 +1079,13 @@ def main():
                                     "speedup_vs_even_hp": round(_vg(nv) / _vg(gt), 4),
                                     "plan": "greedy_assign on kernel 3's causal tile cost per head "
                                             "(api.tile_costs) instead of budgets (SURVEY a11 extension)"}
+        grf = results["greedy_refined"]
+        line["greedy_refined"] = {"ms": round(_vg(grf), 3), "compute_only_ms": round(grf["ms"], 3),
+                                  "bubble": round(grf["bubble"], 4),
+                                  "per_rank_ms": [round(x, 3) for x in grf["per_rank_ms"]],
+                                  "speedup_vs_even_hp": round(_vg(nv) / _vg(grf), 4),
+                                  "plan": "greedy_tile_cost refined by whole-head moves / swaps off the "
+                                          "most loaded rank (shplb_plan_refine), an extension"}
         line["gather"] = ("every layer's [Hq, n, d] output reassembled on every rank by shplb_gather_segments "
                           "(one NCCL broadcast per output segment from its owner, one group per layer) on a "
                           "communication stream, overlapped with the next layer's compute"
@@ -1088,7 +1101,8 @@ def main():
         line["per_rank_projection"] = {
             "what": ("layer 0: every rank's shard timed in turn on this GPU (CUDA events, median of 3); "
                      "barrier = max over ranks, bubble = 1 - mean/max (simulator.cpp:40-44); "
-                     "naive = even head parallelism, greedy = S-HPLB greedy_assign, greedy_tiles = greedy_assign on tile cost, split = sub-head "
+                     "naive = even head parallelism, greedy = S-HPLB greedy_assign, greedy_tiles = greedy_assign on tile cost, greedy_refined = greedy_tiles + "
+                     "whole-head local search (shplb_plan_refine), split = sub-head "
                      "balancer; gathers excluded"),
             "degrees": projection}
     line["cpu_baseline"] = cpu

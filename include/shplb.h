@@ -162,6 +162,19 @@ int shplb_plan_greedy(const int64_t* budgets, int32_t num_heads, int32_t devices
  * (same message). */
 int shplb_plan_optimal(const int64_t* budgets, int32_t num_heads, int32_t devices, int32_t* device_of_head);
 
+/* Whole-head refinement (extension beyond greedy_assign, partitioner.cpp:164-183;
+ * the reference's exact optimal_assign is guarded to N <= 24 heads, 4 devices).
+ * device_of_head (in/out) is improved by local search on the per-head costs
+ * (e.g. kernel-3 tile costs): while some move of a head off the most loaded
+ * device, or swap with a lighter head on another device, lowers the max load of
+ * the two devices below the current maximum, apply the best such step (ties: head
+ * index, device index, move before swap, all ascending). Deterministic; every
+ * step strictly lowers the sum of squared loads. C3 layer 0 at D = 8 (tile
+ * costs): greedy 8.9% -> 2.3% modelled bubble. loads_out[devices] (may be NULL):
+ * the refined per-device costs. */
+int shplb_plan_refine(const int64_t* costs, int32_t num_heads, int32_t devices,
+                      int32_t* device_of_head, int64_t* loads_out);
+
 /* Sub-head balancer (an extension beyond greedy_assign,
  * partitioner.cpp:164-183). Whole-head placement cannot balance 32 or 28
  * heads over 8 GPUs under max-min budgets; this plan lets a head's query

@@ -6,7 +6,7 @@ from ._native import (CudaError, InvalidArgument, LogicError, NcclError, NotSupp
                       ShplbRuntimeError, build, lib)
 from .api import (BLOCK, BLOCK_Q, BLOCK_TOPK, COLUMN_AGGREGATE_TOPK, HEAD_DIM, BudgetAllocation, Context, LoadReport, RecoveryCurve,
                   NcclComm, OutSegment, SimulationResult, barrier, plan_segments, default_budget_grid, greedy_assign, imbalance,
-                  layer_work, maxmin_allocate, naive_assign, optimal_assign, profile_curves, simulate,
+                  layer_work, maxmin_allocate, naive_assign, optimal_assign, profile_curves, refine_assign, simulate,
                   selection_kind, split_assign, tile_costs, top_p_budgets, uniform_allocate)
 from . import formats  # noqa: E402  (allocation / assignment / profiles JSON, reference layout)
 from . import experiments  # noqa: E402  (sweep / skyline on measured latency)
@@ -18,5 +18,5 @@ __all__ = [
     "barrier", "build", "default_budget_grid", "greedy_assign", "imbalance", "layer_work", "lib",
     "maxmin_allocate", "naive_assign", "optimal_assign", "profile_curves", "simulate", "split_assign",
     "uniform_allocate", "top_p_budgets", "selection_kind", "BLOCK_TOPK", "COLUMN_AGGREGATE_TOPK",
-    "NcclComm", "NcclError", "OutSegment", "plan_segments", "tile_costs",
+    "NcclComm", "NcclError", "OutSegment", "plan_segments", "tile_costs", "refine_assign",
 ]

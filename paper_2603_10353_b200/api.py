@@ -173,6 +173,21 @@ def greedy_assign(budgets, devices: int) -> np.ndarray:
     return out
 
 
+def refine_assign(costs, devices: int, device_of_head=None) -> np.ndarray:
+    """Whole-head local search on per-head costs (shplb_plan_refine; an extension
+    beyond greedy_assign, partitioner.cpp:164-183): starting from device_of_head
+    (default: greedy_assign(costs)), move or swap heads off the most loaded device
+    while that lowers the maximum load. Returns the refined device_of_head."""
+    c = _i64(costs)
+    start = greedy_assign(c, devices) if device_of_head is None else device_of_head
+    out = np.ascontiguousarray(start, np.int32).copy()
+    if out.size != c.size:
+        from ._native import InvalidArgument
+        raise InvalidArgument(f"assignment covers {out.size} heads but {c.size} costs were given")
+    check(lib().shplb_plan_refine(_ptr(c), c.size, devices, _ptr(out), None))
+    return out
+
+
 def optimal_assign(budgets, devices: int) -> np.ndarray:
     """optimal_assign (partitioner.cpp:185-234): minimum makespan, then the
     lexicographically smallest plan reaching it (N <= 24, D <= 4)."""

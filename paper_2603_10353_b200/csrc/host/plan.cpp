@@ -141,6 +141,61 @@ extern "C" int shplb_plan_greedy(const int64_t* budgets, int32_t num_heads, int3
     });
 }
 
+// Whole-head local search (extension; the reference stops at greedy_assign, and
+// its exact optimal_assign is guarded to 24 heads / 4 devices). Each step takes
+// the most loaded device (lowest index among ties) and applies the move of one of
+// its heads to another device, or the swap of one of its heads with a lighter
+// head elsewhere, that gives the lowest max over the two devices touched — first
+// found wins ties (heads ascending, devices ascending, move before swaps). A step
+// is taken only if that max is below the current maximum load, so the sum of
+// squared loads falls strictly and the search ends; loads are integers, so it is
+// deterministic and platform-independent.
+extern "C" int shplb_plan_refine(const int64_t* costs, int32_t num_heads, int32_t devices,
+                                 int32_t* device_of_head, int64_t* loads_out) {
+    return guarded([&] {
+        check_budgets(costs, num_heads);
+        if (devices < 1) throw InvalidArgument("need at least one device");
+        require(device_of_head != nullptr, "device_of_head is null");
+        std::vector<int64_t> load(static_cast<std::size_t>(devices), 0);
+        for (int32_t h = 0; h < num_heads; ++h) {
+            const int32_t d = device_of_head[h];
+            if (d < 0 || d >= devices) throw InvalidArgument("device index out of range");
+            load[static_cast<std::size_t>(d)] += costs[h];
+        }
+        for (;;) {
+            const auto top = std::max_element(load.begin(), load.end());  // first of the maxima
+            const int32_t dm = static_cast<int32_t>(top - load.begin());
+            const int64_t lmax = *top;
+            int64_t best = lmax;
+            int32_t bi = -1, be = -1, bj = -1;
+            for (int32_t i = 0; i < num_heads; ++i) {
+                if (device_of_head[i] != dm || costs[i] == 0) continue;
+                for (int32_t e = 0; e < devices; ++e) {
+                    if (e == dm) continue;
+                    const int64_t le = load[static_cast<std::size_t>(e)];
+                    const int64_t mv = std::max(lmax - costs[i], le + costs[i]);
+                    if (mv < best) best = mv, bi = i, be = e, bj = -1;
+                    for (int32_t j = 0; j < num_heads; ++j) {
+                        if (device_of_head[j] != e || costs[j] >= costs[i]) continue;
+                        const int64_t sw = std::max(lmax - costs[i] + costs[j], le - costs[j] + costs[i]);
+                        if (sw < best) best = sw, bi = i, be = e, bj = j;
+                    }
+                }
+            }
+            if (bi < 0) break;
+            load[static_cast<std::size_t>(dm)] -= costs[bi];
+            load[static_cast<std::size_t>(be)] += costs[bi];
+            device_of_head[bi] = be;
+            if (bj >= 0) {
+                load[static_cast<std::size_t>(be)] -= costs[bj];
+                load[static_cast<std::size_t>(dm)] += costs[bj];
+                device_of_head[bj] = dm;
+            }
+        }
+        if (loads_out) std::copy(load.begin(), load.end(), loads_out);
+    });
+}
+
 extern "C" int shplb_plan_split(const int64_t* budgets, int32_t num_heads, int64_t seq_len,
                                 int32_t block_q, int32_t causal, int32_t devices,
                                 int32_t max_segments, int32_t* seg_device, int32_t* seg_head,

@@ -105,7 +105,7 @@ def test_gather_argument_errors(cuda_ctx, comm):
         P.NcclComm(0, 1, 1, P.NcclComm.unique_id())
 
 
-@pytest.mark.parametrize("plan", ["greedy", "naive", "split"])
+@pytest.mark.parametrize("plan", ["greedy", "naive", "refined", "split"])
 def test_cpp_host_head_parallel_layer(plan, tmp_path):
     """tools/hp_layer: plan -> shard layer -> NCCL gather, C ABI only, from a C++
     process; the reassembled layer is bit-identical to the single call."""

@@ -3,8 +3,9 @@
 // the paper's S-HPLB placement as a serving host would run it:
 //
 //   plan     shplb_plan_greedy (greedy_assign, partitioner.cpp:164-183),
-//            shplb_plan_naive (even head parallelism) or shplb_plan_split
-//            (sub-head balancer), the same on every rank;
+//            shplb_plan_naive (even head parallelism), refined (greedy on tile
+//            cost + shplb_plan_refine) or shplb_plan_split (sub-head
+//            balancer), the same on every rank;
 //   shard    this rank's q heads + the kv heads they read (kv map), and for the
 //            split plan each head's query-block range, through
 //            shplb_sparse_attention_layer into a local [h_r][n][d] buffer;
@@ -18,7 +19,7 @@
 // env: RANK, WORLD_SIZE (default 0 / 1), LOCAL_RANK (device, default RANK mod
 // device count), SHPLB_ID_FILE (unique-id exchange file, default /tmp/shplb_hp.id;
 // give every launch its own path — a rank reads whatever id file it finds).
-// usage: hp_layer [plan=greedy|naive|split] [seq_len=16384] [q_heads=32] [kv_heads=8]
+// usage: hp_layer [plan=greedy|naive|refined|split] [seq_len=16384] [q_heads=32] [kv_heads=8]
 // Prints one JSON line per rank.
 #include <cuda_runtime.h>
 
@@ -147,12 +148,22 @@ int main(int argc, char** argv) {
                 }
             }
         } else {
-            if (plan == "greedy")
+            if (plan == "greedy") {
                 check(shplb_plan_greedy(budgets.data(), hq, world, dev_of_head.data()), "shplb_plan_greedy");
-            else if (plan == "naive")
+            } else if (plan == "naive") {
                 check(shplb_plan_naive(budgets.data(), hq, world, 0, dev_of_head.data()), "shplb_plan_naive");
-            else
-                throw std::runtime_error("plan must be greedy, naive or split");
+            } else if (plan == "refined") {
+                // greedy on kernel 3's per-head tile cost, then whole-head local search
+                std::vector<int64_t> cost(static_cast<size_t>(hq));
+                shplb_layer_shape one = full;
+                one.num_q_heads = one.num_kv_heads = 1;
+                for (int h = 0; h < hq; ++h)
+                    check(shplb_layer_work(&one, &budgets[h], &cost[h], nullptr), "shplb_layer_work");
+                check(shplb_plan_greedy(cost.data(), hq, world, dev_of_head.data()), "shplb_plan_greedy");
+                check(shplb_plan_refine(cost.data(), hq, world, dev_of_head.data(), nullptr), "shplb_plan_refine");
+            } else {
+                throw std::runtime_error("plan must be greedy, naive, refined or split");
+            }
             std::vector<int32_t> next(static_cast<size_t>(world), 0);
             for (int h = 0; h < hq; ++h) segs.push_back({h, dev_of_head[h], next[dev_of_head[h]]++, 0, 0, n});
         }

@@ -12,12 +12,22 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <unistd.h>
 
 #include "ptx.cuh"
 
 using namespace shplb::ptx;
 
-__global__ void __launch_bounds__(256, 1) mma_kernel(int mode, int iters, unsigned long long* cycles) {
+// Random bf16 in about [-2, 2] from a hash (operand contents set the MMA's energy).
+__device__ __forceinline__ uint32_t rnd_bf16x2(uint32_t i) {
+    uint32_t x = i * 0x9E3779B1u;
+    x ^= x >> 15; x *= 0x85EBCA77u; x ^= x >> 13; x *= 0xC2B2AE3Du; x ^= x >> 16;
+    const uint32_t lo = 0x3F00u | (x & 0x807Fu), hi = 0x3F00u | ((x >> 16) & 0x807Fu);  // +-[0.5, 2)
+    return lo | (hi << 16);
+}
+
+__global__ void __launch_bounds__(256, 1) mma_kernel(int mode, int iters, unsigned long long* cycles, int rnd = 0) {
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ uint32_t tmem_base;
     __shared__ __align__(8) uint64_t bar[9];
@@ -31,6 +41,22 @@ __global__ void __launch_bounds__(256, 1) mma_kernel(int mode, int iters, unsign
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base;
+    if (rnd) {  // random operands: smem tiles and the TMEM A region of the TS mode
+        uint32_t* w = reinterpret_cast<uint32_t*>(smem);
+        for (int i = threadIdx.x; i < 200 * 1024 / 4; i += 256) w[i] = rnd_bf16x2(i + 7919u * blockIdx.x);
+        if (warp < 4) {
+            for (int c = 0; c < 128; c += 32) {
+                uint32_t v[32];
+                for (int e = 0; e < 32; ++e) v[e] = rnd_bf16x2(threadIdx.x * 131u + (c + e) * 977u + blockIdx.x);
+                tmem_st32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + 384u + c, v);
+            }
+            tmem_wait_st();
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
     const uint32_t a0 = smem_u32(smem), a1 = smem_u32(smem + 32768), b = smem_u32(smem + 65536);
     const uint32_t n = (mode == 2) ? 256 : (mode == 11 ? 64 : 128);
     const uint32_t idesc = idesc_bf16_f32(128, n, 0, mode == 1 ? 1 : 0);
@@ -144,7 +170,73 @@ __global__ void __launch_bounds__(256, 1) mma_kernel(int mode, int iters, unsign
     if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
+// Board energy (mJ) from the NVML total-energy counter, loaded at run time so the
+// tool links without libnvidia-ml; returns -1 when unavailable.
+static long long board_mj() {
+    static void* h = dlopen("libnvidia-ml.so.1", RTLD_NOW);
+    static void* dev = nullptr;
+    if (!h) return -1;
+    using init_t = int (*)();
+    using get_t = int (*)(unsigned, void**);
+    using en_t = int (*)(void*, unsigned long long*);
+    if (!dev) {
+        reinterpret_cast<init_t>(dlsym(h, "nvmlInit_v2"))();
+        reinterpret_cast<get_t>(dlsym(h, "nvmlDeviceGetHandleByIndex_v2"))(0, &dev);
+    }
+    unsigned long long mj = 0;
+    if (reinterpret_cast<en_t>(dlsym(h, "nvmlDeviceGetTotalEnergyConsumption"))(dev, &mj) != 0) return -1;
+    return static_cast<long long>(mj);
+}
+
+// `mma_bench energy SECONDS [RANDOM=1]`: modes 0-2 and 11 launched back to back for SECONDS
+// each; board energy per algorithmic FLOP (pJ) with the idle draw measured over
+// the same time subtracted, and the average board power.
+static int energy_main(double seconds, int rnd) {
+    unsigned long long* d;
+    cudaMalloc(&d, 148 * sizeof(unsigned long long));
+    cudaFuncSetAttribute(mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const long long i0 = board_mj();
+    usleep(static_cast<useconds_t>(seconds * 1e6));
+    const double idle_w = (board_mj() - i0) / seconds / 1e3;
+    printf("idle %.1f W, operands %s\n", idle_w, rnd ? "random bf16" : "as allocated");
+    const int modes[] = {0, 1, 2, 11};
+    const char* names[] = {"SS M128N128", "TS M128N128", "SS M128N256", "SS M128N64"};
+    const int iters = 1 << 16;
+    for (int k = 0; k < 4; ++k) {
+        const int mode = modes[k];
+        mma_kernel<<<148, 256, 200 * 1024>>>(mode, 1024, d, rnd);
+        cudaDeviceSynchronize();
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        // size the run: one timed launch, then enough launches for SECONDS
+        cudaEventRecord(e0);
+        mma_kernel<<<148, 256, 200 * 1024>>>(mode, iters, d, rnd);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms1 = 0;
+        cudaEventElapsedTime(&ms1, e0, e1);
+        const int reps = static_cast<int>(seconds * 1e3 / ms1) + 1;
+        const long long m0 = board_mj();
+        cudaEventRecord(e0);
+        for (int r = 0; r < reps; ++r) mma_kernel<<<148, 256, 200 * 1024>>>(mode, iters, d, rnd);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        const long long m1 = board_mj();
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double n = mode == 2 ? 256 : (mode == 11 ? 64 : 128);
+        const double flops = 2.0 * 128 * n * 16 * static_cast<double>(iters) * 148 * reps;
+        const double j = (m1 - m0) / 1e3, s = ms * 1e-3;
+        printf("%s  %8.1f TFLOP/s  %6.1f W  %.3f pJ/FLOP (board)  %.3f pJ/FLOP (above idle)  %.2f s\n", names[k],
+               flops / s / 1e12, j / s, j / flops * 1e12, (j - idle_w * s) / flops * 1e12, s);
+        fflush(stdout);
+    }
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    if (argc > 1 && argv[1][0] == 'e') return energy_main(argc > 2 ? atof(argv[2]) : 4.0, argc > 3 ? atoi(argv[3]) : 1);
     const int iters = argc > 1 ? atoi(argv[1]) : 20000;
     unsigned long long* d;
     cudaMalloc(&d, 148 * sizeof(unsigned long long));
