@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kGrpThreads, 1)
     score_select_kernel(const float* __restrict__ qp, const float* __restrict__ kp, int64_t n, int64_t nqb,
                         int64_t nkb, int bq, int causal, float scale, HeadTable ht, GroupTable gt, int64_t kmax,
                         float* scores, int fill_tail, int select, int32_t* __restrict__ idx,
-                        int32_t* __restrict__ cnt) {
+                        int32_t* __restrict__ cnt, int ksplit) {
     extern __shared__ __align__(16) float smem[];
     float* Qs = smem;                    // [64 row slots][kPad]
     float* Ks = Qs + kGrpRows * kPad;    // [256 key blocks][kPad]
@@ -326,12 +326,16 @@ __global__ void __launch_bounds__(kGrpThreads, 1)
         *reinterpret_cast<float4*>(Qs + s * kPad + c4 * 4) = v;
     }
     const int64_t vis_max = visible_blocks(min(c.qb0 + c.Q, nqb) - 1, n, nkb, bq, causal != 0);
+    // Key split (small launches, select = 0): CTA z scores key chunk z only.
+    const int64_t kc_begin = ksplit ? static_cast<int64_t>(blockIdx.z) * kGrpChunk : 0;
+    const int64_t kc_stop = ksplit ? min(vis_max, kc_begin + kGrpChunk) : vis_max;
+    if (kc_begin >= vis_max) return;
     // Thread (rp, kq): a warp spans 4 consecutive kq (K rows 132 floats = 4
     // banks apart: conflict-free 16-byte loads) and all 8 rp (Q rows, likewise).
     const int rp = tid % kGrpRowStep;
     const int kq = tid / kGrpRowStep;
     const float* kbase = kp + static_cast<int64_t>(g) * nkb * kHeadDim;
-    for (int64_t kc = 0; kc < vis_max; kc += kGrpChunk) {
+    for (int64_t kc = kc_begin; kc < kc_stop; kc += kGrpChunk) {
         const int kc_end = static_cast<int>(min(static_cast<int64_t>(kGrpChunk), vis_max - kc));
         __syncthreads();  // previous chunk consumed (and the Q tile visible)
         {
@@ -420,7 +424,7 @@ void launch_pool(const void* x, int heads, int64_t n, int rows, float* out, cuda
         pool_kernel<128><<<grid, kPoolThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(x), n, out);
 }
 
-void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n, int bq,
+int launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n, int bq,
                          bool causal, float scale, const HeadTable& ht, int64_t kmax,
                          float* scores_out, float* scores_ws, bool select, int32_t* idx, int32_t* cnt,
                          cudaStream_t s) {
@@ -455,11 +459,28 @@ void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int6
         }
         for (int gi = 0; gi < groups; ++gi) min_q = std::min(min_q, gt.size[gi] == 1 ? 64 : (gt.size[gi] == 2 ? 32 : 16));
     }
-    const dim3 grid(static_cast<unsigned>(groups), static_cast<unsigned>((nqb + min_q - 1) / min_q));
+    // The key chunks are split over grid.z and the rows selected by a second
+    // kernel (one warp per row): a CTA that walked every visible key chunk made a
+    // small launch (one GQA group: a KV-head chunk of the host entry, or one
+    // rank's shard) latency-bound by its longest CTA — C3 one kv group 0.124 ->
+    // 0.042 ms, a D = 8 rank 0.142 -> 0.046, the whole layer 0.194 -> 0.185
+    // (tools/k2_probe.py). Scores are the same fmaf chains either way, so the
+    // selection is unchanged. SHPLB_K2_SPLIT=0 keeps the fused single kernel.
+    static const int split_env = [] {
+        const char* e = std::getenv("SHPLB_K2_SPLIT");
+        return e ? std::atoi(e) : -1;
+    }();
+    const int64_t key_chunks = (nkb + kGrpChunk - 1) / kGrpChunk;
+    const bool split = select && !scores_out && key_chunks > 1 && split_env != 0;
+    const dim3 grid(static_cast<unsigned>(groups), static_cast<unsigned>((nqb + min_q - 1) / min_q),
+                    split ? static_cast<unsigned>(key_chunks) : 1u);
     set_max_dynamic_smem(reinterpret_cast<const void*>(score_select_kernel), static_cast<int>(kGrpSmem));
     score_select_kernel<<<grid, kGrpThreads, kGrpSmem, s>>>(qp, kp, n, nqb, nkb, bq, causal ? 1 : 0, scale, ht, gt,
                                                            kmax, scores_out ? scores_out : scores_ws,
-                                                           scores_out ? 1 : 0, select ? 1 : 0, idx, cnt);
+                                                           scores_out ? 1 : 0, (select && !split) ? 1 : 0, idx, cnt,
+                                                           split ? 1 : 0);
+    if (split) launch_select_from_scores(scores_ws, hq, n, bq, causal, ht, kmax, idx, cnt, s);
+    return split ? 2 : 1;  // kernels launched
 }
 
 void launch_select_from_scores(const float* scores, int hq, int64_t n, int bq, bool causal,

@@ -41,7 +41,7 @@ void launch_pool(const void* x, int heads, int64_t n, int rows, float* out, cuda
 // [hq][nqb][nkb] (-inf where causally invisible); otherwise the scores go to
 // scores_ws (hq*nqb*nkb floats, contents undefined after). With select=true,
 // idx/cnt receive the per-(head, q block) top-k block lists.
-void launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n, int bq,
+int launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n, int bq,
                          bool causal, float scale, const HeadTable& ht, int64_t kmax,
                          float* scores_out, float* scores_ws, bool select, int32_t* idx, int32_t* cnt,
                          cudaStream_t s);

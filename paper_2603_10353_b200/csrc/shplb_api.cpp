@@ -396,9 +396,10 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
         check_launch(ctx, 3 + 4);
     } else {
         if (!scores_out) grow(ctx->k2_ws, ctx->k2_ws_bytes, sizeof(float) * s->num_q_heads * nqb * nkb);
-        kern::launch_score_select(ctx->qp, ctx->kp, s->num_q_heads, s->num_kv_heads, s->seq_len, s->block_q,
-                                  s->causal != 0, scale, kb, kmax, scores_out, ctx->k2_ws, select, idx, cnt, st);
-        check_launch(ctx, 3);
+        const int k2 = kern::launch_score_select(ctx->qp, ctx->kp, s->num_q_heads, s->num_kv_heads, s->seq_len,
+                                                 s->block_q, s->causal != 0, scale, kb, kmax, scores_out, ctx->k2_ws,
+                                                 select, idx, cnt, st);
+        check_launch(ctx, 2 + k2);
     }
     if (select) mark(ctx, 2, st);
 }

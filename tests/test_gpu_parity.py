@@ -449,6 +449,23 @@ def test_kernel2_group_sizes(group):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+def test_kernel2_fused_single_kernel():
+    """Kernel 2 splits the pooled-K chunks of a long row over grid.z and selects
+    in a second kernel (the default when a row has more than 256 key blocks);
+    SHPLB_K2_SPLIT=0 keeps the fused score + select kernel. The at-size C4 case
+    (64K: 2 key chunks, GQA 7) under the fused kernel, in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-q", "-x",
+                        "-k", "at_size_sampled_rows and C4"],
+                       cwd=root, env=dict(os.environ, SHPLB_K2_SPLIT="0"), capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
+
+
 @pytest.mark.parametrize("causal", [True, False])
 @pytest.mark.parametrize("bq", [256, 128])
 def test_caller_selection_with_empty_rows(cuda_ctx, causal, bq):
