@@ -971,12 +971,13 @@ def main():
     projection = None
     if world == 1 and args.project_degrees:
         from paper_2603_10353_b200 import experiments as X
-        rows = X.measured_sweep(ctx, {n: (q, k, v, budgets)}, args.project_degrees, steps=2)
+        rows = X.measured_sweep(ctx, {n: (q, k, v, budgets)}, args.project_degrees, steps=6)
         projection = {}
         for r in rows:
             projection.setdefault(str(r.degree), {})[r.assigner] = {
                 "barrier_ms": round(r.barrier_latency, 3), "bubble": round(r.bubble_fraction, 4),
-                "speedup_vs_naive": round(r.speedup_vs_naive, 4)}
+                "speedup_vs_naive": round(r.speedup_vs_naive, 4),
+                "per_rank_ms": [round(x, 3) for x in r.per_rank_ms]}
     g = results[headline]
     flops_total = g["flops_total"]
     cpu = None
@@ -1099,7 +1100,8 @@ def main():
                                     "what": "layer 0, every causally visible key block (shplb_dense_attention_layer)"}
     if projection:
         line["per_rank_projection"] = {
-            "what": ("layer 0: every rank's shard timed in turn on this GPU (CUDA events, median of 3); "
+            "what": ("layer 0: every rank's shard timed in turn on this GPU (CUDA events, 6 back-to-back calls, "
+                     "3 rounds interleaved over the ranks, median per rank); "
                      "barrier = max over ranks, bubble = 1 - mean/max (simulator.cpp:40-44); "
                      "naive = even head parallelism, greedy = S-HPLB greedy_assign, greedy_tiles = greedy_assign on tile cost, greedy_refined = greedy_tiles + "
                      "whole-head local search (shplb_plan_refine), split = sub-head "
