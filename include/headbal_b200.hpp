@@ -249,6 +249,23 @@ inline Assignment naive_assign(const std::vector<long>& budgets, int devices,
     return a;
 }
 
+// Extension (no reference counterpart): whole-head local search on `assignment`
+// (shplb_plan_refine) with per-head costs — e.g. kernel 3's tile counts — where
+// optimal_assign's guard (24 heads, 4 devices) refuses the instance.
+inline Assignment refine_assign(const std::vector<long>& costs, const Assignment& assignment) {
+    if (assignment.device_of_head.size() != costs.size()) {
+        throw std::invalid_argument("assignment covers " + std::to_string(assignment.device_of_head.size()) +
+                                    " heads but " + std::to_string(costs.size()) + " costs were given");
+    }
+    const std::vector<int64_t> c(costs.begin(), costs.end());
+    std::vector<int32_t> dev(assignment.device_of_head.begin(), assignment.device_of_head.end());
+    check(shplb_plan_refine(c.data(), static_cast<int32_t>(c.size()), assignment.num_devices, dev.data(), nullptr));
+    Assignment a;
+    a.num_devices = assignment.num_devices;
+    a.device_of_head.assign(dev.begin(), dev.end());
+    return a;
+}
+
 inline LoadReport imbalance(const std::vector<long>& budgets, const Assignment& assignment) {
     // The reference's checks and messages before anything is sized or read
     // (Assignment::validate, partitioner.cpp:38-48; imbalance, :236-242).

@@ -6,6 +6,7 @@
 //                       reference; the reference's exception types/messages.
 //   adapter_test gpu  — the GPU layer call through the adapter vs the
 //                       reference's dense_attention at full budget.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -69,6 +70,18 @@ static int run_cpu() {
             const auto rr = naive_assign(ref.budgets, d, NaiveOrder::RoundRobin);
             EXPECT(rr.device_of_head == b200::naive_assign(ref.budgets, d, NaiveOrder::RoundRobin).device_of_head,
                    "naive_assign round robin");
+            // refine_assign (extension): never above greedy's makespan; at or above the
+            // reference's exact optimum where its guard allows it.
+            const auto rf = b200::refine_assign(ref.budgets, g);
+            const auto l_g = b200::imbalance(ref.budgets, g).loads;
+            const long mk_g = *std::max_element(l_g.begin(), l_g.end());
+            const auto l_rf = b200::imbalance(ref.budgets, rf).loads;
+            const long mk_r = *std::max_element(l_rf.begin(), l_rf.end());
+            EXPECT(mk_r <= mk_g, "refine_assign above greedy");
+            if (n <= 24 && d <= 4) {
+                const auto lo = imbalance(ref.budgets, optimal_assign(ref.budgets, d)).loads;
+                EXPECT(*std::max_element(lo.begin(), lo.end()) <= mk_r, "refine_assign below the optimum");
+            }
             const auto l_ref = imbalance(ref.budgets, g_ref), l = b200::imbalance(ref.budgets, g);
             EXPECT(l_ref.loads == l.loads && l_ref.total == l.total && l_ref.imbalance == l.imbalance &&
                        l_ref.argmax_device == l.argmax_device,

@@ -54,7 +54,7 @@ def test_bench_two_ranks_debug_path():
     assert line["n_gpus"] == 2 and len(line["per_rank_ms"]) == 2
     assert line["gather_kind"] == "p2p"
     assert "sub-head balancer" in line["config"]["placement"]
-    for k in ("naive_even_hp", "greedy_whole_head", "split_subhead"):
+    for k in ("naive_even_hp", "greedy_whole_head", "greedy_tile_cost", "greedy_refined", "split_subhead"):
         assert line[k]["ms"] > 0, k
     assert line["e2e"]["value"] > 0
 
