@@ -773,7 +773,8 @@ PLACEMENTS = {
     "greedy": ("greedy (LPT) whole-head plan (greedy_assign, bit-exact with the reference); even head "
                "parallelism (naive_even_hp), greedy on tile cost (greedy_tile_cost), its whole-head "
                "refinement (greedy_refined) and the sub-head balancer (split_subhead) are timed alongside"),
-    "greedy_refined": ("whole-head plan: greedy_assign on kernel 3's tile cost per head, refined by moves / "
+    "greedy_refined": ("whole-head plan: greedy_assign on kernel 3's tile cost per head (+ 4 tiles per visited "
+                       "query tile), refined by moves / "
                        "swaps of heads off the most loaded rank (shplb_plan_refine); the reference's greedy plan, "
                        "even head parallelism and the sub-head balancer are timed alongside"),
     "split": ("sub-head balancer (shplb_plan_split): heads in index order with exact tile costs, cut "
@@ -910,8 +911,8 @@ def main():
     if world > 1:
         plans_l["naive"] = [P.naive_assign(b, world) for b in budgets_l]
         plans_l["greedy_tiles"] = [P.greedy_assign(P.tile_costs(b, n), world) for b in budgets_l]
-        plans_l["greedy_refined"] = [P.refine_assign(P.tile_costs(b, n), world, g)
-                                     for b, g in zip(budgets_l, plans_l["greedy_tiles"])]
+        wcosts = [P.tile_costs(b, n, query_tile_weight=P.api.QUERY_TILE_WEIGHT) for b in budgets_l]
+        plans_l["greedy_refined"] = [P.refine_assign(c, world, P.greedy_assign(c, world)) for c in wcosts]
         plans_l["split"] = [P.split_assign(b, world, n) for b in budgets_l]
     headline = args.placement if world > 1 else "greedy"  # at N = 1 every plan is the whole layer
     results = {}
@@ -1085,8 +1086,9 @@ def main():
                                   "bubble": round(grf["bubble"], 4),
                                   "per_rank_ms": [round(x, 3) for x in grf["per_rank_ms"]],
                                   "speedup_vs_even_hp": round(_vg(nv) / _vg(grf), 4),
-                                  "plan": "greedy_tile_cost refined by whole-head moves / swaps off the "
-                                          "most loaded rank (shplb_plan_refine), an extension"}
+                                  "plan": "greedy_assign on tile cost + 4 tiles per visited query tile, refined "
+                                          "by whole-head moves / swaps off the most loaded rank "
+                                          "(shplb_plan_refine), an extension"}
         line["gather"] = ("every layer's [Hq, n, d] output reassembled on every rank by shplb_gather_segments "
                           "(one NCCL broadcast per output segment from its owner, one group per layer) on a "
                           "communication stream, overlapped with the next layer's compute"

@@ -237,12 +237,22 @@ def split_assign(budgets, devices: int, seq_len: int, block_q: int = BLOCK_Q,
     return SplitPlan(dev[:k].copy(), hd[:k].copy(), qb0[:k].copy(), qb1[:k].copy(), loads)
 
 
-def tile_costs(budgets, seq_len: int, block_q: int = BLOCK_Q, causal: bool = True) -> np.ndarray:
+# Kernel 3's fixed cost per (query block, query half) it visits, in tile
+# equivalents: a least-squares fit of measured per-rank shard times gives 3.4
+# (C3, 128K) and 5.1 (C4, 64K) next to ~6.4 ns per tile (tools/plan_fit.py,
+# profiles/r02/plan_fit_C3.txt). For whole heads it is a per-head constant.
+QUERY_TILE_WEIGHT = 4
+
+
+def tile_costs(budgets, seq_len: int, block_q: int = BLOCK_Q, causal: bool = True,
+               query_tile_weight: int = 0) -> np.ndarray:
     """Per-head cost in kernel 3's 128x128 tiles: sum over query blocks of
     min(ceil(b_h/128), visible key blocks) x query halves holding rows — the
-    work the layer call does for the head (shplb_layer_work per head). Passed to
-    greedy_assign instead of the budgets it is the documented extension of
-    SURVEY a11 (the same LPT, weighted by causal tile cost rather than tokens)."""
+    work the layer call does for the head (shplb_layer_work per head) — plus
+    query_tile_weight per visited query half (QUERY_TILE_WEIGHT models the
+    per-tile fixed cost). Passed to greedy_assign instead of the budgets it is
+    the documented extension of SURVEY a11 (the same LPT, weighted by causal
+    tile cost rather than tokens)."""
     b = np.asarray(budgets, np.int64)
     nkb = (seq_len + BLOCK - 1) // BLOCK
     nqb = (seq_len + block_q - 1) // block_q
@@ -251,7 +261,8 @@ def tile_costs(budgets, seq_len: int, block_q: int = BLOCK_Q, causal: bool = Tru
     vis = np.minimum(last // BLOCK + 1, nkb) if causal else np.full(nqb, nkb)
     halves = np.array([sum(1 for hf in range(block_q // BLOCK) if q * block_q + hf * BLOCK < seq_len) for q in qb])
     kb = np.minimum((b + BLOCK - 1) // BLOCK, nkb)
-    return (np.minimum(kb[:, None], vis[None, :]) * halves[None, :]).sum(1).astype(np.int64)
+    t = np.minimum(kb[:, None], vis[None, :]) * halves[None, :]
+    return (t.sum(1) + int(query_tile_weight) * ((t > 0) * halves[None, :]).sum(1)).astype(np.int64)
 
 
 @dataclass

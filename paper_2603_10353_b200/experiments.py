@@ -151,8 +151,10 @@ def measured_sweep(ctx, layers: dict, degrees, allocator: str = "maxmin", steps:
                                  res_t.bubble_fraction, api.imbalance(budgets, gt, degree).imbalance,
                                  1.0 if res_t.barrier_latency == 0 else res_n.barrier_latency / res_t.barrier_latency,
                                  per_t))
-            # the same, refined by whole-head local search (api.refine_assign)
-            gr = api.refine_assign(api.tile_costs(budgets, q.shape[1]), degree, gt)
+            # whole-head local search (api.refine_assign) on tile cost + the per-query-tile
+            # fixed cost, from greedy on that cost
+            wc = api.tile_costs(budgets, q.shape[1], query_tile_weight=api.QUERY_TILE_WEIGHT)
+            gr = api.refine_assign(wc, degree, api.greedy_assign(wc, degree))
             per_r, res_r = measured_barrier(ctx, q, k, v, budgets, gr, degree, steps)
             rows.append(SweepRow(degree, length, allocator, "greedy_refined", res_r.barrier_latency,
                                  res_r.bubble_fraction, api.imbalance(budgets, gr, degree).imbalance,

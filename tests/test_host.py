@@ -368,6 +368,16 @@ def test_refine_plan_against_reference_exact_solver():
     assert hits_r > hits_g and gap_r < 0.5 * gap_g, (hits_r, hits_g, gap_r, gap_g)
 
 
+def test_tile_costs_query_tile_weight():
+    """tile_costs(..., query_tile_weight=w) adds w per visited (query block, half):
+    for whole heads with any budget that is w x the tiles of a one-block budget."""
+    b = np.array([128, 5000, 40000, 131072], np.int64)
+    for n, bq in ((131072, 256), (70000, 256), (3000, 128)):
+        one = P.tile_costs(np.full(4, 128, np.int64), n, block_q=bq)
+        assert np.array_equal(P.tile_costs(b, n, block_q=bq, query_tile_weight=4),
+                              P.tile_costs(b, n, block_q=bq) + 4 * one)
+
+
 def test_refine_plan_errors():
     with pytest.raises(P.InvalidArgument, match="device index out of range"):
         P.refine_assign([1, 2, 3], 2, np.array([0, 1, 2], np.int32))

@@ -153,12 +153,18 @@ int main(int argc, char** argv) {
             } else if (plan == "naive") {
                 check(shplb_plan_naive(budgets.data(), hq, world, 0, dev_of_head.data()), "shplb_plan_naive");
             } else if (plan == "refined") {
-                // greedy on kernel 3's per-head tile cost, then whole-head local search
+                // greedy on kernel 3's per-head tile cost + 4 tiles per visited query
+                // tile (api.QUERY_TILE_WEIGHT), then whole-head local search
                 std::vector<int64_t> cost(static_cast<size_t>(hq));
                 shplb_layer_shape one = full;
                 one.num_q_heads = one.num_kv_heads = 1;
-                for (int h = 0; h < hq; ++h)
+                const int64_t one_block = 128;  // one key block per query block: tiles = query tiles
+                int64_t qtiles = 0;
+                check(shplb_layer_work(&one, &one_block, &qtiles, nullptr), "shplb_layer_work");
+                for (int h = 0; h < hq; ++h) {
                     check(shplb_layer_work(&one, &budgets[h], &cost[h], nullptr), "shplb_layer_work");
+                    cost[h] += 4 * qtiles;
+                }
                 check(shplb_plan_greedy(cost.data(), hq, world, dev_of_head.data()), "shplb_plan_greedy");
                 check(shplb_plan_refine(cost.data(), hq, world, dev_of_head.data(), nullptr), "shplb_plan_refine");
             } else {

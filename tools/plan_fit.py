@@ -8,6 +8,8 @@ over all (plan, degree, rank) shards by least squares. Prints the fit, its
 residuals, and each plan's modelled vs measured bubble.
 
 usage: python tools/plan_fit.py gpurun_out/v4/bench.json
+(the greedy_refined plan is rebuilt as the current bench builds it: a line taken
+before it moved to the weighted cost refits against the wrong plan)
 """
 import json
 import os
@@ -62,7 +64,8 @@ def main():
         tc = P.tile_costs(budgets, N)
         built = {"naive": P.naive_assign(budgets, D), "greedy": P.greedy_assign(budgets, D),
                  "greedy_tiles": P.greedy_assign(tc, D)}
-        built["greedy_refined"] = P.refine_assign(tc, D, built["greedy_tiles"])
+        wc = P.tile_costs(budgets, N, query_tile_weight=P.api.QUERY_TILE_WEIGHT)
+        built["greedy_refined"] = P.refine_assign(wc, D, P.greedy_assign(wc, D))
         built["split"] = P.split_assign(budgets, D, N)
         for name, rec in plans.items():
             if "per_rank_ms" not in rec or name not in built:
