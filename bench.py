@@ -913,7 +913,7 @@ def main():
         plans_l["greedy_tiles"] = [P.greedy_assign(P.tile_costs(b, n), world) for b in budgets_l]
         wcosts = [P.tile_costs(b, n, query_tile_weight=P.api.QUERY_TILE_WEIGHT) for b in budgets_l]
         plans_l["greedy_refined"] = [P.refine_assign(c, world, P.greedy_assign(c, world)) for c in wcosts]
-        plans_l["split"] = [P.split_assign(b, world, n) for b in budgets_l]
+        plans_l["split"] = [P.split_assign(b, world, n, query_tile_weight=P.api.QUERY_TILE_WEIGHT) for b in budgets_l]
     headline = args.placement if world > 1 else "greedy"  # at N = 1 every plan is the whole layer
     results = {}
     for name, plans in plans_l.items():

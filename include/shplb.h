@@ -192,6 +192,14 @@ int shplb_plan_split(const int64_t* budgets, int32_t num_heads, int64_t seq_len,
                      int32_t causal, int32_t devices, int32_t max_segments, int32_t* seg_device,
                      int32_t* seg_head, int32_t* seg_qb_begin, int32_t* seg_qb_end,
                      int32_t* n_segments, int64_t* loads_out);
+/* The same cut with unit cost = tiles + query_tile_weight x (query halves the
+ * unit visits): kernel 3's fixed per-tile cost in tile equivalents (measured
+ * 2.3-5.5, tools/plan_fit.py; the Python API's QUERY_TILE_WEIGHT = 4). Weight 0
+ * is shplb_plan_split. loads_out in the same weighted units. */
+int shplb_plan_split_weighted(const int64_t* budgets, int32_t num_heads, int64_t seq_len, int32_t block_q,
+                              int32_t causal, int32_t devices, int64_t query_tile_weight, int32_t max_segments,
+                              int32_t* seg_device, int32_t* seg_head, int32_t* seg_qb_begin, int32_t* seg_qb_end,
+                              int32_t* n_segments, int64_t* loads_out);
 
 /* imbalance(budgets, assignment) (partitioner.hpp:50, partitioner.cpp:236-266):
  * loads[devices], total, I = max*D/total, argmax device. */

@@ -20,7 +20,7 @@ EXPORTS = (
     "shplb_uniform_allocate", "shplb_maxmin_allocate", "shplb_recovery_at", "shplb_budget_for_recovery",
     "shplb_profile_curves_host", "shplb_profile_curves",
     "shplb_profile_curves_host_kind", "shplb_profile_curves_kind", "shplb_profile_curves_block",
-    "shplb_plan_naive", "shplb_plan_greedy", "shplb_plan_optimal", "shplb_plan_refine", "shplb_plan_split", "shplb_imbalance",
+    "shplb_plan_naive", "shplb_plan_greedy", "shplb_plan_optimal", "shplb_plan_refine", "shplb_plan_split", "shplb_plan_split_weighted", "shplb_imbalance",
     "shplb_simulate", "shplb_barrier",
     "shplb_ctx_create", "shplb_ctx_destroy", "shplb_ctx_launch_count",
     "shplb_ctx_set_timing", "shplb_ctx_read_timing",
@@ -154,6 +154,7 @@ def lib() -> C.CDLL:
     L.shplb_plan_optimal.argtypes = [vp, i32, i32, vp]
     L.shplb_plan_refine.argtypes = [vp, i32, i32, vp, vp]
     L.shplb_plan_split.argtypes = [vp, i32, i64, i32, i32, i32, i32, vp, vp, vp, vp, P(i32), vp]
+    L.shplb_plan_split_weighted.argtypes = [vp, i32, i64, i32, i32, i32, i64, i32, vp, vp, vp, vp, P(i32), vp]
     L.shplb_imbalance.argtypes = [vp, i32, vp, i32, vp, P(i64), P(f64), P(i32)]
     L.shplb_simulate.argtypes = [vp, i32, f64, f64, vp, P(f64), P(f64)]
     L.shplb_barrier.argtypes = [vp, i32, P(f64), P(f64)]

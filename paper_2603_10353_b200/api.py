@@ -221,18 +221,19 @@ class SplitPlan:
 
 
 def split_assign(budgets, devices: int, seq_len: int, block_q: int = BLOCK_Q,
-                 causal: bool = True) -> SplitPlan:
+                 causal: bool = True, query_tile_weight: int = 0) -> SplitPlan:
     """Sub-head balancer: whole heads in index order, cut at query-block
-    boundaries so every device's tile cost is within half a query block of
+    boundaries so every device's tile cost (+ query_tile_weight per visited
+    query half: shplb_plan_split_weighted) is within half a query block of
     total/devices (at most devices-1 heads are split)."""
     b = _i64(budgets)
     cap = b.size + devices
     dev, hd, qb0, qb1 = (np.empty(cap, np.int32) for _ in range(4))
     loads = np.empty(devices, np.int64)
     ns = C.c_int32()
-    check(lib().shplb_plan_split(_ptr(b), b.size, seq_len, block_q, int(causal), devices, cap,
-                                 _ptr(dev), _ptr(hd), _ptr(qb0), _ptr(qb1), C.byref(ns),
-                                 _ptr(loads)))
+    check(lib().shplb_plan_split_weighted(_ptr(b), b.size, seq_len, block_q, int(causal), devices,
+                                          int(query_tile_weight), cap, _ptr(dev), _ptr(hd), _ptr(qb0),
+                                          _ptr(qb1), C.byref(ns), _ptr(loads)))
     k = ns.value
     return SplitPlan(dev[:k].copy(), hd[:k].copy(), qb0[:k].copy(), qb1[:k].copy(), loads)
 

@@ -196,13 +196,14 @@ extern "C" int shplb_plan_refine(const int64_t* costs, int32_t num_heads, int32_
     });
 }
 
-extern "C" int shplb_plan_split(const int64_t* budgets, int32_t num_heads, int64_t seq_len,
-                                int32_t block_q, int32_t causal, int32_t devices,
-                                int32_t max_segments, int32_t* seg_device, int32_t* seg_head,
-                                int32_t* seg_qb_begin, int32_t* seg_qb_end, int32_t* n_segments,
-                                int64_t* loads_out) {
+extern "C" int shplb_plan_split_weighted(const int64_t* budgets, int32_t num_heads, int64_t seq_len,
+                                         int32_t block_q, int32_t causal, int32_t devices,
+                                         int64_t query_tile_weight, int32_t max_segments, int32_t* seg_device,
+                                         int32_t* seg_head, int32_t* seg_qb_begin, int32_t* seg_qb_end,
+                                         int32_t* n_segments, int64_t* loads_out) {
     return guarded([&] {
         check_budgets(budgets, num_heads);
+        if (query_tile_weight < 0) throw InvalidArgument("query_tile_weight must be nonnegative");
         if (devices < 1) throw InvalidArgument("need at least one device");
         if (seq_len < 1) throw InvalidArgument("K must hold at least one key token");
         if (block_q != 128 && block_q != 256) throw InvalidArgument("block_q must be 128 or 256");
@@ -211,14 +212,16 @@ extern "C" int shplb_plan_split(const int64_t* budgets, int32_t num_heads, int64
         constexpr int64_t bk = 128;
         const int64_t nqb = (seq_len + block_q - 1) / block_q, nkb = (seq_len + bk - 1) / bk;
         // Tiles kernel 3 computes for (head h, query block qb) before selection
-        // (include/shplb.h, shplb_layer_work).
+        // (include/shplb.h, shplb_layer_work), plus query_tile_weight per visited
+        // query half (kernel 3's per-tile fixed cost in tile equivalents).
         auto cost = [&](int32_t h, int64_t qb) -> int64_t {
             int64_t vis = nkb;
             if (causal) vis = std::min(nkb, (std::min((qb + 1) * block_q, seq_len) - 1) / bk + 1);
             const int64_t k = std::min(nkb, (budgets[h] + bk - 1) / bk);
             int64_t halves = 0;
             for (int64_t hf = 0; hf < block_q / bk; ++hf) halves += qb * block_q + hf * bk < seq_len;
-            return std::min(k, vis) * halves;
+            const int64_t kept = std::min(k, vis);
+            return kept * halves + (kept > 0 ? query_tile_weight * halves : 0);
         };
         int64_t total = 0;
         for (int32_t h = 0; h < num_heads; ++h)
@@ -256,6 +259,15 @@ extern "C" int shplb_plan_split(const int64_t* budgets, int32_t num_heads, int64
         }
         *n_segments = nseg;
     });
+}
+
+extern "C" int shplb_plan_split(const int64_t* budgets, int32_t num_heads, int64_t seq_len,
+                                int32_t block_q, int32_t causal, int32_t devices,
+                                int32_t max_segments, int32_t* seg_device, int32_t* seg_head,
+                                int32_t* seg_qb_begin, int32_t* seg_qb_end, int32_t* n_segments,
+                                int64_t* loads_out) {
+    return shplb_plan_split_weighted(budgets, num_heads, seq_len, block_q, causal, devices, 0, max_segments,
+                                     seg_device, seg_head, seg_qb_begin, seg_qb_end, n_segments, loads_out);
 }
 
 extern "C" int shplb_imbalance(const int64_t* budgets, int32_t num_heads,

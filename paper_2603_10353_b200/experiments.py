@@ -102,7 +102,7 @@ def measured_barrier(ctx, q, k, v, budgets, device_of_head, devices: int, steps:
 
 def measured_split_barrier(ctx, q, k, v, budgets, devices: int, steps: int = 3, kind=0):
     group = q.shape[0] // k.shape[0]
-    sp = api.split_assign(budgets, devices, q.shape[1])
+    sp = api.split_assign(budgets, devices, q.shape[1], query_tile_weight=api.QUERY_TILE_WEIGHT)
     per = shards_latency_ms(ctx, q, k, v, [rank_segments(sp, r, group, budgets) for r in range(devices)],
                             steps, kind=kind)
     return per, api.barrier(per), sp

@@ -265,6 +265,33 @@ def test_split_plan_covers_every_block_once_and_balances(seed):
     assert np.abs(sp.loads - tiles / D).max() <= unit_max
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_weighted_split_plan(seed):
+    """shplb_plan_split_weighted: weight 0 is shplb_plan_split; with weight w
+    every (head, query block) is still covered once and each device's load —
+    tiles + w per visited query half — is within one unit of total/D."""
+    rng = np.random.default_rng(50 + seed)
+    hq, D = int(rng.integers(2, 40)), int(rng.integers(1, 9))
+    n = int(rng.choice([5000, 65536, 131072]))
+    budgets = (rng.integers(1, n // 128 + 1, hq) * 128).clip(128, n)
+    a, b = P.split_assign(budgets, D, n), P.split_assign(budgets, D, n, query_tile_weight=0)
+    assert all(np.array_equal(x, y) for x, y in ((a.device, b.device), (a.head, b.head), (a.qb_begin, b.qb_begin),
+                                                  (a.qb_end, b.qb_end), (a.loads, b.loads)))
+    w = 4
+    sp = P.split_assign(budgets, D, n, query_tile_weight=w)
+    nqb = (n + 255) // 256
+    covered = np.zeros((hq, nqb), np.int32)
+    for d, h, b0, e in zip(sp.device, sp.head, sp.qb_begin, sp.qb_end):
+        covered[h, b0:e] += 1
+    assert (covered == 1).all()
+    total = P.tile_costs(budgets, n, query_tile_weight=w).sum()
+    assert sp.loads.sum() == total
+    unit_max = (int(min(budgets.max() // 128 + 1, (n + 127) // 128)) + w) * 2
+    assert np.abs(sp.loads - total / D).max() <= unit_max
+    with pytest.raises(P.InvalidArgument, match="query_tile_weight must be nonnegative"):
+        P.split_assign(budgets, D, n, query_tile_weight=-1)
+
+
 def test_split_plan_beats_whole_head_plans():
     # SURVEY §6-like table: many floor heads + a few heavy ones over 8 devices
     budgets = np.array([128] * 18 + [1344, 3840, 4096, 4352, 4544, 4736, 5760, 6592, 6592,

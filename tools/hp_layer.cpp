@@ -4,8 +4,8 @@
 //
 //   plan     shplb_plan_greedy (greedy_assign, partitioner.cpp:164-183),
 //            shplb_plan_naive (even head parallelism), refined (greedy on tile
-//            cost + shplb_plan_refine) or shplb_plan_split (sub-head
-//            balancer), the same on every rank;
+//            cost + shplb_plan_refine) or shplb_plan_split_weighted (sub-head
+//            balancer, 4 tiles per query tile), the same on every rank;
 //   shard    this rank's q heads + the kv heads they read (kv map), and for the
 //            split plan each head's query-block range, through
 //            shplb_sparse_attention_layer into a local [h_r][n][d] buffer;
@@ -133,9 +133,9 @@ int main(int argc, char** argv) {
             std::vector<int32_t> sd(maxs), sh(maxs), sb(maxs), se(maxs);
             std::vector<int64_t> loads(static_cast<size_t>(world));
             int32_t ns = 0;
-            check(shplb_plan_split(budgets.data(), hq, n, bq, 1, world, maxs, sd.data(), sh.data(), sb.data(),
+            check(shplb_plan_split_weighted(budgets.data(), hq, n, bq, 1, world, 4, maxs, sd.data(), sh.data(), sb.data(),
                                    se.data(), &ns, loads.data()),
-                  "shplb_plan_split");
+                  "shplb_plan_split_weighted");
             for (int r = 0; r < world; ++r) {  // a rank's local layout: its segments in head order
                 std::vector<int> mine;
                 for (int i = 0; i < ns; ++i)
