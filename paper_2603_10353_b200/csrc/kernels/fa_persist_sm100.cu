@@ -1,9 +1,10 @@
-// Kernel 3, persistent CTA-pair variant (block_q = 256): the CTA-pair kernel of
-// fa_pair_sm100.cu (two 128-row query halves on the two SMs of a cluster,
-// tcgen05.mma.cta_group::2 with M = 256, two softmax warpgroups per SM on
-// alternate key blocks with their own running max / row sum / O in TMEM), run
-// as one resident cluster per SM pair that walks a host-built list of query
-// tiles instead of one cluster per tile.
+// Kernel 3, persistent CTA-pair kernel (block_q = 256): the CTA-pair data path
+// (two 128-row query halves on the two SMs of a cluster, tcgen05.mma.cta_group::2
+// with M = 256, two softmax warpgroups per SM on alternate key blocks with their
+// own running max / row sum / O in TMEM), run as one resident cluster per SM
+// pair that walks a host-built list of query tiles. (Its predecessor with one
+// cluster per tile, fa_pair_sm100.cu, was removed once this kernel matched it
+// bit for bit and beat it on short tiles; see git history and DESIGN.md §5.)
 //
 // Why (profiles/r02/k3_tile_trace.json): with a cluster per tile
 // each tile paid ~6.5 K cycles of prologue (barrier init, TMEM alloc, cluster
@@ -14,9 +15,9 @@
 // next tile's Q and K/V while the current tile drains, so S of the next tile
 // is already in TMEM when its softmax warpgroup comes out of the epilogue.
 //
-// Per tile the data path is that of fa_pair_sm100.cu (same MMAs, same online
-// softmax, same merge and TMA-store epilogue, bit-identical outputs). What is
-// new is the cross-tile bookkeeping: every barrier's phase is a running count
+// Per tile the data path is the one-cluster-per-tile kernel's (same MMAs, same
+// online softmax, same merge and TMA-store epilogue, bit-identical outputs). What
+// is new is the cross-tile bookkeeping: every barrier's phase is a running count
 // (K/V stages and P·V slots by global block index, S by each warpgroup's own
 // block count, the Q, selection and output slots by tile index), and three
 // handshakes order the tile boundary:
@@ -540,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1) fa_persist_kernel(const __grid_co
             }
 
             // ---------------------------------------------------- epilogue
-            // As fa_pair_sm100.cu: merge (O_0, l_0, m_0) and (O_1, l_1, m_1),
+            // Merge (O_0, l_0, m_0) and (O_1, l_1, m_1),
             // stage the bf16 tile in this tile's Q slot (its last S completed
             // before its last P·V was issued), store with bulk tensor copies.
             lfin[(wg * 2 + 0) * 128 + r] = l;

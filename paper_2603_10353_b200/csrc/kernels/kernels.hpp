@@ -84,10 +84,7 @@ struct FaParams {
 // dual: block_q = 128 with two query blocks per CTA (tiles packed as pairs, see
 // fa_sm100.cu); otherwise one tile per query block.
 void launch_fa(const FaParams& p, int num_tiles, bool dual, cudaStream_t s);
-// The CTA-pair variant (fa_pair_sm100.cu): bq = 256; one 2-CTA cluster per tile,
-// two softmax warpgroups per CTA on alternate key blocks.
-cudaError_t launch_fa_pair(const FaParams& p, int num_tiles, cudaStream_t s);
-// The persistent CTA-pair variant (fa_persist_sm100.cu): num_clusters resident
+// The persistent CTA-pair kernel (fa_persist_sm100.cu; bq = 256): num_clusters resident
 // clusters taking tiles of p.tiles in order through the ticket counter p.counter.
 cudaError_t launch_fa_persist(const FaParams& p, int num_clusters, cudaStream_t s);
 // Clusters of the persistent kernel that fit on the device at once (0 if the

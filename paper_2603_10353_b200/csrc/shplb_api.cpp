@@ -417,14 +417,13 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
 //       alternate key blocks) as one resident cluster per SM pair taking tiles
 //       of the work list by atomic ticket — tile boundaries 11.4 K -> 2.0 K
 //       cycles; C3 unchanged under the power cap, short tiles up to ~10% faster;
-//   "pair" = fa_pair_sm100.cu, the same data path with one cluster per tile;
 //   "single" = fa_sm100.cu, one CTA with two query halves ping-ponging (also
-//       the block_q = 128 kernel).
+//       the block_q = 128 kernel). (The round-2 one-cluster-per-tile CTA-pair
+//       kernel, the persistent kernel's non-persistent predecessor, was removed.)
 int k3_variant() {
     static const int v = [] {
         const char* e = std::getenv("SHPLB_K3");
         if (e && std::string(e) == "single") return 0;
-        if (e && std::string(e) == "pair") return 1;
         return 2;
     }();
     return v;
@@ -575,9 +574,8 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
     p.tm_q = make_tmap(q, s->num_q_heads, s->seq_len);
     p.tm_k = make_tmap(k, s->num_kv_heads, s->seq_len);
     p.tm_v = make_tmap(v, s->num_kv_heads, s->seq_len);
-    const bool pair = s->block_q == 256 && k3_variant() >= 1;
     const bool persist = s->block_q == 256 && k3_variant() == 2;
-    if (pair) p.tm_k_half = make_tmap(k, s->num_kv_heads, s->seq_len, 64);
+    if (persist) p.tm_k_half = make_tmap(k, s->num_kv_heads, s->seq_len, 64);
     p.out = out;
     p.idx = idx;
     p.cnt = cnt;
@@ -610,12 +608,9 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
             p.num_tiles = ctx->current->num_tiles;
             SHPLB_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st));
             SHPLB_CUDA(kern::launch_fa_persist(p, std::min(maxc, p.num_tiles), st));
-        } else if (pair)
-            SHPLB_CUDA(kern::launch_fa_pair(p, ctx->current->num_tiles, st));
-        else if (pair)
-            SHPLB_CUDA(kern::launch_fa_pair(p, ctx->current->num_tiles, st));
-        else
+        } else {
             kern::launch_fa(p, ctx->current->num_tiles, dual_mode(s), st);
+        }
     }
     check_launch(ctx);
     SHPLB_CUDA(cudaEventRecord(ctx->current->last_use, st));

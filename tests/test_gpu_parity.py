@@ -504,22 +504,6 @@ def test_caller_selection_with_empty_rows(cuda_ctx, causal, bq):
             check_output(out[h, rows], ref, f"caller selection h {h} qb {qb}")
 
 
-def test_cta_pair_kernel3_variant():
-    """block_q = 256 runs the persistent CTA-pair kernel 3 by default; the
-    one-cluster-per-tile CTA-pair kernel (fa_pair_sm100.cu, SHPLB_K3=pair) on
-    the parity cases of this file and the fused-gather tests, in a subprocess."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "tests/test_gpu_gather.py", "-q",
-                        "-x", "-k", "small_gqa_layer or ragged_lengths or mha_and_wide or kv_map or zero_q or "
-                                    "single_kept or full_budget or c1_shape or fused_gather or caller_selection"],
-                       cwd=root, env=dict(os.environ, SHPLB_K3="pair"), capture_output=True, text=True,
-                       timeout=900)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-
-
 def test_single_cta_kernel3_variant():
     """The single-CTA kernel (fa_sm100.cu, SHPLB_K3=single — also the block_q =
     128 kernel) on the parity cases of this file and the fused-gather tests, in a

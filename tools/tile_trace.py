@@ -1,8 +1,6 @@
 """Where kernel 3's cycles go, tile by tile (dev tool, GPU).
 
-usage: SHPLB_LIB=<SHPLB_TILETRACE build of the pair kernel> python tools/tile_trace.py [out.json]
-(build: K3=pair tools/build_variants.sh tt "-DSHPLB_TILETRACE")
-   or: SHPLB_K3=persist SHPLB_LIB=<trace build of the persistent kernel> python tools/tile_trace.py --persist [out.json]
+usage: SHPLB_LIB=<trace build of the persistent kernel> python tools/tile_trace.py --persist [out.json]
 (build: K3=persist tools/build_variants.sh ttp "-DSHPLB_TILETRACE")
 
 Runs the C3 128K layer (the bench's layer-0 inputs and max-min table), reads the per-CTA
