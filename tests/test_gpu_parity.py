@@ -449,6 +449,16 @@ def test_kernel2_group_sizes(group):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("bq", [256, 128])
+@pytest.mark.parametrize("n,causal", [(32769, True), (33000, False), (40000, True)])
+def test_kernel2_key_split_partial_chunk(cuda_ctx, n, causal, bq):
+    """Rows longer than one 256-block pooled-K chunk take the key-split kernel 2
+    (grid.z over chunks, then the selector): 32769 tokens leave a last chunk of
+    one key block, 33000 a ragged one, non-causal rows see every chunk."""
+    spec = LayerSpec(num_q_heads=2, num_kv_heads=1, seq_len=n, seed=n + bq + int(causal))
+    run_case(cuda_ctx, spec, [2, 3], causal=causal, bq=bq)
+
+
 def test_kernel2_fused_single_kernel():
     """Kernel 2 splits the pooled-K chunks of a long row over grid.z and selects
     in a second kernel (the default when a row has more than 256 key blocks);
