@@ -113,18 +113,11 @@ constexpr size_t kSmemSel = kSmemV + 2 * kTileBytes;
 constexpr size_t kSmemBar = kSmemSel + 2 * kMaxSelected * sizeof(int32_t);  // one list per half (dual)
 constexpr size_t kSmemTotal = kSmemBar + sizeof(Barriers) + 1024;  // + alignment slack
 
-// K-major SW128 operand (Q, K): k-step kk (16 elements) lives in d chunk kk/4
-// at byte offset (kk%4)*32 within each 128-byte row; 8-row groups are 1024 B
-// apart (SBO); LBO is unused for swizzled K-major.
-__device__ __forceinline__ uint64_t desc_kmajor(uint32_t tile_addr, int kk) {
-    return umma_desc_sw128(tile_addr + (kk >> 2) * kChunkBytes + (kk & 3) * 32, 16, 1024);
-}
-// MN-major SW128 operand (V as B of P.V): N = d spans the two 64-wide d
-// chunks (LBO = 16 KB apart); K = keys, 8-key groups 1024 B apart (SBO);
-// k-step kk starts 16 keys = 2 KB further.
-__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t tile_addr, int kk) {
-    return umma_desc_sw128(tile_addr + kk * 2048, kChunkBytes, 1024);
-}
+// Operand layouts (the descriptor walk per k-step is in ptx.cuh's mma_tile_*):
+// K-major SW128 Q / K — k-step kk (16 elements) lives in d chunk kk/4 at byte
+// offset (kk%4)*32 within each 128-byte row, 8-row groups 1024 B apart (SBO);
+// MN-major SW128 V as B of P.V — N = d spans the two 64-wide d chunks (LBO =
+// 16 KB apart), K = keys, 8-key groups 1024 B apart, k-step kk 2 KB further.
 
 #ifdef SHPLB_TRACE  // dev-only: per-block clock64 timeline of one CTA, printed at exit
 constexpr int kTraceBlocks = 48;
