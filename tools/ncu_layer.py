@@ -17,7 +17,8 @@ from paper_2603_10353_b200.workload import LayerSpec, make_layer  # noqa: E402
 
 n = int(os.environ.get("TUNE_N", "131072"))
 calls = int(os.environ.get("CALLS", "3"))
-q, k, v = make_layer(LayerSpec(num_q_heads=32, num_kv_heads=8, seq_len=n, seed=2603), "cuda")
+hq, hkv = int(os.environ.get("HQ", "32")), int(os.environ.get("HKV", "8"))  # C4: HQ=28 HKV=4 TUNE_N=65536
+q, k, v = make_layer(LayerSpec(num_q_heads=hq, num_kv_heads=hkv, seq_len=n, seed=2603), "cuda")
 ctx = P.Context(0)
 budgets, info, _ = calibrate.layer_budgets(q, k, 0.25, kind="token", rows=128, ctx=ctx)
 out = torch.empty_like(q)
