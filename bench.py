@@ -315,10 +315,21 @@ def run_layer(ctx, ls, out, stream):
                                stream=stream, q_block_range=ls.ranges, kind=KIND)
 
 
+def board_energy_mj(index):
+    """The board's total energy counter (mJ, NVML), or None."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        return pynvml.nvmlDeviceGetTotalEnergyConsumption(pynvml.nvmlDeviceGetHandleByIndex(index))
+    except Exception:  # noqa: BLE001 - no NVML: the line simply carries no energy
+        return None
+
+
 def time_stack(ctx, shards, steps, warmup, world, stream):
     """K timed steps of the whole stack (every layer's kernels 1-3 back to back
     on one stream, inputs resident). Returns ms per layer, mean per-call stage
-    ms, launches per step, and one output buffer."""
+    ms, launches per step, one output buffer, and the board energy per layer
+    over the timed region (J, NVML; None without it)."""
     import torch
     hmax = max(1, max(len(ls.heads) for ls in shards))
     ref = next((ls.q for ls in shards if ls.heads), shards[0].q)
@@ -338,12 +349,15 @@ def time_stack(ctx, shards, steps, warmup, world, stream):
     ctx.set_timing(True)
     launches0 = ctx.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    mj0 = board_energy_mj(torch.cuda.current_device())
     e0.record(stream)
     for _ in range(steps):
         for ls in shards:
             run_layer(ctx, ls, out[:len(ls.heads)], stream)
     e1.record(stream)
     torch.cuda.synchronize()
+    mj1 = board_energy_mj(torch.cuda.current_device())
+    joules = None if mj0 is None or mj1 is None else (mj1 - mj0) / 1e3 / (steps * len(shards))
     launches = (ctx.launches - launches0) // max(1, steps)
     stages = ctx.read_timing(max_calls=steps * len(shards) + 8)
     ctx.set_timing(False)
@@ -351,7 +365,7 @@ def time_stack(ctx, shards, steps, warmup, world, stream):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / (steps * len(shards))
     st = stages.mean(axis=0) if len(stages) else np.zeros(3)
-    return ms, st, launches, out
+    return ms, st, launches, out, joules
 
 
 def time_stack_gathered(ctx, shards, plans, hq, steps, warmup, world, stream, hp_comm):
@@ -928,13 +942,13 @@ def main():
         sampler = ClockSampler(local) if (name == headline) else None
         if sampler:
             sampler.start()
-        ms, stages, launches, _ = time_stack(ctx, shards, args.steps, args.warmup, world, stream)
+        ms, stages, launches, _, joules = time_stack(ctx, shards, args.steps, args.warmup, world, stream)
         clocks = sampler.stop() if sampler else None
         flops = sum(ls.flops for ls in shards) / L  # per layer, this rank
         per_rank = allgather_float(ms, world)
         per_rank_k3 = allgather_float(float(stages[2]), world)
         res = {"ms": max(per_rank), "per_rank_ms": per_rank, "stages": stages, "launches": launches,
-               "clocks": clocks, "flops_local": flops,
+               "clocks": clocks, "flops_local": flops, "joules": joules,
                "flops_total": sum(allgather_float(flops, world)),
                "bubble": P.barrier(per_rank).bubble_fraction,
                "k3_bubble": P.barrier(per_rank_k3).bubble_fraction,
@@ -1046,6 +1060,14 @@ def main():
         "gpu_launches": g["launches"],
         "clocks": g["clocks"],
     }
+    if g.get("joules"):
+        # This rank's board over the timed region (NVML): under sw_power_cap the
+        # layer time is this energy over the cap.
+        line["energy"] = {"joules_per_layer": round(g["joules"], 3),
+                          "avg_power_w": round(g["joules"] / (g["per_rank_ms"][0] / 1e3), 1),
+                          "pj_per_flop": round(g["joules"] / g["flops_local"] * 1e12, 4),
+                          "what": "board energy (NVML total-energy counter) over the timed region / "
+                                  "layers timed; rank 0's board; pJ per algorithmic FLOP of its layer"}
     if "e2e" in g:
         e2e_ms, h2d, d2h, n_e2e = g["e2e"]
         line["e2e"] = {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": h2d,
