@@ -41,7 +41,7 @@
 // first inside a group, as the hardware scheduler hands out the one-cluster-
 // per-tile kernel's clusters, so the clusters in flight share K/V in L2). The
 // leader's QK producer takes the next tile with an atomic ticket on a
-// per-launch counter (zeroed on the stream before the launch) once a slot is
+// per-launch counter (zero at launch; the launch's last draw resets it) once a slot is
 // free — about one tile ahead of its use — and hands it to the peer CTA
 // through distributed shared memory; a ticket past the list ends the cluster.
 // (A static LPT assignment of tiles to clusters was measured first: it left
@@ -210,6 +210,11 @@ __global__ void __launch_bounds__(kThreads, 1) fa_persist_kernel(const __grid_co
                 if (rank == 0) {
                     if (lane == 0) {
                         ticket = atomicAdd(p.counter, 1);
+                        // Every cluster draws exactly one ticket past the list, so the
+                        // launch's last draw returns the counter to zero for the next
+                        // launch on this ring slot (no memset on the stream: a memset
+                        // runs on a copy engine and queues behind bulk transfers).
+                        if (ticket == p.num_tiles + static_cast<int>(gridDim.x >> 1) - 1) atomicExch(p.counter, 0);
                         asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(peer_tkt + 4u * r.slot), "r"(ticket)
                                      : "memory");
                         asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(

@@ -429,9 +429,11 @@ int k3_variant() {
     return v;
 }
 
-// Tile-ticket counters of the persistent kernel 3: one per launch from a ring,
-// zeroed on the launch's stream, so launches of one context in flight on
-// different streams never share a counter.
+// Tile-ticket counters of the persistent kernel 3: one per launch from a ring
+// (zeroed once; each launch's last ticket draw resets its counter), so launches
+// of one context in flight on different streams never share a counter. No
+// memset per launch: a memset runs on a copy engine and, behind the host-buffer
+// entry's bulk transfers, held kernel 3 back ~50 us per chunk.
 constexpr int kTicketRing = 64;
 
 // block_q = 128: two query blocks per kernel-3 CTA (each with its own selection
@@ -603,10 +605,12 @@ void run_fa(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, const voi
         if (persist) {
             const int maxc = kern::fa_persist_max_clusters();
             if (maxc < 1) throw CudaError("kernel 3 (persistent): no cluster fits on the device");
-            if (!ctx->tickets) SHPLB_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->tickets), kTicketRing * sizeof(int32_t)));
+            if (!ctx->tickets) {  // zero once; every launch leaves its counter at zero again
+                SHPLB_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->tickets), kTicketRing * sizeof(int32_t)));
+                SHPLB_CUDA(cudaMemset(ctx->tickets, 0, kTicketRing * sizeof(int32_t)));
+            }
             p.counter = ctx->tickets + (ctx->ticket_seq++ % kTicketRing);
             p.num_tiles = ctx->current->num_tiles;
-            SHPLB_CUDA(cudaMemsetAsync(p.counter, 0, sizeof(int32_t), st));
             SHPLB_CUDA(kern::launch_fa_persist(p, std::min(maxc, p.num_tiles), st));
         } else {
             kern::launch_fa(p, ctx->current->num_tiles, dual_mode(s), st);
