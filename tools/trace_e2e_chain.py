@@ -2,7 +2,9 @@
 kernels and memcpys from a CUPTI trace (torch.profiler). Prints where the
 compute stream idles between the first and the last kernel (gaps > 20 us, with
 what the copy engines were doing), the H2D / D2H busy time, and the span.
-    python tools/trace_e2e_chain.py [layers]"""
+    python tools/trace_e2e_chain.py [layers] [--device]
+(--device: the same layers from device-resident inputs through the device
+entry, as bench.py's `value` runs them.)"""
 import json
 import os
 import sys
@@ -16,22 +18,30 @@ from paper_2603_10353_b200.workload import LayerSpec, make_layer  # noqa: E402
 
 
 def main():
-    L = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    device = "--device" in sys.argv
+    L = int(args[0]) if args else 4
     n = int(os.environ.get("TRACE_N", "131072"))
     rng = np.random.default_rng(0)
     layers = []
     for li in range(L):
         q, k, v = make_layer(LayerSpec(seq_len=n, seed=2603 + li), "cuda")
         b = (rng.integers(1, 512, 32) * 128).astype(np.int64)
-        layers.append((tuple(t.cpu().pin_memory() for t in (q, k, v)), b))
+        layers.append(((q, k, v) if device else tuple(t.cpu().pin_memory() for t in (q, k, v)), b))
         del q, k, v
-    outs = [torch.empty(layers[0][0][0].shape, dtype=torch.bfloat16).pin_memory() for _ in range(L)]
     ctx = P.Context(0)
     s = torch.cuda.Stream()
+    if device:
+        outs = [torch.empty_like(layers[0][0][0]) for _ in range(L)]
+    else:
+        outs = [torch.empty(layers[0][0][0].shape, dtype=torch.bfloat16).pin_memory() for _ in range(L)]
 
     def step():
         for ((qh, kh, vh), b), o in zip(layers, outs):
-            ctx.sparse_attention_layer_host(qh, kh, vh, b, out=o, stream=s, asynchronous=True)
+            if device:
+                ctx.sparse_attention_layer(qh, kh, vh, b, out=o, stream=s)
+            else:
+                ctx.sparse_attention_layer_host(qh, kh, vh, b, out=o, stream=s, asynchronous=True)
         s.synchronize()
 
     step()
@@ -61,8 +71,8 @@ def main():
                          "after": prev, "before": nm, "short_ops_in_gap": inside})
         if b >= cur:
             cur, prev = b, nm
-    first_h2d = min(a for a, _, k_, _ in ev if k_ == "h2d")
-    last_d2h = max(b for _, b, k_, _ in ev if k_ == "d2h")
+    first_h2d = min((a for a, _, k_, _ in ev if k_ == "h2d"), default=t0)
+    last_d2h = max((b for _, b, k_, _ in ev if k_ == "d2h"), default=t1)
     busy = lambda kind: sum(b - a for a, b, k_, _ in ev if k_ == kind) / 1e3  # noqa: E731
     print(json.dumps({"layers": L, "span_ms": round((last_d2h - first_h2d) / 1e3, 3),
                       "kernel_span_ms": round((t1 - t0) / 1e3, 3),
