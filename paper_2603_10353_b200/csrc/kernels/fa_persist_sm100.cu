@@ -71,7 +71,21 @@ constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 0, kColP = 128, kColO = 256;  // P_w at kColP + 64 w, O_w at kColO + 128 w
 constexpr uint32_t kIdescS = idesc_bf16_f32(256, 128, 0, 0);   // Q K-major, K K-major
 constexpr uint32_t kIdescPV = idesc_bf16_f32(256, 128, 0, 1);  // P (TMEM), V MN-major
-constexpr float kRescaleThreshold = 8.0f;
+// Lazy rescale: a warpgroup's reference m moves only when a block's max exceeds
+// it by more than 2^kRescaleThreshold. P is bf16 and l / O are fp32, so P up to
+// 2^32 costs no precision (only the 2^8 of fp16-P kernels would overflow); the
+// high threshold lets almost every block skip its row max: P is exponentiated
+// against m first, and a block sum <= 2^32 proves every P <= 2^32, i.e. the max
+// rule would keep m too. Only otherwise (or at a row's first block, or a sum
+// that overflowed to +inf) is the max taken, and P recomputed if m moves.
+// C3: 64 FMNMX3 per 128 scores saved, kernel 3 ~1.3% faster under the power
+// cap (profiles/r02/k3_spec_max_ab.txt). SHPLB_EXACT_MAX (diagnostic) takes
+// every block's max; SHPLB_RESCALE_LOG2 sets the threshold.
+#ifndef SHPLB_RESCALE_LOG2
+#define SHPLB_RESCALE_LOG2 32
+#endif
+constexpr float kRescaleThreshold = static_cast<float>(SHPLB_RESCALE_LOG2);
+constexpr float kRescaleSum = static_cast<float>(1ull << SHPLB_RESCALE_LOG2);
 constexpr int kWarpQK = 8, kWarpS = 9, kWarpV = 10;  // 11: the P·V issuer
 // sel_empty arrivals per tile: V producer, S and P·V issuer warps (which on
 // the peer only keep the slot phases), 8 softmax warps.
@@ -487,6 +501,37 @@ __global__ void __launch_bounds__(kThreads, 1) fa_persist_kernel(const __grid_co
                     for (int c = 0; c < kBlock; ++c)
                         if (key0 + c > lim) s[c] = -INFINITY;
                 }
+                // P = 2^(s*scale - m), its row sum, packed bf16 pairs.
+                float2 sum2[2];
+                uint32_t pk[4][16];
+                auto exps = [&](float msub) {
+                    const float2 nm2 = make_float2(-msub, -msub);
+                    sum2[0] = sum2[1] = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int e = 0; e < kBlock / 2; ++e) {
+                        const float2 x = ffma2(make_float2(s[2 * e], s[2 * e + 1]), sc2, nm2);
+                        float2 pe;
+#ifdef SHPLB_DIAG_NOEXP  // dev-only energy/timing diagnostic (wrong results): no MUFU
+                        pe = x;
+#else
+                        pe.x = ex2(x.x);
+                        pe.y = ex2(x.y);
+#endif
+                        sum2[e & 1] = fadd2(sum2[e & 1], pe);
+                        pk[e >> 4][e & 15] = pack_bf16x2(pe.x, pe.y);
+                    }
+                };
+                const float mprev = m;
+#ifndef SHPLB_EXACT_MAX
+                // Exponentiate against the current m first (see kRescaleThreshold).
+                bool need_max = m == -INFINITY;
+                if (!need_max) {
+                    exps(m);
+                    const float2 sp = fadd2(sum2[0], sum2[1]);
+                    need_max = !(sp.x + sp.y <= kRescaleSum);  // also +inf / NaN
+                }
+                if (need_max) {
+#endif
                 float mx8[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) mx8[e] = -INFINITY;
@@ -494,27 +539,15 @@ __global__ void __launch_bounds__(kThreads, 1) fa_persist_kernel(const __grid_co
                 for (int c = 0; c < kBlock; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], s[c]);
                 const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * sl2;
-                // Lazy rule: raise m only when the block max exceeds it by > 2^8.
-                const float mprev = m;
+                // Lazy rule: raise m only when the block max exceeds it by > 2^kRescaleThreshold.
                 if (mx > m + kRescaleThreshold || (m == -INFINITY && mx > -INFINITY)) m = mx;
-                const bool rose = m != mprev && mprev != -INFINITY;
-                const float msub = (m == -INFINITY) ? 0.0f : m;
-                const float2 nm2 = make_float2(-msub, -msub);
-                float2 sum2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-                uint32_t pk[4][16];
-#pragma unroll
-                for (int e = 0; e < kBlock / 2; ++e) {
-                    const float2 x = ffma2(make_float2(s[2 * e], s[2 * e + 1]), sc2, nm2);
-                    float2 pe;
-#ifdef SHPLB_DIAG_NOEXP  // dev-only energy/timing diagnostic (wrong results): no MUFU
-                    pe = x;
-#else
-                    pe.x = ex2(x.x);
-                    pe.y = ex2(x.y);
-#endif
-                    sum2[e & 1] = fadd2(sum2[e & 1], pe);
-                    pk[e >> 4][e & 15] = pack_bf16x2(pe.x, pe.y);
+#ifndef SHPLB_EXACT_MAX
+                if (m != mprev || mprev == -INFINITY) exps(m == -INFINITY ? 0.0f : m);
                 }
+#else
+                exps(m == -INFINITY ? 0.0f : m);
+#endif
+                const bool rose = m != mprev && mprev != -INFINITY;
                 // This warpgroup's previous P·V in this tile (which read P_w and
                 // accumulated into O_w) must be done before P_w is rewritten and
                 // O_w rescaled; the first block of a tile follows the previous

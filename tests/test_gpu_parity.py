@@ -431,6 +431,30 @@ def test_zero_q_gives_uniform_weights_over_kept_keys(cuda_ctx):
     check_output(out[0], ref, "zero q")
 
 
+@pytest.mark.parametrize("bq", [256, 128])
+@pytest.mark.parametrize("gain", [3.0, 12.0, 60.0])
+def test_score_jumps_between_blocks(cuda_ctx, gain, bq):
+    """Later key blocks score far above the first kept one (K of every third
+    block scaled by `gain`): the running max of a row must move — kernel 3's
+    lazy rescale (and, for jumps past 2^32 or to +inf in fp32, its exact-max
+    fallback) — and the output still match the fp64 kept-set softmax."""
+    n = 2048
+    spec = LayerSpec(num_q_heads=2, num_kv_heads=1, seq_len=n, seed=int(gain) + bq)
+    q, k, v = make_layer(spec, "cpu")
+    k = k.float()
+    for b in range(1, n // 128, 3):
+        k[:, b * 128:(b + 1) * 128] *= gain
+    k = k.to(torch.bfloat16)
+    qb, kb, vb = bf16_bits(q), bf16_bits(k), bf16_bits(v)
+    k_blocks = np.array([6, 16], np.int64)
+    _, idx_o, cnt_o, out_o = O.layer(qb, kb, vb, k_blocks, bq=bq, causal=True, kmax=16)
+    out = cuda_ctx.sparse_attention_layer(q.cuda(), k.cuda(), v.cuda(), k_blocks * 128, causal=True, block_q=bq)
+    torch.cuda.synchronize()
+    idx, cnt = cuda_ctx.last_selection(2, n)
+    assert np.array_equal(cnt.cpu().numpy(), cnt_o) and np.array_equal(idx.cpu().numpy(), idx_o)
+    check_output(out, out_o, f"score jumps x{gain}")
+
+
 @pytest.mark.parametrize("group", ["1", "3"])
 def test_kernel2_group_sizes(group):
     """Kernel 2 scores up to 4 q heads of one kv head per CTA (64 row slots =
