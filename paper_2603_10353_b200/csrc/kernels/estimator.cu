@@ -35,12 +35,9 @@ constexpr int kPoolThreads = 256;  // 16 row groups x 16 column groups of 8 colu
 // (all kRows/16 loads in flight); the 16 group partials per column are then
 // added in ascending group order.
 template <int kRows>
-__global__ void __launch_bounds__(kPoolThreads) pool_kernel(const __nv_bfloat16* __restrict__ x,
-                                                            int64_t n, float* __restrict__ out) {
-    __shared__ float part[kPoolSplit][kHeadDim + 4];
-    const int64_t b = blockIdx.x;
-    const int64_t head = blockIdx.y;
-    const int64_t nb = gridDim.x;
+__device__ __forceinline__ void pool_block(const __nv_bfloat16* __restrict__ x, int64_t n, int64_t head,
+                                           int64_t b, int64_t nb, float* __restrict__ out,
+                                           float (&part)[kPoolSplit][kHeadDim + 4]) {
     const int g = threadIdx.x >> 4;
     const int cg = threadIdx.x & 15;
     const int64_t t0 = b * kRows;
@@ -78,6 +75,21 @@ __global__ void __launch_bounds__(kPoolThreads) pool_kernel(const __nv_bfloat16*
         for (int gg = 0; gg < kPoolSplit; ++gg) total = __fadd_rn(total, part[gg][c]);
         out[(head * nb + b) * kHeadDim + c] = __fdiv_rn(total, static_cast<float>(cnt));
     }
+}
+
+// Q (kRowsQ-row blocks) and K (kBlock-row blocks) of a layer in one launch: the
+// first nbq * hq CTAs pool Q, the rest K (one launch and one tail per layer
+// call instead of one per tensor).
+template <int kRowsQ>
+__global__ void __launch_bounds__(kPoolThreads) pool_qk_kernel(const __nv_bfloat16* __restrict__ q, int64_t nbq,
+                                                               int hq, const __nv_bfloat16* __restrict__ k,
+                                                               int64_t nbk, int64_t n, float* __restrict__ qp,
+                                                               float* __restrict__ kp) {
+    __shared__ float part[kPoolSplit][kHeadDim + 4];
+    const int64_t id = blockIdx.x;
+    const int64_t nq = nbq * hq;
+    if (id < nq) pool_block<kRowsQ>(q, n, id / nbq, id % nbq, nbq, qp, part);
+    else pool_block<kBlock>(k, n, (id - nq) / nbk, (id - nq) % nbk, nbk, kp, part);
 }
 
 // Key blocks (of kBlock keys) visible to query block qb of bq rows.
@@ -415,13 +427,16 @@ __global__ void check_finite_kernel(const uint16_t* __restrict__ x, int64_t coun
 
 }  // namespace
 
-void launch_pool(const void* x, int heads, int64_t n, int rows, float* out, cudaStream_t s) {
-    const int64_t nb = (n + rows - 1) / rows;
-    const dim3 grid(static_cast<unsigned>(nb), heads);
-    if (rows == 256)
-        pool_kernel<256><<<grid, kPoolThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(x), n, out);
+void launch_pool_qk(const void* q, int hq, int bq, const void* k, int hkv, int64_t n, float* qp, float* kp,
+                    cudaStream_t s) {
+    const int64_t nbq = (n + bq - 1) / bq, nbk = (n + kBlock - 1) / kBlock;
+    const unsigned grid = static_cast<unsigned>(nbq * hq + nbk * hkv);
+    const auto* qb = static_cast<const __nv_bfloat16*>(q);
+    const auto* kb = static_cast<const __nv_bfloat16*>(k);
+    if (bq == 256)
+        pool_qk_kernel<256><<<grid, kPoolThreads, 0, s>>>(qb, nbq, hq, kb, nbk, n, qp, kp);
     else
-        pool_kernel<128><<<grid, kPoolThreads, 0, s>>>(static_cast<const __nv_bfloat16*>(x), n, out);
+        pool_qk_kernel<128><<<grid, kPoolThreads, 0, s>>>(qb, nbq, hq, kb, nbk, n, qp, kp);
 }
 
 int launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n, int bq,

@@ -32,15 +32,15 @@ struct GroupTable {
     uint8_t size[kMaxHeads];    // heads in the group (1..4)
 };
 
-// Kernel 1: x [heads][n][128] bf16 -> out [heads][ceil(n/rows)][128] fp32 block means
-// (rows = 128 or 256).
-void launch_pool(const void* x, int heads, int64_t n, int rows, float* out, cudaStream_t s);
-
 // Kernel 2 (fused score + select): pooled q [hq][nqb][128], pooled k
 // [hkv][nkb][128]; q head h scores against pooled kv head ht.kv[h]. scores_out (nullable) receives the full score matrix
 // [hq][nqb][nkb] (-inf where causally invisible); otherwise the scores go to
 // scores_ws (hq*nqb*nkb floats, contents undefined after). With select=true,
 // idx/cnt receive the per-(head, q block) top-k block lists.
+// Kernel 1: Q [hq][n][128] and K [hkv][n][128] bf16 -> qp [hq][ceil(n/bq)][128] and
+// kp [hkv][ceil(n/128)][128] fp32 block means (bq = 128 or 256), one launch.
+void launch_pool_qk(const void* q, int hq, int bq, const void* k, int hkv, int64_t n, float* qp, float* kp,
+                    cudaStream_t s);
 int launch_score_select(const float* qp, const float* kp, int hq, int hkv, int64_t n, int bq,
                          bool causal, float scale, const HeadTable& ht, int64_t kmax,
                          float* scores_out, float* scores_ws, bool select, int32_t* idx, int32_t* cnt,

@@ -379,8 +379,7 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
     if (select) mark(ctx, 0, st);
     {
         Nvtx r("shplb.k1_pool");
-        kern::launch_pool(q, s->num_q_heads, s->seq_len, s->block_q, ctx->qp, st);
-        kern::launch_pool(k, s->num_kv_heads, s->seq_len, kern::kBlock, ctx->kp, st);
+        kern::launch_pool_qk(q, s->num_q_heads, s->block_q, k, s->num_kv_heads, s->seq_len, ctx->qp, ctx->kp, st);
     }
     if (select) mark(ctx, 1, st);
     Nvtx r2("shplb.k2_score_select");
@@ -393,13 +392,13 @@ void pool_and_score(shplb_ctx* ctx, const shplb_layer_shape* s, const void* q, c
                                   s->causal != 0, scale, kb, kmax, ws, nullptr, false, nullptr, nullptr, st);
         kern::launch_colagg_select(ws, s->num_q_heads, s->seq_len, s->block_q, s->causal != 0, kb, kmax,
                                    ws + n_scores, ctx->ca_kept, idx, cnt, st);
-        check_launch(ctx, 3 + 4);
+        check_launch(ctx, 2 + 4);
     } else {
         if (!scores_out) grow(ctx->k2_ws, ctx->k2_ws_bytes, sizeof(float) * s->num_q_heads * nqb * nkb);
         const int k2 = kern::launch_score_select(ctx->qp, ctx->kp, s->num_q_heads, s->num_kv_heads, s->seq_len,
                                                  s->block_q, s->causal != 0, scale, kb, kmax, scores_out, ctx->k2_ws,
                                                  select, idx, cnt, st);
-        check_launch(ctx, 2 + k2);
+        check_launch(ctx, 1 + k2);
     }
     if (select) mark(ctx, 2, st);
 }
