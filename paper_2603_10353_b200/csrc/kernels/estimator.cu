@@ -30,66 +30,83 @@ namespace {
 
 constexpr int kPoolThreads = 256;  // 16 row groups x 16 column groups of 8 columns
 
-// One CTA pools one kRows-row block (128 or 256) of one head. Thread (g, cg)
-// sums rows g, g+16, ... (ascending) of columns 8cg..8cg+7 with 16-byte loads
-// (all kRows/16 loads in flight); the 16 group partials per column are then
-// added in ascending group order.
-template <int kRows>
-__device__ __forceinline__ void pool_block(const __nv_bfloat16* __restrict__ x, int64_t n, int64_t head,
-                                           int64_t b, int64_t nb, float* __restrict__ out,
-                                           float (&part)[kPoolSplit][kHeadDim + 4]) {
+// One CTA pools kRows rows (128 or 256) of one head into kSub output blocks of
+// kRows / kSub rows each. Thread (g, cg) sums rows g, g+16, ... (ascending) of
+// columns 8cg..8cg+7 of each output block with 16-byte loads (all kRows/16 loads
+// in flight); the 16 group partials per column are then added in ascending
+// group order — per output block the same additions in the same order whatever
+// kSub, so pooled values do not depend on how blocks are packed into CTAs.
+template <int kRows, int kSub>
+__device__ __forceinline__ void pool_rows(const __nv_bfloat16* __restrict__ x, int64_t n, int64_t head,
+                                          int64_t b0, int64_t nb, float* __restrict__ out,
+                                          float (&part)[kSub][kPoolSplit][kHeadDim + 4]) {
+    constexpr int kLoads = kRows / kPoolSplit, kPerSub = kLoads / kSub, kSubRows = kRows / kSub;
     const int g = threadIdx.x >> 4;
     const int cg = threadIdx.x & 15;
-    const int64_t t0 = b * kRows;
+    const int64_t t0 = b0 * kSubRows;  // b0: first output block of this CTA
     const int cnt = static_cast<int>(min(static_cast<int64_t>(kRows), n - t0));
     const __nv_bfloat16* base = x + (head * n + t0) * kHeadDim + cg * 8;
 
-    uint4 v[kRows / kPoolSplit];
+    uint4 v[kLoads];
 #pragma unroll
-    for (int s = 0; s < kRows / kPoolSplit; ++s) {
+    for (int s = 0; s < kLoads; ++s) {
         const int t = g + s * kPoolSplit;
         v[s] = t < cnt ? __ldg(reinterpret_cast<const uint4*>(base + static_cast<int64_t>(t) * kHeadDim))
                        : make_uint4(0, 0, 0, 0);
     }
-    float acc[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+    for (int j = 0; j < kSub; ++j) {
+        float acc[8];
 #pragma unroll
-    for (int s = 0; s < kRows / kPoolSplit; ++s) {
-        if (g + s * kPoolSplit < cnt) {
-            const uint32_t w[4] = {v[s].x, v[s].y, v[s].z, v[s].w};
+        for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                acc[2 * e] = __fadd_rn(acc[2 * e], __uint_as_float(w[e] << 16));
-                acc[2 * e + 1] = __fadd_rn(acc[2 * e + 1], __uint_as_float(w[e] & 0xFFFF0000u));
+        for (int s = j * kPerSub; s < (j + 1) * kPerSub; ++s) {
+            if (g + s * kPoolSplit < cnt) {
+                const uint32_t w[4] = {v[s].x, v[s].y, v[s].z, v[s].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    acc[2 * e] = __fadd_rn(acc[2 * e], __uint_as_float(w[e] << 16));
+                    acc[2 * e + 1] = __fadd_rn(acc[2 * e + 1], __uint_as_float(w[e] & 0xFFFF0000u));
+                }
             }
         }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) part[j][g][cg * 8 + e] = acc[e];
     }
-#pragma unroll
-    for (int e = 0; e < 8; ++e) part[g][cg * 8 + e] = acc[e];
     __syncthreads();
-    if (threadIdx.x < kHeadDim) {
-        const int c = threadIdx.x;
-        float total = 0.0f;
+    if (threadIdx.x < kSub * kHeadDim) {
+        const int j = threadIdx.x / kHeadDim, c = threadIdx.x % kHeadDim;
+        const int cj = min(kSubRows, cnt - j * kSubRows);  // rows of output block b0 + j
+        if (cj > 0) {
+            float total = 0.0f;
 #pragma unroll
-        for (int gg = 0; gg < kPoolSplit; ++gg) total = __fadd_rn(total, part[gg][c]);
-        out[(head * nb + b) * kHeadDim + c] = __fdiv_rn(total, static_cast<float>(cnt));
+            for (int gg = 0; gg < kPoolSplit; ++gg) total = __fadd_rn(total, part[j][gg][c]);
+            out[(head * nb + b0 + j) * kHeadDim + c] = __fdiv_rn(total, static_cast<float>(cj));
+        }
     }
 }
 
-// Q (kRowsQ-row blocks) and K (kBlock-row blocks) of a layer in one launch: the
-// first nbq * hq CTAs pool Q, the rest K (one launch and one tail per layer
-// call instead of one per tensor).
+// Kernel 1: Q and K of a layer in one launch. The first nbq * hq CTAs pool Q
+// (one kRowsQ-row block each), the rest K — at kRowsQ = 256 two 128-row key
+// blocks per CTA, so both halves of the grid have the same shape and register
+// footprint (a 128-row K CTA at the Q path's ~95 registers would run at half
+// the occupancy it needs).
 template <int kRowsQ>
 __global__ void __launch_bounds__(kPoolThreads) pool_qk_kernel(const __nv_bfloat16* __restrict__ q, int64_t nbq,
                                                                int hq, const __nv_bfloat16* __restrict__ k,
                                                                int64_t nbk, int64_t n, float* __restrict__ qp,
                                                                float* __restrict__ kp) {
-    __shared__ float part[kPoolSplit][kHeadDim + 4];
+    constexpr int kSubK = kRowsQ / kBlock;
+    __shared__ float part[kSubK][kPoolSplit][kHeadDim + 4];
     const int64_t id = blockIdx.x;
     const int64_t nq = nbq * hq;
-    if (id < nq) pool_block<kRowsQ>(q, n, id / nbq, id % nbq, nbq, qp, part);
-    else pool_block<kBlock>(k, n, (id - nq) / nbk, (id - nq) % nbk, nbk, kp, part);
+    if (id < nq) {
+        pool_rows<kRowsQ, 1>(q, n, id / nbq, id % nbq, nbq, qp,
+                             *reinterpret_cast<float(*)[1][kPoolSplit][kHeadDim + 4]>(&part[0]));
+    } else {
+        const int64_t ck = (nbk + kSubK - 1) / kSubK;  // K CTAs per head
+        pool_rows<kRowsQ, kSubK>(k, n, (id - nq) / ck, ((id - nq) % ck) * kSubK, nbk, kp, part);
+    }
 }
 
 // Key blocks (of kBlock keys) visible to query block qb of bq rows.
@@ -430,7 +447,8 @@ __global__ void check_finite_kernel(const uint16_t* __restrict__ x, int64_t coun
 void launch_pool_qk(const void* q, int hq, int bq, const void* k, int hkv, int64_t n, float* qp, float* kp,
                     cudaStream_t s) {
     const int64_t nbq = (n + bq - 1) / bq, nbk = (n + kBlock - 1) / kBlock;
-    const unsigned grid = static_cast<unsigned>(nbq * hq + nbk * hkv);
+    const int64_t ck = (nbk + bq / kBlock - 1) / (bq / kBlock);  // K CTAs per head
+    const unsigned grid = static_cast<unsigned>(nbq * hq + ck * hkv);
     const auto* qb = static_cast<const __nv_bfloat16*>(q);
     const auto* kb = static_cast<const __nv_bfloat16*>(k);
     if (bq == 256)
