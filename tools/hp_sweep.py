@@ -78,12 +78,14 @@ def main():
     print(json.dumps({"kind": "budget_table", **base}), flush=True)
     for D in cfg["devices"]:
         rows = {}
-        plans = {"naive": P.naive_assign(budgets, D), "greedy": P.greedy_assign(budgets, D)}
+        wc = P.tile_costs(budgets, n, query_tile_weight=P.api.QUERY_TILE_WEIGHT)
+        plans = {"naive": P.naive_assign(budgets, D), "greedy": P.greedy_assign(budgets, D),
+                 "greedy_refined": P.refine_assign(wc, D, P.greedy_assign(wc, D))}
         for name, plan in plans.items():
             per = [shard_time(ctx, q, k, v, rank_shard(plan, r, group, budgets), a.steps)
                    for r in range(D)]
             rows[name] = (per, float(P.imbalance(budgets, plan, D).imbalance))
-        sp = P.split_assign(budgets, D, n)
+        sp = P.split_assign(budgets, D, n, query_tile_weight=P.api.QUERY_TILE_WEIGHT)
         per = []
         for r in range(D):
             seg = rank_segments(sp, r, group, budgets)
