@@ -554,6 +554,30 @@ def test_single_cta_kernel3_variant():
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
+def test_ticket_ring_reuse_over_many_launches(cuda_ctx):
+    """The persistent kernel 3 takes tiles with a per-launch ticket counter from
+    a ring of 64 and resets it itself (its last draw): 150 launches with three
+    different tile counts, alternating between two (ordered) streams, wrap the
+    ring twice; every output equals a fresh context's."""
+    spec = LayerSpec(num_q_heads=4, num_kv_heads=2, seq_len=1536, seed=12)
+    q, k, v = (t.cuda() for t in make_layer(spec, "cpu"))
+    tables = [np.array(b, np.int64) for b in ([128, 256, 384, 512], [1536, 128, 640, 256], [768, 768, 768, 768])]
+    fresh = P.Context(0)
+    want = [fresh.sparse_attention_layer(q, k, v, b) for b in tables]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    for i in range(150):
+        s_ = streams[i % 2]
+        with torch.cuda.stream(s_):
+            outs.append((i % 3, cuda_ctx.sparse_attention_layer(q, k, v, tables[i % 3], stream=s_)))
+        streams[(i + 1) % 2].wait_stream(s_)  # the context's workspace is shared: keep the launches ordered
+    torch.cuda.synchronize()
+    for t, o in outs:
+        assert torch.equal(o, want[t])
+    fresh.close()
+
+
 def test_work_list_cache_eviction(monkeypatch):
     """Kernel-3 work lists are LRU-evicted (SHPLB_WORKLIST_CACHE entries) with
     stream-ordered frees: cycling more distinct budget tables than the cache
